@@ -1,0 +1,189 @@
+/*
+ * tio.h — C ABI of libtio, the B200 (sm_100a) lifetime / plan / migration
+ * hot path.  Plain pointers and sizes only; no torch types.
+ *
+ * The reference (`offloader`, pure Python) has no FFI: its boundary is the
+ * module API re-exported by pkg/src/offloader/__init__.py:4-65.  Each entry
+ * point below names the reference function(s) it replaces; the Python shim
+ * paper_2506_06472_b200/ (and INTEGRATION.md's ctypes stub) binds them with
+ * the reference's names, argument meaning and exceptions.
+ *
+ * Conventions
+ *   - return value: TIO_OK (0) or a negative TIO_ERR_* code; the message of
+ *     the last failure on the calling thread is available via tio_last_error.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *   - memory kinds: TIO_MEM_HOST (pageable or pinned host pointers; copied to
+ *     the device inside the call) or TIO_MEM_DEVICE (device pointers, used in
+ *     place, must stay valid for the lifetime of the handle).
+ *   - handles are opaque, owned by the library, freed with *_destroy.
+ *   - integers are int64 (times in microseconds, sizes in bytes); the
+ *     reference uses unbounded Python ints, callers must stay inside int64.
+ */
+#ifndef TIO_H_
+#define TIO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TIO_ABI_VERSION 1
+
+enum {
+    TIO_OK = 0,
+    TIO_ERR_INVALID = -1,        /* bad argument / handle (ValueError)                 */
+    TIO_ERR_UNSATISFIABLE = -2,  /* planner.py:59-66 UnsatisfiableTraceError           */
+    TIO_ERR_CHANNEL_CONFIG = -3, /* bandwidth.py:27-28 ChannelConfigError              */
+    TIO_ERR_CUDA = -4,           /* CUDA runtime failure                               */
+    TIO_ERR_NOMEM = -5,
+    TIO_ERR_INTERNAL = -6,       /* planner.py:316-320 divergence assert / invariant   */
+    TIO_ERR_OVERFLOW = -7,       /* value outside the int64 domain                     */
+    TIO_ERR_SIMULATION = -8      /* simulator.py:51-52 SimulationError                 */
+};
+
+enum { TIO_MEM_HOST = 0, TIO_MEM_DEVICE = 1 };
+enum { TIO_KIND_INTERMEDIATE = 0, TIO_KIND_GLOBAL = 1 };
+enum { TIO_DEST_NONE = 0, TIO_DEST_SSD = 1, TIO_DEST_CPU = 2 };
+
+/* Column form of a trace (reference Trace, trace.py:87-110).  accesses of
+ * tensor i are accesses[access_ptr[i] .. access_ptr[i+1]).  The trace must
+ * satisfy validate_trace (trace.py:125-157); the library re-checks the
+ * invariants its kernels depend on and fails with TIO_ERR_INVALID. */
+typedef struct tio_trace_desc {
+    int64_t num_kernels;
+    const int64_t *duration_us;   /* [num_kernels]      */
+    int64_t num_tensors;
+    const int64_t *tensor_id;     /* [num_tensors]      */
+    const int64_t *size_bytes;    /* [num_tensors]      */
+    const int8_t *kind;           /* [num_tensors]      */
+    const int64_t *access_ptr;    /* [num_tensors + 1]  */
+    int64_t num_events;
+    const int32_t *accesses;      /* [num_events] kernel indices */
+} tio_trace_desc;
+
+typedef struct tio_trace tio_trace;
+typedef struct tio_plan tio_plan;
+
+/* ChannelRates (bandwidth.py:178-214); rates in bytes/us, may be fractional
+ * (durations use the exact binary value, like Fraction(float)). */
+typedef struct tio_rates {
+    double ssd_offload;
+    double ssd_prefetch;
+    int has_host;
+    double host_offload;
+    double host_prefetch;
+} tio_rates;
+
+/* Device views of the lifetime products (owned by the trace handle). */
+typedef struct tio_lifetime_view {
+    int64_t num_kernels, num_tensors, num_periods;
+    int64_t iteration_us;          /* trace.py:106-107                         */
+    const int64_t *starts;         /* [N+1] kernel start times, starts[N]=iter */
+    const int64_t *timeline;       /* [N]   analysis.py:97-108                 */
+    const int64_t *active;         /* [N]   analysis.py:111-117                */
+    /* inactive periods in reference order (analysis.py:58-83) */
+    const int64_t *period_tensor;  /* [P] tensor position in the trace         */
+    const int32_t *period_start;   /* [P] start_kernel                         */
+    const int32_t *period_end;     /* [P] end_kernel                           */
+    const int8_t *period_wraps;    /* [P]                                      */
+    const int64_t *tensor_period_ptr; /* [T+1] first period of each tensor     */
+} tio_lifetime_view;
+
+/* Summary of a finished plan. */
+typedef struct tio_plan_info {
+    int64_t num_commits;           /* rounds that committed (planner.py:336)  */
+    int64_t num_entries;           /* 2 * num_commits                          */
+    int64_t num_over;              /* over_capacity_kernels count              */
+    int64_t capacity_bytes;
+    int64_t residual_peak_bytes;   /* MemoryTimeline.peak()                    */
+    int64_t planned_host_bytes;    /* planner.py:354-358                       */
+    int64_t num_candidates;        /* inactive periods considered              */
+    int64_t rounds;                /* evaluation rounds run on the device      */
+    int64_t unsat_kernel;          /* set when TIO_ERR_UNSATISFIABLE           */
+    int64_t unsat_bytes;
+} tio_plan_info;
+
+/* One CommittedMigration (planner.py:97-111), commit order.  Relieved
+ * kernels are up to two ranges [lo,hi] (tail, then head for wrap periods);
+ * an empty range has lo > hi.  benefit = (benefit_hi << 64) | benefit_lo. */
+typedef struct tio_commit {
+    int64_t tensor_id;
+    int64_t tensor_pos;
+    int64_t start_kernel, end_kernel;
+    int64_t wraps;
+    int64_t destination;           /* TIO_DEST_SSD / TIO_DEST_CPU              */
+    int64_t off_start, off_end, pre_start, pre_end;
+    uint64_t benefit_lo, benefit_hi;
+    int64_t cost;
+    int64_t rel0_lo, rel0_hi, rel1_lo, rel1_hi;
+} tio_commit;
+
+/* One PlanEntry (planner.py:69-76), plan order (sorted, urgent marked). */
+typedef struct tio_entry {
+    int64_t tensor_id;
+    int64_t tensor_pos;
+    int64_t trigger_us;
+    int64_t deadline_us;
+    int32_t action;                /* 0 offload, 1 prefetch                    */
+    int32_t target;                /* TIO_DEST_SSD / TIO_DEST_CPU; 0 = GPU     */
+    int32_t urgent;
+    int32_t pad;
+} tio_entry;
+
+int tio_abi_version(void);
+/* Copies the last error message of this thread (NUL-terminated, truncated). */
+int tio_last_error(char *buf, size_t len);
+/* Loaded-code identification: device name, SM count, build arch. */
+int tio_device_info(char *buf, size_t len);
+
+/* ---- trace (replaces building a Trace + Trace.kernel_start_times) ------- */
+int tio_trace_create(const tio_trace_desc *desc, int mem_kind, void *stream, tio_trace **out);
+int tio_trace_destroy(tio_trace *t);
+
+/* ---- lifetime stage --------------------------------------------------------
+ * Replaces analysis.py:58-117 (compute_inactive_periods,
+ * compute_memory_timeline, per_kernel_active_bytes) and trace.py:97-107.
+ * Enqueues the lifetime kernels on `stream`; tio_lifetime_view synchronises
+ * the stream and returns device pointers (valid until the next call or
+ * destroy). */
+int tio_lifetime(tio_trace *t, void *stream);
+int tio_lifetime_view_get(tio_trace *t, void *stream, tio_lifetime_view *out);
+/* Copy lifetime products to host buffers (any may be NULL). */
+int tio_lifetime_copy_out(tio_trace *t, void *stream, int64_t *starts, int64_t *timeline,
+                          int64_t *active, int64_t *period_tensor, int32_t *period_start,
+                          int32_t *period_end, int8_t *period_wraps);
+
+/* ---- planner -----------------------------------------------------------------
+ * Replaces planner.py:267-370 plan_migrations (+ mark_urgent :373-397).
+ * Runs the lifetime stage first if it has not run.  Returns
+ * TIO_ERR_UNSATISFIABLE (info.unsat_kernel/unsat_bytes set, no plan handle)
+ * when some kernel's active bytes exceed capacity, TIO_ERR_CHANNEL_CONFIG for
+ * a non-positive rate. */
+int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap,
+                    void *stream, tio_plan **out, tio_plan_info *info);
+int tio_plan_info_get(tio_plan *p, tio_plan_info *out);
+/* Host copies: commits[num_commits], entries[num_entries], residual[N],
+ * over[num_over]; any may be NULL. */
+int tio_plan_copy_out(tio_plan *p, void *stream, tio_commit *commits, tio_entry *entries,
+                      int64_t *residual, int64_t *over);
+/* write_plan (planner.py:402-420), byte-identical.  Call with buf=NULL to get
+ * the size in *len; then with a buffer of that size. */
+int tio_plan_write(tio_plan *p, void *stream, char *buf, size_t *len);
+int tio_plan_destroy(tio_plan *p);
+
+/* One-shot end-to-end call (the e2e bench leg): host trace in, host plan
+ * entries out.  Equivalent to trace_create(HOST) + plan_create + copy_out. */
+int tio_plan_host(const tio_trace_desc *desc, int64_t capacity, const tio_rates *rates,
+                  int64_t host_cap, void *stream, tio_plan_info *info,
+                  tio_entry *entries, int64_t entries_cap);
+
+/* ---- channel primitives (bandwidth.py:75-84) ------------------------------- */
+/* ceil(nbytes / rate) exactly; TIO_ERR_CHANNEL_CONFIG for rate <= 0. */
+int tio_transfer_duration(double rate, int64_t nbytes, int64_t *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TIO_H_ */

@@ -1,0 +1,615 @@
+// capi.cu — the C ABI of libtio (include/tio.h): handle management and the
+// orchestration of the lifetime / planner kernels on a caller stream.
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "lifetime.cuh"
+#include "planner.cuh"
+#include "plan_setup.cuh"
+#include "radix_sort.cuh"
+#include "scan.cuh"
+
+namespace tio {
+
+static thread_local char g_err[1024];
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+// Stream-ordered device allocations owned by a handle.
+struct Arena {
+    std::vector<void *> ptrs;
+    cudaStream_t stream = nullptr;
+    template <typename T>
+    int alloc(T **out, int64_t n) {
+        void *p = nullptr;
+        size_t bytes = sizeof(T) * (size_t)(n > 0 ? n : 1);
+        cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+        if (e != cudaSuccess) return fail(TIO_ERR_NOMEM, "cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
+        ptrs.push_back(p);
+        *out = static_cast<T *>(p);
+        return TIO_OK;
+    }
+    void release() {
+        for (void *p : ptrs) cudaFreeAsync(p, stream);
+        ptrs.clear();
+    }
+};
+
+static int ensure_pool() {
+    static bool done = false;
+    if (done) return TIO_OK;
+    int dev = 0;
+    TIO_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    TIO_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thresh = UINT64_MAX;  // keep freed blocks for reuse across plans
+    TIO_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    done = true;
+    return TIO_OK;
+}
+
+// Decode a rate into the exact integer form used by duration_of.
+static int decode_rate(double rate, RateCode *rc) {
+    memset(rc, 0, sizeof(*rc));
+    if (!(rate > 0) || std::isnan(rate) || std::isinf(rate))
+        return fail(TIO_ERR_CHANNEL_CONFIG, "rate must be > 0");
+    if (rate == std::floor(rate)) {
+        if (rate >= 9223372036854775808.0) { rc->huge = 1; rc->num = 1; return TIO_OK; }
+        rc->num = (int64_t)rate;
+        return TIO_OK;
+    }
+    int ex = 0;
+    double mant = std::frexp(rate, &ex);
+    uint64_t m = (uint64_t)std::ldexp(mant, 53);
+    int k = 53 - ex;
+    while (k > 0 && (m & 1u) == 0) { m >>= 1; --k; }
+    if (k > 64) return fail(TIO_ERR_CHANNEL_CONFIG, "rate %.17g has more than 64 fractional bits", rate);
+    rc->num = (int64_t)m;
+    rc->shift = k;
+    return TIO_OK;
+}
+
+}  // namespace tio
+
+using namespace tio;
+
+struct tio_trace {
+    int64_t N = 0, T = 0, E = 0;
+    const int64_t *dur = nullptr, *tid = nullptr, *size = nullptr, *ptr = nullptr;
+    const int8_t *kind = nullptr;
+    const int32_t *acc = nullptr;
+    Arena arena;          // owned input columns (host input) + lifetime products
+    bool lifetime_enqueued = false;
+    bool synced = false;
+    int64_t *starts = nullptr, *timeline = nullptr, *active = nullptr, *diff = nullptr;
+    int64_t *p_tensor = nullptr, *tpp = nullptr, *blk = nullptr, *scalars = nullptr;
+    int32_t *p_start = nullptr, *p_end = nullptr;
+    int8_t *p_wraps = nullptr;
+    int lgrid = 0;
+    // host copies after sync
+    int64_t num_periods = 0, iteration = 0, flags = 0, ids_unsorted = 0;
+};
+
+struct tio_plan {
+    Arena arena;
+    tio_plan_info info{};
+    int64_t N = 0;
+    tio_commit *commits = nullptr;
+    tio_entry *entries = nullptr;
+    int64_t *resid = nullptr;
+    int64_t *over = nullptr;
+};
+
+extern "C" {
+
+int tio_abi_version(void) { return TIO_ABI_VERSION; }
+
+int tio_last_error(char *buf, size_t len) {
+    if (!buf || !len) return TIO_ERR_INVALID;
+    strncpy(buf, g_err, len - 1);
+    buf[len - 1] = 0;
+    return TIO_OK;
+}
+
+int tio_device_info(char *buf, size_t len) {
+    int dev = 0;
+    cudaDeviceProp prop;
+    TIO_CUDA(cudaGetDevice(&dev));
+    TIO_CUDA(cudaGetDeviceProperties(&prop, dev));
+    snprintf(buf, len, "%s sm_%d%d %d SMs, built for sm_100a", prop.name, prop.major, prop.minor,
+             prop.multiProcessorCount);
+    return TIO_OK;
+}
+
+int tio_transfer_duration(double rate, int64_t nbytes, int64_t *out) {
+    if (!out) return fail(TIO_ERR_INVALID, "null out");
+    if (nbytes < 0) return fail(TIO_ERR_INVALID, "negative transfer size");
+    RateCode rc;
+    TIO_TRY(decode_rate(rate, &rc));
+    *out = duration_of(rc, nbytes);
+    return TIO_OK;
+}
+
+int tio_trace_create(const tio_trace_desc *d, int mem_kind, void *stream, tio_trace **out) {
+    if (!d || !out) return fail(TIO_ERR_INVALID, "null argument");
+    if (d->num_kernels < 0 || d->num_tensors < 0 || d->num_events < 0)
+        return fail(TIO_ERR_INVALID, "negative size");
+    if (d->num_kernels >= INT32_MAX || d->num_events >= INT32_MAX || d->num_tensors >= INT32_MAX)
+        return fail(TIO_ERR_OVERFLOW, "trace too large for 32-bit kernel/tensor indices");
+    TIO_TRY(ensure_pool());
+    cudaStream_t s = (cudaStream_t)stream;
+    tio_trace *t = new tio_trace();
+    t->arena.stream = s;
+    t->N = d->num_kernels;
+    t->T = d->num_tensors;
+    t->E = d->num_events;
+    if (mem_kind == TIO_MEM_DEVICE) {
+        t->dur = d->duration_us; t->tid = d->tensor_id; t->size = d->size_bytes;
+        t->kind = d->kind; t->ptr = d->access_ptr; t->acc = d->accesses;
+    } else if (mem_kind == TIO_MEM_HOST) {
+        int64_t *dur, *tid, *size, *ptr;
+        int8_t *kind;
+        int32_t *acc;
+        int rc = TIO_OK;
+        if ((rc = t->arena.alloc(&dur, t->N)) || (rc = t->arena.alloc(&tid, t->T)) ||
+            (rc = t->arena.alloc(&size, t->T)) || (rc = t->arena.alloc(&kind, t->T)) ||
+            (rc = t->arena.alloc(&ptr, t->T + 1)) || (rc = t->arena.alloc(&acc, t->E))) {
+            t->arena.release();
+            delete t;
+            return rc;
+        }
+        cudaError_t e = cudaSuccess;
+        if (t->N) e = cudaMemcpyAsync(dur, d->duration_us, 8 * t->N, cudaMemcpyHostToDevice, s);
+        if (!e && t->T) e = cudaMemcpyAsync(tid, d->tensor_id, 8 * t->T, cudaMemcpyHostToDevice, s);
+        if (!e && t->T) e = cudaMemcpyAsync(size, d->size_bytes, 8 * t->T, cudaMemcpyHostToDevice, s);
+        if (!e && t->T) e = cudaMemcpyAsync(kind, d->kind, t->T, cudaMemcpyHostToDevice, s);
+        if (!e) e = cudaMemcpyAsync(ptr, d->access_ptr, 8 * (t->T + 1), cudaMemcpyHostToDevice, s);
+        if (!e && t->E) e = cudaMemcpyAsync(acc, d->accesses, 4 * t->E, cudaMemcpyHostToDevice, s);
+        if (e) {
+            t->arena.release();
+            delete t;
+            return fail(TIO_ERR_CUDA, "trace upload failed: %s", cudaGetErrorString(e));
+        }
+        t->dur = dur; t->tid = tid; t->size = size; t->kind = kind; t->ptr = ptr; t->acc = acc;
+    } else {
+        delete t;
+        return fail(TIO_ERR_INVALID, "unknown mem_kind %d", mem_kind);
+    }
+    *out = t;
+    return TIO_OK;
+}
+
+int tio_trace_destroy(tio_trace *t) {
+    if (!t) return TIO_OK;
+    t->arena.release();
+    cudaStreamSynchronize(t->arena.stream);
+    delete t;
+    return TIO_OK;
+}
+
+int tio_lifetime(tio_trace *t, void *stream) {
+    if (!t) return fail(TIO_ERR_INVALID, "null trace");
+    cudaStream_t s = (cudaStream_t)stream;
+    t->arena.stream = s;
+    if (!t->starts) {
+        TIO_TRY(lifetime_grid(&t->lgrid));
+        TIO_TRY(t->arena.alloc(&t->starts, t->N + 1));
+        TIO_TRY(t->arena.alloc(&t->timeline, t->N));
+        TIO_TRY(t->arena.alloc(&t->active, t->N));
+        TIO_TRY(t->arena.alloc(&t->diff, t->N + 1));
+        TIO_TRY(t->arena.alloc(&t->p_tensor, t->E));
+        TIO_TRY(t->arena.alloc(&t->p_start, t->E));
+        TIO_TRY(t->arena.alloc(&t->p_end, t->E));
+        TIO_TRY(t->arena.alloc(&t->p_wraps, t->E));
+        TIO_TRY(t->arena.alloc(&t->tpp, t->T + 1));
+        TIO_TRY(t->arena.alloc(&t->blk, 3 * (int64_t)t->lgrid));
+        TIO_TRY(t->arena.alloc(&t->scalars, SC_COUNT));
+    }
+    TIO_CUDA(cudaMemsetAsync(t->active, 0, 8 * (t->N > 0 ? t->N : 1), s));
+    TIO_CUDA(cudaMemsetAsync(t->diff, 0, 8 * (t->N + 1), s));
+    TIO_CUDA(cudaMemsetAsync(t->scalars, 0, 8 * SC_COUNT, s));
+    if (t->T == 0) TIO_CUDA(cudaMemsetAsync(t->tpp, 0, 8, s));
+    LifetimeArgs a;
+    a.N = t->N; a.T = t->T; a.E = t->E;
+    a.dur = t->dur; a.tid = t->tid; a.size = t->size; a.kind = t->kind; a.ptr = t->ptr; a.acc = t->acc;
+    a.starts = t->starts; a.timeline = t->timeline; a.active = t->active; a.diff = t->diff;
+    a.p_tensor = t->p_tensor; a.p_start = t->p_start; a.p_end = t->p_end; a.p_wraps = t->p_wraps;
+    a.tensor_pptr = t->tpp;
+    a.blk_periods = t->blk; a.blk_dur = t->blk + t->lgrid; a.blk_diff = t->blk + 2 * t->lgrid;
+    a.scalars = t->scalars;
+    if (t->N == 0) {
+        // no kernels: every trace with tensors is invalid (accesses out of range)
+        TIO_CUDA(cudaMemsetAsync(t->starts, 0, 8, s));
+        if (t->T > 0) {
+            int64_t bad = 8;
+            TIO_CUDA(cudaMemcpyAsync(t->scalars + SC_FLAGS, &bad, 8, cudaMemcpyHostToDevice, s));
+            TIO_CUDA(cudaStreamSynchronize(s));
+        }
+    } else {
+        TIO_TRY(launch_lifetime(a, t->lgrid, s));
+    }
+    t->lifetime_enqueued = true;
+    t->synced = false;
+    return TIO_OK;
+}
+
+static int lifetime_sync(tio_trace *t, cudaStream_t s) {
+    if (!t->lifetime_enqueued) TIO_TRY(tio_lifetime(t, s));
+    if (t->synced) return TIO_OK;
+    int64_t sc[SC_COUNT];
+    TIO_CUDA(cudaMemcpyAsync(sc, t->scalars, sizeof(sc), cudaMemcpyDeviceToHost, s));
+    int64_t it = 0;
+    TIO_CUDA(cudaMemcpyAsync(&it, t->starts + t->N, 8, cudaMemcpyDeviceToHost, s));
+    TIO_CUDA(cudaStreamSynchronize(s));
+    t->num_periods = t->T > 0 ? sc[SC_NUM_PERIODS] : 0;
+    t->flags = sc[SC_FLAGS];
+    t->ids_unsorted = sc[SC_IDS_UNSORTED];
+    t->iteration = it;
+    t->synced = true;
+    if (t->flags) return fail(TIO_ERR_INVALID, "trace violates model invariants (flags 0x%llx)",
+                              (unsigned long long)t->flags);
+    return TIO_OK;
+}
+
+int tio_lifetime_view_get(tio_trace *t, void *stream, tio_lifetime_view *v) {
+    if (!t || !v) return fail(TIO_ERR_INVALID, "null argument");
+    TIO_TRY(lifetime_sync(t, (cudaStream_t)stream));
+    v->num_kernels = t->N; v->num_tensors = t->T; v->num_periods = t->num_periods;
+    v->iteration_us = t->iteration;
+    v->starts = t->starts; v->timeline = t->timeline; v->active = t->active;
+    v->period_tensor = t->p_tensor; v->period_start = t->p_start; v->period_end = t->p_end;
+    v->period_wraps = t->p_wraps; v->tensor_period_ptr = t->tpp;
+    return TIO_OK;
+}
+
+int tio_lifetime_copy_out(tio_trace *t, void *stream, int64_t *starts, int64_t *timeline, int64_t *active,
+                          int64_t *period_tensor, int32_t *period_start, int32_t *period_end,
+                          int8_t *period_wraps) {
+    if (!t) return fail(TIO_ERR_INVALID, "null trace");
+    cudaStream_t s = (cudaStream_t)stream;
+    TIO_TRY(lifetime_sync(t, s));
+    const int64_t N = t->N, P = t->num_periods;
+    if (starts) TIO_CUDA(cudaMemcpyAsync(starts, t->starts, 8 * (N + 1), cudaMemcpyDeviceToHost, s));
+    if (timeline && N) TIO_CUDA(cudaMemcpyAsync(timeline, t->timeline, 8 * N, cudaMemcpyDeviceToHost, s));
+    if (active && N) TIO_CUDA(cudaMemcpyAsync(active, t->active, 8 * N, cudaMemcpyDeviceToHost, s));
+    if (P) {
+        if (period_tensor) TIO_CUDA(cudaMemcpyAsync(period_tensor, t->p_tensor, 8 * P, cudaMemcpyDeviceToHost, s));
+        if (period_start) TIO_CUDA(cudaMemcpyAsync(period_start, t->p_start, 4 * P, cudaMemcpyDeviceToHost, s));
+        if (period_end) TIO_CUDA(cudaMemcpyAsync(period_end, t->p_end, 4 * P, cudaMemcpyDeviceToHost, s));
+        if (period_wraps) TIO_CUDA(cudaMemcpyAsync(period_wraps, t->p_wraps, P, cudaMemcpyDeviceToHost, s));
+    }
+    TIO_CUDA(cudaStreamSynchronize(s));
+    return TIO_OK;
+}
+
+static int bitlen(uint64_t v) {
+    int b = 0;
+    while (v) { ++b; v >>= 1; }
+    return b;
+}
+
+static unsigned grid_for(int64_t n, int threads = 256) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 16) b = 148 * 16;
+    return (unsigned)b;
+}
+
+int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap, void *stream,
+                    tio_plan **out, tio_plan_info *info) {
+    if (!t || !rates || !out) return fail(TIO_ERR_INVALID, "null argument");
+    *out = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    TIO_TRY(lifetime_sync(t, s));
+    const int64_t N = t->N, T = t->T, P = t->num_periods, I = t->iteration;
+    tio_plan *p = new tio_plan();
+    p->arena.stream = s;
+    p->N = N;
+    tio_plan_info &pi = p->info;
+    memset(&pi, 0, sizeof(pi));
+    pi.capacity_bytes = capacity;
+    pi.num_candidates = P;
+    Arena &A = p->arena;
+    auto bail = [&](int rc) { A.release(); cudaStreamSynchronize(s); if (info) *info = pi; delete p; return rc; };
+#define PTRY(expr) do { int _r = (expr); if (_r != TIO_OK) return bail(_r); } while (0)
+#define PCUDA(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) return bail(fail(TIO_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e))); } while (0)
+
+    int64_t *ps;
+    PTRY(A.alloc(&ps, PS_COUNT));
+    PCUDA(cudaMemsetAsync(ps, 0, 8 * PS_COUNT, s));
+    // unsatisfiable check first (planner.py:275-278), before any channel is built
+    {
+        unsigned long long *first;
+        PTRY(A.alloc(&first, 1));
+        PCUDA(cudaMemsetAsync(first, 0xff, 8, s));
+        if (N) k_unsat<<<grid_for(N), 256, 0, s>>>(t->active, N, capacity, first);
+        k_unsat_finish<<<1, 1, 0, s>>>(t->active, first, N, ps, t->scalars + SC_FLAGS);
+        PCUDA(cudaGetLastError());
+    }
+    RateCode rc[4];
+    int rate_err = decode_rate(rates->ssd_offload, &rc[0]);
+    if (!rate_err) rate_err = decode_rate(rates->ssd_prefetch, &rc[1]);
+    if (!rate_err && rates->has_host) rate_err = decode_rate(rates->host_offload, &rc[2]);
+    if (!rate_err && rates->has_host) rate_err = decode_rate(rates->host_prefetch, &rc[3]);
+    if (!rates->has_host) { rc[2] = rc[0]; rc[3] = rc[1]; }
+    if (rate_err) {
+        int64_t hs[PS_COUNT];
+        PCUDA(cudaMemcpyAsync(hs, ps, sizeof(hs), cudaMemcpyDeviceToHost, s));
+        PCUDA(cudaStreamSynchronize(s));
+        if (hs[PS_STATUS] == 1) {
+            pi.unsat_kernel = hs[PS_UNSAT_K]; pi.unsat_bytes = hs[PS_UNSAT_B];
+            return bail(fail(TIO_ERR_UNSATISFIABLE, "kernel %lld uses %lld bytes actively, more than capacity %lld; "
+                             "no offloading plan can help", (long long)pi.unsat_kernel,
+                             (long long)pi.unsat_bytes, (long long)capacity));
+        }
+        return bail(rate_err);
+    }
+    const bool has_host = rates->has_host != 0;
+
+    // ---- candidate order: tensors by id, then start kernel
+    int32_t *rank;
+    int64_t *cnt_by_rank, *cand_ptr, *scan_tmp;
+    PTRY(A.alloc(&rank, T));
+    PTRY(A.alloc(&cnt_by_rank, T + 1));
+    PTRY(A.alloc(&cand_ptr, T + 1));
+    PTRY(A.alloc(&scan_tmp, scan_tmp_elems(T + 1) + 2));
+    int64_t *dupflag;
+    PTRY(A.alloc(&dupflag, 1));
+    PCUDA(cudaMemsetAsync(dupflag, 0, 8, s));
+    if (T > 0) {
+        if (t->ids_unsorted) {
+            uint64_t *k0, *k1;
+            uint32_t *v0, *v1, *hist;
+            PTRY(A.alloc(&k0, T)); PTRY(A.alloc(&k1, T));
+            PTRY(A.alloc(&v0, T)); PTRY(A.alloc(&v1, T));
+            PTRY(A.alloc(&hist, radix_hist_elems(T)));
+            k_id_keys<<<grid_for(T), 256, 0, s>>>(t->tid, T, k0, v0);
+            bool in_tmp = false;
+            PTRY(radix_sort_pairs(k0, v0, k1, v1, hist, T, 64, s, &in_tmp));
+            k_rank<<<grid_for(T), 256, 0, s>>>(in_tmp ? k1 : k0, in_tmp ? v1 : v0, T, t->tpp, rank,
+                                              cnt_by_rank, dupflag);
+        } else {
+            k_rank<<<grid_for(T), 256, 0, s>>>(nullptr, nullptr, T, t->tpp, rank, cnt_by_rank, dupflag);
+        }
+        PCUDA(cudaGetLastError());
+        PTRY(exclusive_scan(cnt_by_rank, cand_ptr, T, scan_tmp, cand_ptr + T, s));
+    }
+
+    // ---- candidates + planner state
+    PlanArgs a;
+    memset(&a, 0, sizeof(a));
+    int64_t *c_size, *c_ready, *c_deadline, *c_d, *c_tid, *place;
+    int32_t *c_sk, *c_ek, *c_first, *c_last, *c_tpos, *rng, *list0, *list1;
+    int8_t *c_wraps, *st;
+    PTRY(A.alloc(&c_size, P)); PTRY(A.alloc(&c_ready, P)); PTRY(A.alloc(&c_deadline, P));
+    PTRY(A.alloc(&c_d, 4 * P)); PTRY(A.alloc(&c_tid, P)); PTRY(A.alloc(&place, 4 * P));
+    PTRY(A.alloc(&c_sk, P)); PTRY(A.alloc(&c_ek, P)); PTRY(A.alloc(&c_first, P)); PTRY(A.alloc(&c_last, P));
+    PTRY(A.alloc(&c_tpos, P)); PTRY(A.alloc(&rng, 4 * P)); PTRY(A.alloc(&list0, P)); PTRY(A.alloc(&list1, P));
+    PTRY(A.alloc(&c_wraps, P)); PTRY(A.alloc(&st, P));
+    if (P > 0) {
+        CandBuild cb;
+        cb.num_periods = t->scalars + SC_NUM_PERIODS;
+        cb.p_tensor = t->p_tensor; cb.p_start = t->p_start; cb.p_end = t->p_end; cb.p_wraps = t->p_wraps;
+        cb.tpp = t->tpp; cb.rank = rank; cb.cand_ptr = cand_ptr;
+        cb.size = t->size; cb.tid = t->tid; cb.ptr = t->ptr; cb.starts = t->starts; cb.dur = t->dur; cb.acc = t->acc;
+        cb.iteration = I; cb.has_host = has_host;
+        for (int q = 0; q < 4; ++q) cb.rates[q] = rc[q];
+        cb.c_size = c_size; cb.c_sk = c_sk; cb.c_ek = c_ek; cb.c_first = c_first; cb.c_last = c_last;
+        cb.c_wraps = c_wraps; cb.c_ready = c_ready; cb.c_deadline = c_deadline; cb.c_d = c_d; cb.c_tid = c_tid;
+        cb.c_tpos = c_tpos; cb.st = st;
+        k_build_candidates<<<grid_for(P), 256, 0, s>>>(cb);
+        PCUDA(cudaGetLastError());
+    }
+    int G = 0;
+    PTRY(plan_loop_grid(&G));
+    int64_t *resid, *local_cp, *chunk_sum;
+    PTRY(A.alloc(&resid, N)); PTRY(A.alloc(&local_cp, N + 1)); PTRY(A.alloc(&chunk_sum, G));
+    if (N) PCUDA(cudaMemcpyAsync(resid, t->timeline, 8 * N, cudaMemcpyDeviceToDevice, s));
+    const int nch = has_host ? 4 : 2;
+    const int64_t ch_cap = 3 * P + 3;
+    for (int q = 0; q < 4; ++q)
+        for (int bb = 0; bb < 2; ++bb) {
+            if (q < nch) {
+                PTRY(A.alloc(&a.ch_s[q][bb], ch_cap));
+                PTRY(A.alloc(&a.ch_e[q][bb], ch_cap));
+            } else {
+                a.ch_s[q][bb] = a.ch_s[0][bb];
+                a.ch_e[q][bb] = a.ch_e[0][bb];
+            }
+        }
+    int64_t *occ_s, *occ_e, *occ_z;
+    PTRY(A.alloc(&occ_s, has_host ? P : 1)); PTRY(A.alloc(&occ_e, has_host ? P : 1)); PTRY(A.alloc(&occ_z, has_host ? P : 1));
+    Best *blk_best;
+    PTRY(A.alloc(&blk_best, G));
+    PTRY(A.alloc(&p->commits, P));
+    a.N = N; a.P = P; a.iteration = I; a.capacity = capacity; a.host_cap = host_cap;
+    a.has_host = has_host;
+    a.chunk = (int32_t)((N + 1 + G - 1) / G);
+    a.starts = t->starts; a.dur = t->dur; a.resid = resid; a.local_cp = local_cp; a.chunk_sum = chunk_sum;
+    a.c_size = c_size; a.c_sk = c_sk; a.c_ek = c_ek; a.c_first = c_first; a.c_last = c_last; a.c_wraps = c_wraps;
+    a.c_ready = c_ready; a.c_deadline = c_deadline; a.c_d = c_d;
+    a.st = st; a.place = place; a.rng = rng; a.list0 = list0; a.list1 = list1;
+    a.ch_cap = ch_cap;
+    a.occ_s = occ_s; a.occ_e = occ_e; a.occ_size = occ_z;
+    a.blk_best = blk_best; a.commits = p->commits; a.scalars = ps; a.c_tid = c_tid; a.c_tpos = c_tpos;
+    PTRY(launch_plan_loop(a, G, s));
+
+    int64_t hs[PS_COUNT];
+    int64_t dup = 0;
+    PCUDA(cudaMemcpyAsync(hs, ps, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    PCUDA(cudaMemcpyAsync(&dup, dupflag, 8, cudaMemcpyDeviceToHost, s));
+    PCUDA(cudaStreamSynchronize(s));
+    if (dup) return bail(fail(TIO_ERR_INVALID, "duplicate tensor id"));
+    if (hs[PS_STATUS] == 1) {
+        pi.unsat_kernel = hs[PS_UNSAT_K]; pi.unsat_bytes = hs[PS_UNSAT_B];
+        return bail(fail(TIO_ERR_UNSATISFIABLE, "kernel %lld uses %lld bytes actively, more than capacity %lld; "
+                         "no offloading plan can help", (long long)pi.unsat_kernel,
+                         (long long)pi.unsat_bytes, (long long)capacity));
+    }
+    if (hs[PS_STATUS] == 2) return bail(fail(TIO_ERR_INVALID, "trace violates model invariants"));
+    if (hs[PS_INVARIANT]) return bail(fail(TIO_ERR_INTERNAL, "channel bookings overlapped (disjointness invariant)"));
+    const int64_t nc = hs[PS_COMMITS];
+    pi.num_commits = nc;
+    pi.num_entries = 2 * nc;
+    pi.rounds = hs[PS_ROUNDS];
+
+    // ---- epilogue: over list, peak, planned host, sorted + urgent entries
+    p->resid = resid;
+    int64_t *flag, *pos, *ovt, *peakp, *hostp;
+    PTRY(A.alloc(&flag, N)); PTRY(A.alloc(&pos, N + 1)); PTRY(A.alloc(&p->over, N));
+    PTRY(A.alloc(&ovt, scan_tmp_elems(N) + 2)); PTRY(A.alloc(&peakp, 2)); PTRY(A.alloc(&hostp, 1));
+    PCUDA(cudaMemsetAsync(peakp, 0, 16, s));
+    {
+        int64_t lmin = LLONG_MIN;
+        PCUDA(cudaMemcpyAsync(peakp, &lmin, 8, cudaMemcpyHostToDevice, s));
+    }
+    if (N) {
+        k_over_flags<<<grid_for(N), 256, 0, s>>>(resid, N, capacity, flag, (long long *)peakp);
+        PTRY(exclusive_scan(flag, pos, N, ovt, pos + N, s));
+        k_over_write<<<grid_for(N), 256, 0, s>>>(flag, pos, N, p->over);
+    }
+    k_planned_host<<<1, 256, 0, s>>>(occ_s, occ_e, occ_z, hs[PS_OCC], hostp);
+    PTRY(A.alloc(&p->entries, 2 * nc));
+    if (nc > 0) {
+        const int64_t ne = 2 * nc;
+        uint64_t *k0, *k1;
+        uint32_t *v0, *v1, *hist;
+        PTRY(A.alloc(&k0, ne)); PTRY(A.alloc(&k1, ne)); PTRY(A.alloc(&v0, ne)); PTRY(A.alloc(&v1, ne));
+        PTRY(A.alloc(&hist, radix_hist_elems(ne)));
+        const int rbits = bitlen((uint64_t)(T > 0 ? T - 1 : 0));
+        const int tbits = bitlen((uint64_t)(2 * I > 0 ? 2 * I : 1));
+        bool in_tmp = false;
+        uint32_t *order;
+        if (tbits + rbits + 1 <= 64) {
+            k_entry_keys<<<grid_for(ne), 256, 0, s>>>(p->commits, nc, rank, rbits, 0, k0, v0);
+            PTRY(radix_sort_pairs(k0, v0, k1, v1, hist, ne, tbits + rbits + 1, s, &in_tmp));
+            order = in_tmp ? v1 : v0;
+        } else {
+            k_entry_keys<<<grid_for(ne), 256, 0, s>>>(p->commits, nc, rank, rbits, 1, k0, v0);
+            PTRY(radix_sort_pairs(k0, v0, k1, v1, hist, ne, rbits + 1, s, &in_tmp));
+            uint64_t *kk = in_tmp ? k1 : k0, *kt = in_tmp ? k0 : k1;
+            uint32_t *vv = in_tmp ? v1 : v0, *vt = in_tmp ? v0 : v1;
+            k_regather_keys<<<grid_for(ne), 256, 0, s>>>(p->commits, vv, ne, kk);
+            bool in2 = false;
+            PTRY(radix_sort_pairs(kk, vv, kt, vt, hist, ne, tbits, s, &in2));
+            order = in2 ? vt : vv;
+        }
+        k_emit_entries<<<grid_for(ne), 256, 0, s>>>(p->commits, order, ne, t->starts, t->ptr, t->acc, t->kind, I,
+                                                     p->entries);
+        PCUDA(cudaGetLastError());
+    }
+    int64_t tail[3] = {0, 0, 0};
+    PCUDA(cudaMemcpyAsync(&tail[0], peakp, 8, cudaMemcpyDeviceToHost, s));
+    PCUDA(cudaMemcpyAsync(&tail[1], hostp, 8, cudaMemcpyDeviceToHost, s));
+    if (N) PCUDA(cudaMemcpyAsync(&tail[2], pos + N, 8, cudaMemcpyDeviceToHost, s));
+    PCUDA(cudaStreamSynchronize(s));
+    pi.residual_peak_bytes = N ? tail[0] : 0;
+    pi.planned_host_bytes = tail[1];
+    pi.num_over = N ? tail[2] : 0;
+    if (info) *info = pi;
+    *out = p;
+    return TIO_OK;
+#undef PTRY
+#undef PCUDA
+}
+
+int tio_plan_info_get(tio_plan *p, tio_plan_info *out) {
+    if (!p || !out) return fail(TIO_ERR_INVALID, "null argument");
+    *out = p->info;
+    return TIO_OK;
+}
+
+int tio_plan_copy_out(tio_plan *p, void *stream, tio_commit *commits, tio_entry *entries, int64_t *residual,
+                      int64_t *over) {
+    if (!p) return fail(TIO_ERR_INVALID, "null plan");
+    cudaStream_t s = (cudaStream_t)stream;
+    const tio_plan_info &i = p->info;
+    if (commits && i.num_commits)
+        TIO_CUDA(cudaMemcpyAsync(commits, p->commits, sizeof(tio_commit) * i.num_commits, cudaMemcpyDeviceToHost, s));
+    if (entries && i.num_entries)
+        TIO_CUDA(cudaMemcpyAsync(entries, p->entries, sizeof(tio_entry) * i.num_entries, cudaMemcpyDeviceToHost, s));
+    if (residual && p->N) TIO_CUDA(cudaMemcpyAsync(residual, p->resid, 8 * p->N, cudaMemcpyDeviceToHost, s));
+    if (over && i.num_over) TIO_CUDA(cudaMemcpyAsync(over, p->over, 8 * i.num_over, cudaMemcpyDeviceToHost, s));
+    TIO_CUDA(cudaStreamSynchronize(s));
+    return TIO_OK;
+}
+
+// write_plan (planner.py:402-420): json.dumps default separators
+int tio_plan_write(tio_plan *p, void *stream, char *buf, size_t *len) {
+    if (!p || !len) return fail(TIO_ERR_INVALID, "null argument");
+    const tio_plan_info &i = p->info;
+    std::vector<tio_entry> ents((size_t)i.num_entries);
+    std::vector<int64_t> over((size_t)i.num_over);
+    TIO_TRY(tio_plan_copy_out(p, stream, nullptr, ents.data(), nullptr, over.data()));
+    std::string out;
+    out.reserve(160 + 24 * over.size() + 110 * ents.size());
+    char tmp[256];
+    snprintf(tmp, sizeof(tmp),
+             "{\"version\": 1, \"capacity_bytes\": %lld, \"residual_peak_bytes\": %lld, "
+             "\"planned_host_bytes\": %lld, \"over_capacity_kernels\": [",
+             (long long)i.capacity_bytes, (long long)i.residual_peak_bytes, (long long)i.planned_host_bytes);
+    out += tmp;
+    for (size_t k = 0; k < over.size(); ++k) {
+        snprintf(tmp, sizeof(tmp), k ? ", %lld" : "%lld", (long long)over[k]);
+        out += tmp;
+    }
+    out += "]}";
+    static const char *targets[] = {"GPU", "SSD", "CPU"};
+    for (const tio_entry &e : ents) {
+        snprintf(tmp, sizeof(tmp),
+                 "\n{\"tensor\": %lld, \"action\": \"%s\", \"trigger_us\": %lld, \"deadline_us\": %lld, "
+                 "\"target\": \"%s\", \"urgent\": %s}",
+                 (long long)e.tensor_id, e.action ? "prefetch" : "offload", (long long)e.trigger_us,
+                 (long long)e.deadline_us, targets[e.target < 0 || e.target > 2 ? 0 : e.target],
+                 e.urgent ? "true" : "false");
+        out += tmp;
+    }
+    out += "\n";
+    if (!buf) { *len = out.size(); return TIO_OK; }
+    if (*len < out.size()) { *len = out.size(); return fail(TIO_ERR_INVALID, "buffer too small"); }
+    memcpy(buf, out.data(), out.size());
+    *len = out.size();
+    return TIO_OK;
+}
+
+int tio_plan_destroy(tio_plan *p) {
+    if (!p) return TIO_OK;
+    p->arena.release();
+    cudaStreamSynchronize(p->arena.stream);
+    delete p;
+    return TIO_OK;
+}
+
+int tio_plan_host(const tio_trace_desc *desc, int64_t capacity, const tio_rates *rates, int64_t host_cap,
+                  void *stream, tio_plan_info *info, tio_entry *entries, int64_t entries_cap) {
+    tio_trace *t = nullptr;
+    TIO_TRY(tio_trace_create(desc, TIO_MEM_HOST, stream, &t));
+    tio_plan *p = nullptr;
+    int rc = tio_plan_create(t, capacity, rates, host_cap, stream, &p, info);
+    if (rc == TIO_OK) {
+        if (entries && info->num_entries > entries_cap) rc = fail(TIO_ERR_INVALID, "entries buffer too small");
+        else rc = tio_plan_copy_out(p, stream, nullptr, entries, nullptr, nullptr);
+        tio_plan_destroy(p);
+    }
+    tio_trace_destroy(t);
+    return rc;
+}
+
+}  // extern "C"

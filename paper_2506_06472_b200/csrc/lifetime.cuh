@@ -1,0 +1,39 @@
+// lifetime.cuh — lifetime-stage kernel interface.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tio {
+
+constexpr int LIFETIME_THREADS = 256;
+
+// scalars[] slots shared by the lifetime and planner kernels
+enum { SC_GLOBAL_BYTES = 0, SC_NUM_PERIODS = 1, SC_FLAGS = 2, SC_IDS_UNSORTED = 3, SC_COUNT = 8 };
+
+struct LifetimeArgs {
+    int64_t N, T, E;
+    const int64_t *dur;
+    const int64_t *tid;
+    const int64_t *size;
+    const int8_t *kind;
+    const int64_t *ptr;
+    const int32_t *acc;
+    int64_t *starts;       // [N+1]
+    int64_t *timeline;     // [N]
+    int64_t *active;       // [N]   zeroed by the caller
+    int64_t *diff;         // [N+1] zeroed by the caller
+    int64_t *p_tensor;     // [E]   capacity (P <= E)
+    int32_t *p_start;
+    int32_t *p_end;
+    int8_t *p_wraps;
+    int64_t *tensor_pptr;  // [T+1]
+    int64_t *blk_periods;  // [grid]
+    int64_t *blk_dur;      // [grid]
+    int64_t *blk_diff;     // [grid]
+    int64_t *scalars;      // [SC_COUNT] zeroed by the caller
+};
+
+int lifetime_grid(int *blocks);
+int launch_lifetime(const LifetimeArgs &args, int blocks, cudaStream_t stream);
+
+}  // namespace tio

@@ -1,0 +1,562 @@
+// planner.cu — Algorithm 1 (reference planner.py:267-370) as one persistent
+// cooperative kernel: every round evaluates all live candidates in parallel,
+// reduces the exact argmax of benefit/cost, and commits it, with two grid
+// barriers per round.
+//
+// Exactness — how each reference rule is kept:
+//   * channel searches (bandwidth.py:88-120) run on sorted, pairwise disjoint
+//     interval arrays (committed bookings and their +-iteration shadows,
+//     :139-151); the walk starts at a binary-searched position, which cannot
+//     change the result for disjoint intervals (the merge step flags any
+//     overlap as an invariant failure);
+//   * a candidate's cached placement is re-derived only when the last commit's
+//     bookings overlap it (booking more intervals can only push an earliest
+//     fit later and a latest fit earlier, so a non-overlapped placement is still
+//     the optimum); SSD infeasibility is permanent for the same reason;
+//   * benefit = size x sum of durations of covered kernels with residual >
+//     capacity (planner.py:253-262); covered kernels form <= 2 contiguous
+//     ranges (:232-250) and the sum comes from a chunked prefix array that is
+//     rebuilt where kernels flipped to non-critical;
+//   * the winner is the max of benefit/cost by 192-bit cross products, ties to
+//     the lowest candidate index = first in (tensor_id, start_kernel) order
+//     (:295-310);
+//   * commit: bookings + shadows, residual -= size on every covered kernel,
+//     host occupancy (:314-348).
+// Candidates that can never win again are dropped from the live lists:
+// infeasible on both paths, or zero benefit on a path whose window can only
+// shrink (SSD without a host path, or host).
+#include "common.cuh"
+#include "block_scan.cuh"
+#include "planner.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tio {
+
+constexpr int MAXG = 1024;
+
+struct LastCommit {
+    int64_t dest;                 // 0 none (first round), 1 SSD, 2 CPU
+    int64_t off_s[3], off_e[3];   // new bookings on the offload channel
+    int64_t pre_s[3], pre_e[3];   // new bookings on the prefetch channel
+    int64_t nb;                   // bookings per channel (3 with shadows, 1 without)
+    int64_t occ_s, occ_e;         // new host occupancy (CPU commits)
+};
+
+struct ChanView {
+    const int64_t *s, *e;
+    int64_t n;
+};
+
+// ---------------------------------------------------------------- channels
+// bandwidth.py:88-100 reserve_earliest
+__device__ int64_t ch_earliest(const ChanView &c, int64_t ready, int64_t d) {
+    int64_t lo = 0, hi = c.n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (ld_cg(c.e + mid) > ready) hi = mid; else lo = mid + 1;
+    }
+    int64_t t = ready;
+    for (int64_t i = lo; i < c.n; ++i) {
+        int64_t s = ld_cg(c.s + i);
+        if (s >= t + d) break;
+        int64_t e = ld_cg(c.e + i);
+        if (e > t) t = e;
+    }
+    return t;
+}
+
+// bandwidth.py:102-120 reserve_latest; false = None
+__device__ bool ch_latest(const ChanView &c, int64_t deadline, int64_t not_before, int64_t d,
+                          int64_t *out) {
+    int64_t start = deadline - d;
+    int64_t lo = 0, hi = c.n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (ld_cg(c.s + mid) < deadline) lo = mid + 1; else hi = mid;
+    }
+    for (int64_t i = lo - 1; i >= 0; --i) {
+        if (start < not_before) return false;
+        int64_t s = ld_cg(c.s + i);
+        if (s >= start + d) continue;
+        int64_t e = ld_cg(c.e + i);
+        if (e <= start) break;
+        start = s - d;
+    }
+    if (start < not_before) return false;
+    *out = start;
+    return true;
+}
+
+// candidate_window (planner.py:147-176) on one channel pair.
+// Incremental refit: channels only gain bookings, so the new earliest offload
+// is >= the cached one and the new latest prefetch <= the cached one; the
+// searches restart from the cached placement (hint_off / hint_pre_end) instead
+// of from ready / deadline, which gives the same optimum without re-walking
+// the packed prefix.  First fits pass hint_off = ready, hint_pre_end = deadline.
+__device__ bool fit_pair(const ChanView &off, const ChanView &pre, int64_t d_off, int64_t d_pre,
+                         int64_t iteration, int64_t hint_off, int64_t hint_pre_end,
+                         int64_t *off_s, int64_t *pre_s) {
+    if (d_off > iteration || d_pre > iteration) return false;
+    int64_t o = ch_earliest(off, hint_off, d_off);
+    int64_t t_off = o + d_off;
+    int64_t f;
+    if (!ch_latest(pre, hint_pre_end, t_off, d_pre, &f)) return false;
+    if (!(t_off < f)) return false;
+    *off_s = o;
+    *pre_s = f;
+    return true;
+}
+
+// _host_peak_occupancy (planner.py:179-186)
+__device__ int64_t host_peak(const int64_t *os, const int64_t *oe, const int64_t *oz, int64_t h,
+                             int64_t lo, int64_t hi) {
+    int64_t peak = 0;
+    for (int64_t pi = -1; pi < h; ++pi) {
+        int64_t p;
+        if (pi < 0) p = lo;
+        else {
+            p = ld_cg(os + pi);
+            if (!(lo <= p && p <= hi)) continue;
+        }
+        int64_t sum = 0;
+        for (int64_t j = 0; j < h; ++j)
+            if (ld_cg(os + j) <= p && p < ld_cg(oe + j)) sum += ld_cg(oz + j);
+        if (sum > peak) peak = sum;
+    }
+    return peak;
+}
+
+// _covered_kernels (planner.py:232-250) as <= 2 kernel ranges
+__device__ void covered_ranges(const int64_t *__restrict__ starts, int64_t N, int64_t iteration,
+                               int wraps, int32_t sk, int32_t ek, int32_t first, int32_t last,
+                               int64_t lo_t, int64_t hi_t, int32_t r[4]) {
+    r[0] = 1; r[1] = 0; r[2] = 1; r[3] = 0;
+    auto range = [&](int64_t a, int64_t b, int64_t sh, int32_t &olo, int32_t &ohi) {
+        int64_t L = a, H = b + 1;
+        while (L < H) {
+            int64_t M = (L + H) >> 1;
+            if (__ldg(starts + M) + sh >= lo_t) H = M; else L = M + 1;
+        }
+        int64_t klo = L;
+        L = klo; H = b + 1;
+        while (L < H) {
+            int64_t M = (L + H) >> 1;
+            if (__ldg(starts + M + 1) + sh <= hi_t) L = M + 1; else H = M;
+        }
+        olo = (int32_t)klo;
+        ohi = (int32_t)(L - 1);
+    };
+    if (!wraps) {
+        if (sk <= ek) range(sk, ek, 0, r[0], r[1]);
+    } else {
+        if (last + 1 <= N - 1) range(last + 1, N - 1, 0, r[0], r[1]);
+        if (first - 1 >= 0) range(0, first - 1, iteration, r[2], r[3]);
+    }
+}
+
+__device__ __forceinline__ bool overlaps(int64_t x, int64_t d, const int64_t *s, const int64_t *e, int64_t nb) {
+    for (int q = 0; q < nb; ++q)
+        if (x < e[q] && s[q] < x + d) return true;
+    return false;
+}
+
+__device__ __forceinline__ bool better(const Best &a, const Best &b) {
+    if (a.benefit == 0) return false;
+    if (b.benefit == 0) return true;
+    if (ratio_gt(a.benefit, a.cost, b.benefit, b.cost)) return true;
+    if (ratio_gt(b.benefit, b.cost, a.benefit, a.cost)) return false;
+    return a.idx < b.idx;
+}
+
+__device__ __forceinline__ void shfl_best(Best &dst, const Best &src, int lane) {
+    const int64_t *p = reinterpret_cast<const int64_t *>(&src);
+    int64_t *q = reinterpret_cast<int64_t *>(&dst);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(Best) / 8); ++i) q[i] = __shfl_sync(0xffffffffu, p[i], lane);
+}
+
+__device__ void block_best(Best &mine, Best *sm_best) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        Best other;
+        shfl_best(other, mine, (lane + o) & 31);
+        if (lane + o < 32 && better(other, mine)) mine = other;
+    }
+    if (lane == 0) sm_best[warp] = mine;
+    __syncthreads();
+    if (warp == 0) {
+        mine = lane < nw ? sm_best[lane] : Best{};
+        if (lane >= nw) mine.benefit = 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            Best other;
+            shfl_best(other, mine, (lane + o) & 31);
+            if (lane + o < 32 && better(other, mine)) mine = other;
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- the kernel
+__global__ void __launch_bounds__(PLAN_THREADS)
+plan_loop_kernel(PlanArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int64_t cp_prefix[MAXG + 1];
+    __shared__ Best sm_best[PLAN_THREADS / 32];
+    __shared__ Best s_win;
+    __shared__ LastCommit last;
+    __shared__ int64_t sm_scan[40];
+    __shared__ int64_t ch_n[4];
+    __shared__ int32_t ch_par[4];
+    __shared__ int64_t s_nocc;
+    __shared__ int64_t s_seg_len;
+    __shared__ int32_t s_list_par;
+    __shared__ int64_t s_crit;
+
+    const int64_t N = a.N, P = a.P, I = a.iteration, cap = a.capacity;
+    const int G = gridDim.x;
+    const int b = blockIdx.x;
+    const int64_t KC = a.chunk;
+    const int64_t x0 = (int64_t)b * KC;                       // chunk over x in [0, N]
+    const int64_t x1 = (x0 + KC < N + 1) ? x0 + KC : N + 1;
+    const int64_t seg0 = P * b / G, seg1 = P * (b + 1) / G;
+    const int64_t period = I > 0 ? I : 0;
+    const int64_t nb = period > 0 ? 3 : 1;
+
+    if (ld_cg(&a.scalars[PS_STATUS]) != 0) return;  // unsatisfiable (set by setup)
+
+    // ---- setup: residual = timeline, chunk prefix of critical durations
+    auto rebuild_chunk = [&]() {
+        int64_t run = 0;
+        for (int64_t base = x0; base < x1; base += blockDim.x) {
+            int64_t x = base + threadIdx.x;
+            int64_t w = 0;
+            if (x < x1 && x < N && ld_cg(&a.resid[x]) > cap) w = __ldg(&a.dur[x]);
+            int64_t tot;
+            int64_t ex = block_exclusive_sum<int64_t>(w, sm_scan, &tot);
+            if (x < x1) a.local_cp[x] = run + ex;
+            run += tot;
+        }
+        if (threadIdx.x == 0) a.chunk_sum[b] = run;
+    };
+    {
+        int64_t crit = 0;
+        for (int64_t x = x0 + threadIdx.x; x < x1 && x < N; x += blockDim.x)
+            crit += ld_cg(&a.resid[x]) > cap;
+        __syncthreads();
+        rebuild_chunk();
+        int64_t tot = block_sum<int64_t>(crit, sm_scan);
+        if (threadIdx.x == 0 && tot) atomic_add_i64(&a.scalars[PS_CRIT], tot);
+        for (int64_t i = seg0 + threadIdx.x; i < seg1; i += blockDim.x) a.list0[i] = (int32_t)i;
+        if (threadIdx.x == 0) {
+            s_seg_len = seg1 - seg0;
+            s_list_par = 0;
+            last.dest = 0;
+            last.nb = nb;
+            s_nocc = 0;
+            for (int q = 0; q < 4; ++q) { ch_n[q] = 0; ch_par[q] = 0; }
+        }
+    }
+    grid.sync();
+
+    for (int64_t round = 0;; ++round) {
+        // ---- round prologue: crit count + chunk prefix (identical in every CTA)
+        if (threadIdx.x == 0) s_crit = ld_cg(&a.scalars[PS_CRIT]);
+        {
+            int64_t v = 0;
+            int nchunks = (int)((N + 1 + KC - 1) / KC);
+            // exclusive prefix of chunk sums into cp_prefix[0..nchunks]
+            for (int base = 0; base < nchunks; base += blockDim.x) {
+                int j = base + threadIdx.x;
+                int64_t w = j < nchunks ? ld_cg(&a.chunk_sum[j]) : 0;
+                int64_t tot;
+                int64_t ex = block_exclusive_sum<int64_t>(w, sm_scan, &tot);
+                if (j < nchunks) cp_prefix[j] = v + ex;
+                v += tot;
+            }
+            if (threadIdx.x == 0) cp_prefix[nchunks] = v;
+        }
+        __syncthreads();
+        if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
+
+        // ---- phase E: evaluate live candidates of this block's segment
+        const int32_t *lin = s_list_par ? a.list1 : a.list0;
+        int32_t *lout = s_list_par ? a.list0 : a.list1;
+        ChanView cv[4];
+        for (int q = 0; q < 4; ++q) {
+            cv[q].s = a.ch_s[q][ch_par[q]];
+            cv[q].e = a.ch_e[q][ch_par[q]];
+            cv[q].n = ch_n[q];
+        }
+        Best mine{};
+        mine.benefit = 0;
+        const int64_t seg_len = s_seg_len;
+        int64_t kept_total = 0;
+        for (int64_t base = 0; base < seg_len; base += blockDim.x) {
+            int64_t pos = base + threadIdx.x;
+            bool keep = false;
+            int32_t c = -1;
+            if (pos < seg_len) {
+                c = lin[seg0 + pos];
+                int8_t st = ld_cg(&a.st[c]);
+                if (!(st & ST_GONE)) {
+                    keep = true;
+                    int ssd = st & 3, host = (st >> 2) & 3;
+                    const int64_t size = __ldg(&a.c_size[c]);
+                    const int64_t ready = __ldg(&a.c_ready[c]), deadline = __ldg(&a.c_deadline[c]);
+                    const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
+                    bool moved = false;
+                    // SSD path
+                    int64_t h_off = ready, h_pre = deadline;
+                    if (ssd == S_OK) { h_off = ld_cg(&a.place[4 * c]); h_pre = ld_cg(&a.place[4 * c + 1]) + d1; }
+                    if (ssd == S_UNK ||
+                        (ssd == S_OK && last.dest == TIO_DEST_SSD &&
+                         (overlaps(h_off, d0, last.off_s, last.off_e, last.nb) ||
+                          overlaps(h_pre - d1, d1, last.pre_s, last.pre_e, last.nb)))) {
+                        int64_t os, ps;
+                        if (fit_pair(cv[0], cv[1], d0, d1, I, h_off, h_pre, &os, &ps)) {
+                            ssd = S_OK;
+                            a.place[4 * c] = os;
+                            a.place[4 * c + 1] = ps;
+                        } else {
+                            ssd = S_DEAD;
+                        }
+                        moved = true;
+                    }
+                    // host path (only consulted once the SSD path is dead: planner.py:211-227)
+                    if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
+                        const int64_t d2 = __ldg(&a.c_d[4 * c + 2]), d3 = __ldg(&a.c_d[4 * c + 3]);
+                        bool refit = host == H_UNK;
+                        bool recap = false;
+                        if (!refit && last.dest == TIO_DEST_CPU) {
+                            refit = overlaps(ld_cg(&a.place[4 * c + 2]), d2, last.off_s, last.off_e, last.nb) ||
+                                    overlaps(ld_cg(&a.place[4 * c + 3]), d3, last.pre_s, last.pre_e, last.nb);
+                            if (!refit && host == H_OK) {
+                                int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
+                                recap = last.occ_s <= hi && last.occ_e > lo;
+                            }
+                        }
+                        if (refit) {
+                            int64_t os, ps;
+                            int64_t g_off = ready, g_pre = deadline;
+                            if (host != H_UNK) { g_off = ld_cg(&a.place[4 * c + 2]); g_pre = ld_cg(&a.place[4 * c + 3]) + d3; }
+                            if (fit_pair(cv[2], cv[3], d2, d3, I, g_off, g_pre, &os, &ps)) {
+                                a.place[4 * c + 2] = os;
+                                a.place[4 * c + 3] = ps;
+                                recap = true;
+                                moved = true;
+                            } else {
+                                host = H_DEAD;
+                                moved = true;
+                            }
+                        }
+                        if (recap) {
+                            int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
+                            int64_t occ = host_peak(a.occ_s, a.occ_e, a.occ_size, s_nocc, lo, hi);
+                            host = (occ + size > a.host_cap) ? H_CAPFAIL : H_OK;
+                        }
+                    }
+                    int dest = ssd == S_OK ? TIO_DEST_SSD : (ssd == S_DEAD && host == H_OK ? TIO_DEST_CPU : 0);
+                    int8_t nst = (int8_t)(ssd | (host << 2));
+                    if (ssd == S_DEAD && (!a.has_host || host == H_DEAD)) {
+                        nst |= ST_GONE;
+                        keep = false;
+                    } else if (dest) {
+                        const int q0 = dest == TIO_DEST_SSD ? 0 : 2;
+                        const int64_t os = ld_cg(&a.place[4 * c + q0]);
+                        const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
+                        const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
+                        int32_t r[4];
+                        if (moved) {
+                            covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                                           __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
+                                           os + doff, ps, r);
+                            for (int q = 0; q < 4; ++q) a.rng[4 * c + q] = r[q];
+                        } else {
+                            for (int q = 0; q < 4; ++q) r[q] = ld_cg(&a.rng[4 * c + q]);
+                        }
+                        int64_t ct = 0;
+                        for (int q = 0; q < 4; q += 2) {
+                            if (r[q] <= r[q + 1]) {
+                                int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
+                                ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
+                                      (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
+                            }
+                        }
+                        if (ct == 0) {
+                            // benefit only ever shrinks on a host window or on an SSD
+                            // window without a host path to fall back to
+                            if (dest == TIO_DEST_CPU || !a.has_host) { nst |= ST_GONE; keep = false; }
+                        } else {
+                            Best cand;
+                            cand.benefit = (u128)(uint64_t)size * (uint64_t)ct;
+                            cand.cost = doff + dpre;
+                            cand.idx = c;
+                            cand.dest = dest;
+                            cand.off_s = os; cand.off_e = os + doff;
+                            cand.pre_s = ps; cand.pre_e = ps + dpre;
+                            cand.size = size;
+                            for (int q = 0; q < 4; ++q) cand.r[q] = r[q];
+                            if (better(cand, mine)) mine = cand;
+                        }
+                    }
+                    if (nst != st) a.st[c] = nst;
+                }
+            }
+            // stable in-block compaction of the live list into the other buffer
+            int64_t tot;
+            int64_t ex = block_exclusive_sum<int64_t>(keep ? 1 : 0, sm_scan, &tot);
+            if (keep) lout[seg0 + kept_total + ex] = c;
+            kept_total += tot;
+        }
+        block_best(mine, sm_best);
+        if (threadIdx.x == 0) {
+            a.blk_best[b] = mine;
+            s_seg_len = kept_total;
+            s_list_par ^= 1;
+        }
+        grid.sync();
+
+        // ---- phase C: global argmax (redundant per block) and commit
+        {
+            Best w{};
+            w.benefit = 0;
+            for (int j = threadIdx.x; j < G; j += blockDim.x) {
+                Best o = a.blk_best[j];
+                if (better(o, w)) w = o;
+            }
+            block_best(w, sm_best);
+            if (threadIdx.x == 0) {
+                s_win = w;
+                if (b == 0) a.scalars[PS_ROUNDS] = round + 1;
+            }
+            __syncthreads();
+        }
+        const Best w = s_win;
+        if (w.benefit == 0) break;  // planner.py:311-312 no viable candidate
+        const int q0 = w.dest == TIO_DEST_SSD ? 0 : 2;
+        // new bookings, sorted: (-period, 0, +period)
+        int64_t ns[2][3], ne[2][3];
+        {
+            int64_t sh[3] = {-period, 0, period};
+            int k = 0;
+            for (int j = 0; j < 3; ++j) {
+                if (nb == 1 && j != 1) continue;
+                ns[0][k] = w.off_s + sh[j]; ne[0][k] = w.off_e + sh[j];
+                ns[1][k] = w.pre_s + sh[j]; ne[1][k] = w.pre_e + sh[j];
+                ++k;
+            }
+        }
+        // merge the bookings into the other buffer of both channels (all blocks)
+        for (int side = 0; side < 2; ++side) {
+            const int q = q0 + side;
+            const int64_t n = ch_n[q];
+            const int64_t *os = a.ch_s[q][ch_par[q]], *oe = a.ch_e[q][ch_par[q]];
+            int64_t *ds = a.ch_s[q][ch_par[q] ^ 1], *de = a.ch_e[q][ch_par[q] ^ 1];
+            for (int64_t i = (int64_t)b * blockDim.x + threadIdx.x; i <= n; i += (int64_t)G * blockDim.x) {
+                int64_t si = i < n ? ld_cg(os + i) : 0, ei = i < n ? ld_cg(oe + i) : 0;
+                int64_t sprev = i > 0 ? ld_cg(os + i - 1) : 0, eprev = i > 0 ? ld_cg(oe + i - 1) : 0;
+                int64_t cnt = 0;
+                for (int j = 0; j < nb; ++j) {
+                    const int64_t js = ns[side][j], je = ne[side][j];
+                    bool after_prev = i == 0 || sprev < js;
+                    bool before_cur = i == n || js < si;
+                    if (after_prev && before_cur) {
+                        ds[i + j] = js; de[i + j] = je;
+                        if ((i > 0 && eprev > js) || (i < n && je > si))
+                            a.scalars[PS_INVARIANT] = 1;   // App. A-9 disjointness violated
+                    }
+                    if (i < n && js < si) ++cnt;
+                }
+                if (i < n) { ds[i + cnt] = si; de[i + cnt] = ei; }
+            }
+        }
+        // residual update on this block's kernel chunk (planner.py:322-324)
+        {
+            int32_t flips = 0;
+            for (int rq = 0; rq < 4; rq += 2) {
+                int64_t lo = w.r[rq], hi = w.r[rq + 1];
+                if (lo > hi) continue;
+                if (lo < x0) lo = x0;
+                if (hi > x1 - 1) hi = x1 - 1;
+                if (hi > N - 1) hi = N - 1;
+                for (int64_t k = lo + threadIdx.x; k <= hi; k += blockDim.x) {
+                    int64_t old = ld_cg(&a.resid[k]);
+                    int64_t nw = old - w.size;
+                    a.resid[k] = nw;
+                    if (old > cap && nw <= cap) ++flips;
+                }
+            }
+            int32_t tf = block_sum<int32_t>(flips, reinterpret_cast<int32_t *>(sm_scan));
+            __syncthreads();
+            if (tf) {
+                rebuild_chunk();
+                if (threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_CRIT], -(int64_t)tf);
+            }
+        }
+        // block 0: commit record, host occupancy, mark the winner gone
+        if (b == 0 && threadIdx.x == 0) {
+            int64_t j = a.scalars[PS_COMMITS];
+            tio_commit cm;
+            cm.tensor_id = a.c_tid[w.idx];
+            cm.tensor_pos = a.c_tpos[w.idx];
+            cm.start_kernel = a.c_sk[w.idx];
+            cm.end_kernel = a.c_ek[w.idx];
+            cm.wraps = a.c_wraps[w.idx];
+            cm.destination = w.dest;
+            cm.off_start = w.off_s; cm.off_end = w.off_e;
+            cm.pre_start = w.pre_s; cm.pre_end = w.pre_e;
+            cm.benefit_lo = (uint64_t)w.benefit;
+            cm.benefit_hi = (uint64_t)(w.benefit >> 64);
+            cm.cost = w.cost;
+            cm.rel0_lo = w.r[0]; cm.rel0_hi = w.r[1]; cm.rel1_lo = w.r[2]; cm.rel1_hi = w.r[3];
+            a.commits[j] = cm;
+            a.scalars[PS_COMMITS] = j + 1;
+            a.st[w.idx] = (int8_t)(ld_cg(&a.st[w.idx]) | ST_GONE);
+            if (w.dest == TIO_DEST_CPU) {
+                int64_t h = s_nocc;
+                a.occ_s[h] = w.off_e; a.occ_e[h] = w.pre_s; a.occ_size[h] = w.size;
+                a.scalars[PS_OCC] = h + 1;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            last.dest = w.dest;
+            for (int j = 0; j < nb; ++j) {
+                last.off_s[j] = ns[0][j]; last.off_e[j] = ne[0][j];
+                last.pre_s[j] = ns[1][j]; last.pre_e[j] = ne[1][j];
+            }
+            last.occ_s = w.off_e; last.occ_e = w.pre_s;
+            if (w.dest == TIO_DEST_CPU) s_nocc += 1;
+            ch_n[q0] += nb; ch_n[q0 + 1] += nb;
+            ch_par[q0] ^= 1; ch_par[q0 + 1] ^= 1;
+        }
+        grid.sync();
+    }
+}
+
+int plan_loop_grid(int *blocks) {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0, sms = 0, per_sm = 0;
+        TIO_CUDA(cudaGetDevice(&dev));
+        TIO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        TIO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_loop_kernel, PLAN_THREADS, 0));
+        if (per_sm < 1) return fail(TIO_ERR_CUDA, "planner kernel cannot be resident");
+        cached = sms * (per_sm < 2 ? per_sm : 2);
+        if (cached > MAXG) cached = MAXG;
+    }
+    *blocks = cached;
+    return TIO_OK;
+}
+
+int launch_plan_loop(const PlanArgs &args, int blocks, cudaStream_t stream) {
+    void *params[] = {const_cast<PlanArgs *>(&args)};
+    TIO_CUDA(cudaLaunchCooperativeKernel((const void *)plan_loop_kernel, dim3(blocks), dim3(PLAN_THREADS),
+                                         params, 0, stream));
+    return TIO_OK;
+}
+
+}  // namespace tio

@@ -1,0 +1,72 @@
+// planner.cuh — on-device Algorithm 1 (reference planner.py:267-370).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace tio {
+
+constexpr int PLAN_THREADS = 256;
+
+// candidate SSD/host evaluation state (2 bits each in st[c])
+enum : int { S_UNK = 0, S_OK = 1, S_DEAD = 2 };                   // SSD path
+enum : int { H_UNK = 0, H_OK = 1, H_CAPFAIL = 2, H_DEAD = 3 };    // host path
+constexpr int8_t ST_GONE = (int8_t)0x40;  // committed or permanently useless
+
+// planner scalars[] slots
+enum {
+    PS_COMMITS = 0, PS_ROUNDS = 1, PS_CRIT = 2, PS_STATUS = 3, PS_OCC = 4,
+    PS_UNSAT_K = 5, PS_UNSAT_B = 6, PS_INVARIANT = 7, PS_COUNT = 8
+};
+
+// best candidate of a block (and, after the grid reduction, of the round)
+struct Best {
+    u128 benefit;          // 0 = none
+    int64_t cost;
+    int64_t idx;           // candidate index (planner order); tie-break
+    int64_t dest;          // TIO_DEST_*
+    int64_t off_s, off_e, pre_s, pre_e;
+    int64_t size;
+    int32_t r[4];
+};
+
+struct PlanArgs {
+    int64_t N, P, iteration, capacity, host_cap;
+    int32_t has_host;
+    int32_t chunk;                 // kernels per chunk (crit prefix / residual ownership)
+    // immutable per-kernel data
+    const int64_t *starts;         // [N+1]
+    const int64_t *dur;            // [N]
+    // residual pressure
+    int64_t *resid;                // [N]
+    int64_t *local_cp;             // [N+1] prefix of dur*[resid>cap] within each chunk
+    int64_t *chunk_sum;            // [grid]
+    // candidates (immutable, planner order)
+    const int64_t *c_size;
+    const int32_t *c_sk, *c_ek, *c_first, *c_last;
+    const int8_t *c_wraps;
+    const int64_t *c_ready, *c_deadline;
+    const int64_t *c_d;            // [4P] ssd_off, ssd_pre, host_off, host_pre
+    // candidate state
+    int8_t *st;                    // [P]
+    int64_t *place;                // [4P] ssd_off_s, ssd_pre_s, host_off_s, host_pre_s
+    int32_t *rng;                  // [4P]
+    int32_t *list0, *list1;        // [P] alive lists (per-block segments)
+    // channels: 4 channels (ssd.off, ssd.pre, host.off, host.pre) x 2 buffers
+    int64_t *ch_s[4][2];
+    int64_t *ch_e[4][2];
+    int64_t ch_cap;
+    // host occupancy intervals (CPU commits)
+    int64_t *occ_s, *occ_e, *occ_size;
+    // reduction + outputs
+    Best *blk_best;                // [grid]
+    tio_commit *commits;           // [P]
+    int64_t *scalars;              // [PS_COUNT]
+    const int64_t *c_tid;          // [P] tensor id per candidate (for commit records)
+    const int32_t *c_tpos;         // [P]
+};
+
+int plan_loop_grid(int *blocks);
+int launch_plan_loop(const PlanArgs &args, int blocks, cudaStream_t stream);
+
+}  // namespace tio
