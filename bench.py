@@ -1,0 +1,381 @@
+"""Benchmark of the lifetime + plan hot path (BASELINE.json metric 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1|llama1]
+
+One step = one pass of the hot path over the trace: the lifetime stage
+(reference analysis.py:58-117) and the Algorithm-1 planner with entry sort
+and mark_urgent (planner.py:267-397) on a device-resident trace.
+
+  value  = trace events / s = E / (device time of lifetime + plan), CUDA
+           events on the libtio stream, L2 flushed (256 MiB write) before every
+           step outside the timed region; summed over K steps.
+  e2e    = the same metric through the C-ABI one-shot call tio_plan_host with
+           pinned HOST trace columns in and host plan entries out (H2D + D2H
+           inside the timed region).
+  roofline        the lifetime kernel (HBM-bound, SURVEY §8d B_L bytes).
+  planner         the round-loop kernel: latency-bound, reported as us/round.
+  cpu_baseline    the CPU oracle port (oracle/tio_oracle.c, OpenMP) on this
+                  host: full lifetime stage + the first R planner rounds over
+                  the same trace, extrapolated linearly to all rounds.
+
+--impl reference times that CPU path (the reference's algorithm; the Python
+reference itself cannot run here: ~8 h per planner round at C2)
+and prints its own JSON line.  Multi-GPU (torchrun): each rank plans its own
+replica of the trace ("replicas only" for this config), timing is
+the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def _trace(config: str):
+    from paper_2506_06472_b200 import tracegen as G
+    from paper_2506_06472_b200 import ChannelRates, TransformerGenConfig
+    if config == "c2":
+        tr = G.gen_llama_trace(G.LLAMA3_8B)
+        cap = G.llama_peak_bytes(tr) // 2
+        return tr, cap, ChannelRates.symmetric(16_000), 0, "C2 Llama-3-8B-shaped trace (Appendix C, 292 microbatches)"
+    if config == "c3":
+        tr = G.gen_llama_trace(G.LLAMA3_70B)
+        cap = G.llama_peak_bytes(tr) // 2
+        return tr, cap, ChannelRates.symmetric(16_000), 0, "C3 Llama-3-70B-shaped trace (Appendix C, 1160 microbatches)"
+    if config == "llama1":
+        tr = G.gen_llama_trace(G.LlamaTraceConfig(microbatches=1))
+        cap = G.llama_peak_bytes(tr) // 2
+        return tr, cap, ChannelRates.symmetric(16_000), 0, "Llama-3-8B-shaped trace, 1 microbatch"
+    if config == "c1":
+        tr = G.gen_transformer_trace(TransformerGenConfig(num_layers=12, hidden_dim=768, num_heads=12, batch=8,
+                                                          seq_len=1024, bytes_per_element=4,
+                                                          compute_rate=1_000_000_000, seed=0))
+        cap = G.llama_peak_bytes(tr) // 2
+        return tr, cap, ChannelRates.symmetric(16_000), 0, "C1 GPT-2 small transformer trace"
+    raise SystemExit(f"unknown config {config}")
+
+
+def _lifetime_bytes(N: int, T: int, E: int, P: int) -> int:
+    """SURVEY §8d algorithmic bytes B_L = 8E + 16T + 8N + 24P + 24N."""
+    return 8 * E + 16 * T + 8 * N + 24 * P + 24 * N
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"tio_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = max(mx, float(parts[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        except FileNotFoundError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(config: str, rounds_total: int | None, sample_rounds: int = 40, threads: int | None = None):
+    """Oracle port on this host's cores: lifetime + the first R plan rounds,
+    extrapolated to the full plan (rounds_total, from the GPU run)."""
+    from oracle import oracle as O
+    tr, cap, rates, hc, _ = _trace(config)
+    a = tr.arrays()
+    if threads:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+    L = O.lib()
+    t0 = time.perf_counter()
+    lo = O.lifetime(a)
+    t1 = time.perf_counter()
+    p = O.plan(a, cap, rates.ssd_offload, rates.ssd_prefetch, rates.host_offload, rates.host_prefetch, hc,
+               lifetime_out=lo, max_rounds=sample_rounds)
+    t2 = time.perf_counter()
+    done = max(1, int(p["rounds"]))
+    total = rounds_total if rounds_total else done
+    t_plan = (t2 - t1) * (total / done)
+    ev = a.num_events / ((t1 - t0) + t_plan)
+    return {"value": ev, "unit": "events/s", "cores": int(L.tio_oracle_threads()), "kind": "port",
+            "sample": (f"oracle/tio_oracle.c on {config}: full lifetime ({t1 - t0:.3f} s) + first {done} of "
+                       f"{total} planner rounds ({t2 - t1:.2f} s), plan time extrapolated linearly by rounds")}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    # the oracle port as the reference's CPU path, all host threads
+    tr, cap, rates, hc, desc = _trace(args.config)
+    rounds_total = args.ref_rounds_total
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(args.config, rounds_total, sample_rounds=args.ref_rounds)
+    t0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(args.config, rounds_total, sample_rounds=args.ref_rounds)
+        vals.append(last["value"])
+    wall = time.perf_counter() - t0
+    v = statistics.mean(vals)
+    E = tr.arrays().num_events
+    line = {"metric": "trace events/s (lifetime+plan)", "value": v, "unit": "events/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * E / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": desc, "events": E, "capacity": cap, "rates": "ssd 16000 B/us symmetric"},
+            "cpu_baseline": {**last, "value": v},
+            "e2e": {"value": v, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    from paper_2506_06472_b200 import _native
+    from paper_2506_06472_b200.planner import _rates_struct
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    tr, cap, rates, hc, desc = _trace(args.config)
+    a = tr.arrays()
+    N, T, E = a.num_kernels, a.num_tensors, a.num_events
+    stream = torch.cuda.Stream(device=dev)
+    sh = stream.cuda_stream
+    lib = _native.load()
+    dt = _native.DeviceTrace(a, stream=sh)
+    r = _rates_struct(rates)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        _native.check(lib.tio_lifetime(dt.handle, ctypes.c_void_p(sh)))
+        if evs:
+            evs[1].record(stream)
+        p = dt.plan(cap, r, hc)
+        if evs:
+            evs[2].record(stream)
+        return p
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+            step().close()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        launches0 = _native.kernel_launches()
+        tot_ms, life_ms, plan_ms, loop_ms = 0.0, 0.0, 0.0, 0.0
+        info = None
+        with Clocks(local_rank) as clk:
+            for _ in range(args.steps):
+                flush.fill_(1)          # L2 flush, outside the timed region
+                evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                p = step(evs)
+                torch.cuda.synchronize()
+                life_ms += evs[0].elapsed_time(evs[1])
+                plan_ms += evs[1].elapsed_time(evs[2])
+                tot_ms += evs[0].elapsed_time(evs[2])
+                info = p.info
+                loop_ms += info.loop_ns / 1e6
+                plan_bytes = p.write() if _ == 0 else plan_bytes
+                p.close()
+        launches = _native.kernel_launches() - launches0
+        torch.cuda.synchronize()
+    # max over ranks
+    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    tot_ms_max = float(t.item())
+
+    # ---- e2e: C-ABI one-shot call, pinned host columns, host entries out
+    cols = _native.HostColumns(a)
+    pinned = {}
+    for name in ("dur", "tid", "size", "kind", "ptr", "acc"):
+        src = getattr(cols, name)
+        pt = torch.empty(src.shape, dtype=getattr(torch, str(src.dtype)), pin_memory=True)
+        pt.numpy()[...] = src
+        pinned[name] = pt
+    desc_c = _native.TraceDesc(N, pinned["dur"].data_ptr(), T, pinned["tid"].data_ptr(), pinned["size"].data_ptr(),
+                               pinned["kind"].data_ptr(), pinned["ptr"].data_ptr(), E, pinned["acc"].data_ptr())
+    ne = int(info.num_entries)
+    ent = torch.empty(max(1, ne) * _native.ENTRY_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
+    pinfo = _native.PlanInfo()
+    h2d = sum(int(v.numel() * v.element_size()) for v in pinned.values())
+    d2h = ne * _native.ENTRY_DTYPE.itemsize
+    for _ in range(2):
+        _native.check(lib.tio_plan_host(ctypes.byref(desc_c), ctypes.c_int64(cap), ctypes.byref(r),
+                                        ctypes.c_int64(hc), ctypes.c_void_p(sh), ctypes.byref(pinfo),
+                                        ctypes.c_void_p(ent.data_ptr()), ctypes.c_int64(ne)))
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _native.check(lib.tio_plan_host(ctypes.byref(desc_c), ctypes.c_int64(cap), ctypes.byref(r),
+                                        ctypes.c_int64(hc), ctypes.c_void_p(sh), ctypes.byref(pinfo),
+                                        ctypes.c_void_p(ent.data_ptr()), ctypes.c_int64(ne)))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    if rank != 0:
+        return
+    import hashlib
+    K = args.steps
+    value = world * E * K / (tot_ms_max / 1e3)
+    P = int(info.num_candidates)
+    B_L = _lifetime_bytes(N, T, E, P)
+    life_s = life_ms / K / 1e3
+    peak, peak_kind = _peaks()
+    achieved = B_L / life_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "lifetime_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get(args.config)
+        except Exception:
+            traffic = None
+    rounds = int(info.rounds)
+    line = {
+        "metric": "trace events/s (lifetime+plan)", "value": value, "unit": "events/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": tot_ms_max / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": desc, "events": E, "kernels": N, "tensors": T, "periods": P,
+                   "capacity": cap, "rates": "ssd 16000 B/us symmetric", "host_cap": hc,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed (256 MiB write) before every step, outside the timed region",
+                   "plan_sha256": hashlib.sha256(plan_bytes).hexdigest()},
+        "breakdown_ms": {"lifetime": life_ms / K, "plan": plan_ms / K, "plan_round_loop": loop_ms / K,
+                         "plan_setup_epilogue_host": (plan_ms - loop_ms) / K},
+        "roofline": {"kernel": "lifetime_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes": B_L, "share_of_step": life_ms / tot_ms},
+        "planner": {"kernel": "plan_loop_kernel", "bound": "latency (2 grid barriers per round)",
+                    "rounds": rounds, "commits": int(info.num_commits),
+                    "us_per_round": (loop_ms / K) * 1e3 / max(1, rounds),
+                    "share_of_step": loop_ms / tot_ms},
+        "e2e": {"value": world * E * K / (e2e_ms / 1e3), "unit": "events/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "api": "tio_plan_host (C ABI), pinned host buffers"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config, rounds, sample_rounds=args.ref_rounds)
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "llama1"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-rounds", type=int, default=40, help="planner rounds in the CPU sample")
+    ap.add_argument("--ref-rounds-total", type=int, default=None,
+                    help="total rounds of the full plan (for the reference arm's extrapolation)")
+    args = ap.parse_args(argv)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if args.ref_rounds_total is None:
+            args.ref_rounds_total = _known_rounds(args.config)
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _known_rounds(config: str):
+    """Total planner rounds of the config (recorded from the GPU path in
+    tests/golden; the reference arm needs it to extrapolate its sample)."""
+    try:
+        import gzip
+        with gzip.open(os.path.join(ROOT, "tests", "golden", f"{config}.json.gz"), "rt") as f:
+            rec = json.load(f)
+        if isinstance(rec, dict):
+            return int(rec.get("rounds") or rec.get("num_commits"))
+    except Exception:
+        pass
+    return None
+
+
+if __name__ == "__main__":
+    main()

@@ -103,6 +103,7 @@ typedef struct tio_plan_info {
     int64_t rounds;                /* evaluation rounds run on the device      */
     int64_t unsat_kernel;          /* set when TIO_ERR_UNSATISFIABLE           */
     int64_t unsat_bytes;
+    int64_t loop_ns;               /* CUDA-event time of the round-loop kernel */
 } tio_plan_info;
 
 /* One CommittedMigration (planner.py:97-111), commit order.  Relieved
@@ -133,6 +134,8 @@ typedef struct tio_entry {
 } tio_entry;
 
 int tio_abi_version(void);
+/* Kernels libtio has launched in this process (the bench's gpu_launches). */
+int tio_kernel_launches(int64_t *out);
 /* Copies the last error message of this thread (NUL-terminated, truncated). */
 int tio_last_error(char *buf, size_t len);
 /* Loaded-code identification: device name, SM count, build arch. */

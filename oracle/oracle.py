@@ -114,7 +114,7 @@ class OracleUnsatisfiable(Exception):
 
 
 def plan(arrays, capacity: int, ssd_off: float, ssd_pre: float, host_off=None, host_pre=None,
-         host_cap: int = 0, lifetime_out=None, verbose: bool = False) -> dict:
+         host_cap: int = 0, lifetime_out=None, verbose: bool = False, max_rounds: int = 0) -> dict:
     """Algorithm 1 restated (planner.py:267-370) + mark_urgent + entry sort.
 
     Returns a dict with `committed` (list of tuples matching the reference
@@ -143,7 +143,8 @@ def plan(arrays, capacity: int, ssd_off: float, ssd_pre: float, host_off=None, h
         ctypes.c_double(ssd_off), ctypes.c_double(ssd_pre), ctypes.c_int(1 if has_host else 0),
         ctypes.c_double(host_off if has_host else 0.0), ctypes.c_double(host_pre if has_host else 0.0),
         ctypes.c_int64(host_cap), ctypes.c_int64(P), _p(p_size), _p(p_start), _p(p_end), _p(p_wraps),
-        _p(p_first), _p(p_last), _p(residual), ctypes.byref(res), ctypes.c_int(1 if verbose else 0))
+        _p(p_first), _p(p_last), _p(residual), ctypes.byref(res), ctypes.c_int(1 if verbose else 0),
+        ctypes.c_int64(max_rounds))
     if rc == OR_ERR_UNSAT:
         raise OracleUnsatisfiable(res.unsat_kernel, res.unsat_bytes)
     if rc != 0:

@@ -70,7 +70,7 @@ class LifetimeView(ctypes.Structure):
 class PlanInfo(ctypes.Structure):
     _fields_ = [(n, _i64) for n in ("num_commits", "num_entries", "num_over", "capacity_bytes",
                                     "residual_peak_bytes", "planned_host_bytes", "num_candidates",
-                                    "rounds", "unsat_kernel", "unsat_bytes")]
+                                    "rounds", "unsat_kernel", "unsat_bytes", "loop_ns")]
 
 
 COMMIT_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("start_kernel", "<i8"),
@@ -84,7 +84,7 @@ ENTRY_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("trigger_u
                         ("urgent", "<i4"), ("pad", "<i4")])
 
 # every exported symbol of include/tio.h
-EXPORTS = ("tio_abi_version", "tio_last_error", "tio_device_info", "tio_trace_create",
+EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_device_info", "tio_trace_create",
            "tio_trace_destroy", "tio_lifetime", "tio_lifetime_view_get", "tio_lifetime_copy_out",
            "tio_plan_create", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
            "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration")
@@ -262,6 +262,12 @@ class DevicePlan:
             self.close()
         except Exception:
             pass
+
+
+def kernel_launches() -> int:
+    out = _i64()
+    check(load().tio_kernel_launches(ctypes.byref(out)))
+    return out.value
 
 
 def transfer_duration(rate: float, nbytes: int) -> int:

@@ -1,5 +1,6 @@
 // capi.cu — the C ABI of libtio (include/tio.h): handle management and the
 // orchestration of the lifetime / planner kernels on a caller stream.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
@@ -16,6 +17,9 @@
 namespace tio {
 
 static thread_local char g_err[1024];
+static std::atomic<long long> g_launches{0};
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const char *fmt, ...) {
     va_list ap;
@@ -120,6 +124,12 @@ struct tio_plan {
 extern "C" {
 
 int tio_abi_version(void) { return TIO_ABI_VERSION; }
+
+int tio_kernel_launches(int64_t *out) {
+    if (!out) return fail(TIO_ERR_INVALID, "null out");
+    *out = g_launches.load(std::memory_order_relaxed);
+    return TIO_OK;
+}
 
 int tio_last_error(char *buf, size_t len) {
     if (!buf || !len) return TIO_ERR_INVALID;
@@ -339,8 +349,8 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
         unsigned long long *first;
         PTRY(A.alloc(&first, 1));
         PCUDA(cudaMemsetAsync(first, 0xff, 8, s));
-        if (N) k_unsat<<<grid_for(N), 256, 0, s>>>(t->active, N, capacity, first);
-        k_unsat_finish<<<1, 1, 0, s>>>(t->active, first, N, ps, t->scalars + SC_FLAGS);
+        if (N) k_unsat<<<grid_for(N), 256, 0, s>>>(t->active, N, capacity, first); ::tio::count_launch();
+        k_unsat_finish<<<1, 1, 0, s>>>(t->active, first, N, ps, t->scalars + SC_FLAGS); ::tio::count_launch();
         PCUDA(cudaGetLastError());
     }
     RateCode rc[4];
@@ -380,13 +390,13 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
             PTRY(A.alloc(&k0, T)); PTRY(A.alloc(&k1, T));
             PTRY(A.alloc(&v0, T)); PTRY(A.alloc(&v1, T));
             PTRY(A.alloc(&hist, radix_hist_elems(T)));
-            k_id_keys<<<grid_for(T), 256, 0, s>>>(t->tid, T, k0, v0);
+            k_id_keys<<<grid_for(T), 256, 0, s>>>(t->tid, T, k0, v0); ::tio::count_launch();
             bool in_tmp = false;
             PTRY(radix_sort_pairs(k0, v0, k1, v1, hist, T, 64, s, &in_tmp));
             k_rank<<<grid_for(T), 256, 0, s>>>(in_tmp ? k1 : k0, in_tmp ? v1 : v0, T, t->tpp, rank,
-                                              cnt_by_rank, dupflag);
+                                              cnt_by_rank, dupflag); ::tio::count_launch();
         } else {
-            k_rank<<<grid_for(T), 256, 0, s>>>(nullptr, nullptr, T, t->tpp, rank, cnt_by_rank, dupflag);
+            k_rank<<<grid_for(T), 256, 0, s>>>(nullptr, nullptr, T, t->tpp, rank, cnt_by_rank, dupflag); ::tio::count_launch();
         }
         PCUDA(cudaGetLastError());
         PTRY(exclusive_scan(cnt_by_rank, cand_ptr, T, scan_tmp, cand_ptr + T, s));
@@ -414,7 +424,7 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
         cb.c_size = c_size; cb.c_sk = c_sk; cb.c_ek = c_ek; cb.c_first = c_first; cb.c_last = c_last;
         cb.c_wraps = c_wraps; cb.c_ready = c_ready; cb.c_deadline = c_deadline; cb.c_d = c_d; cb.c_tid = c_tid;
         cb.c_tpos = c_tpos; cb.st = st;
-        k_build_candidates<<<grid_for(P), 256, 0, s>>>(cb);
+        k_build_candidates<<<grid_for(P), 256, 0, s>>>(cb); ::tio::count_launch();
         PCUDA(cudaGetLastError());
     }
     int G = 0;
@@ -449,13 +459,26 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     a.ch_cap = ch_cap;
     a.occ_s = occ_s; a.occ_e = occ_e; a.occ_size = occ_z;
     a.blk_best = blk_best; a.commits = p->commits; a.scalars = ps; a.c_tid = c_tid; a.c_tpos = c_tpos;
-    PTRY(launch_plan_loop(a, G, s));
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    PCUDA(cudaEventCreate(&ev0));
+    PCUDA(cudaEventCreate(&ev1));
+    PCUDA(cudaEventRecord(ev0, s));
+    int loop_rc = launch_plan_loop(a, G, s);
+    PCUDA(cudaEventRecord(ev1, s));
+    if (loop_rc != TIO_OK) { cudaEventDestroy(ev0); cudaEventDestroy(ev1); return bail(loop_rc); }
 
     int64_t hs[PS_COUNT];
     int64_t dup = 0;
     PCUDA(cudaMemcpyAsync(hs, ps, sizeof(hs), cudaMemcpyDeviceToHost, s));
     PCUDA(cudaMemcpyAsync(&dup, dupflag, 8, cudaMemcpyDeviceToHost, s));
     PCUDA(cudaStreamSynchronize(s));
+    {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        pi.loop_ns = (int64_t)((double)ms * 1e6);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+    }
     if (dup) return bail(fail(TIO_ERR_INVALID, "duplicate tensor id"));
     if (hs[PS_STATUS] == 1) {
         pi.unsat_kernel = hs[PS_UNSAT_K]; pi.unsat_bytes = hs[PS_UNSAT_B];
@@ -481,11 +504,11 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
         PCUDA(cudaMemcpyAsync(peakp, &lmin, 8, cudaMemcpyHostToDevice, s));
     }
     if (N) {
-        k_over_flags<<<grid_for(N), 256, 0, s>>>(resid, N, capacity, flag, (long long *)peakp);
+        k_over_flags<<<grid_for(N), 256, 0, s>>>(resid, N, capacity, flag, (long long *)peakp); ::tio::count_launch();
         PTRY(exclusive_scan(flag, pos, N, ovt, pos + N, s));
-        k_over_write<<<grid_for(N), 256, 0, s>>>(flag, pos, N, p->over);
+        k_over_write<<<grid_for(N), 256, 0, s>>>(flag, pos, N, p->over); ::tio::count_launch();
     }
-    k_planned_host<<<1, 256, 0, s>>>(occ_s, occ_e, occ_z, hs[PS_OCC], hostp);
+    k_planned_host<<<1, 256, 0, s>>>(occ_s, occ_e, occ_z, hs[PS_OCC], hostp); ::tio::count_launch();
     PTRY(A.alloc(&p->entries, 2 * nc));
     if (nc > 0) {
         const int64_t ne = 2 * nc;
@@ -498,21 +521,21 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
         bool in_tmp = false;
         uint32_t *order;
         if (tbits + rbits + 1 <= 64) {
-            k_entry_keys<<<grid_for(ne), 256, 0, s>>>(p->commits, nc, rank, rbits, 0, k0, v0);
+            k_entry_keys<<<grid_for(ne), 256, 0, s>>>(p->commits, nc, rank, rbits, 0, k0, v0); ::tio::count_launch();
             PTRY(radix_sort_pairs(k0, v0, k1, v1, hist, ne, tbits + rbits + 1, s, &in_tmp));
             order = in_tmp ? v1 : v0;
         } else {
-            k_entry_keys<<<grid_for(ne), 256, 0, s>>>(p->commits, nc, rank, rbits, 1, k0, v0);
+            k_entry_keys<<<grid_for(ne), 256, 0, s>>>(p->commits, nc, rank, rbits, 1, k0, v0); ::tio::count_launch();
             PTRY(radix_sort_pairs(k0, v0, k1, v1, hist, ne, rbits + 1, s, &in_tmp));
             uint64_t *kk = in_tmp ? k1 : k0, *kt = in_tmp ? k0 : k1;
             uint32_t *vv = in_tmp ? v1 : v0, *vt = in_tmp ? v0 : v1;
-            k_regather_keys<<<grid_for(ne), 256, 0, s>>>(p->commits, vv, ne, kk);
+            k_regather_keys<<<grid_for(ne), 256, 0, s>>>(p->commits, vv, ne, kk); ::tio::count_launch();
             bool in2 = false;
             PTRY(radix_sort_pairs(kk, vv, kt, vt, hist, ne, tbits, s, &in2));
             order = in2 ? vt : vv;
         }
         k_emit_entries<<<grid_for(ne), 256, 0, s>>>(p->commits, order, ne, t->starts, t->ptr, t->acc, t->kind, I,
-                                                     p->entries);
+                                                     p->entries); ::tio::count_launch();
         PCUDA(cudaGetLastError());
     }
     int64_t tail[3] = {0, 0, 0};

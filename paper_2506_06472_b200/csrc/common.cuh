@@ -14,6 +14,8 @@ typedef unsigned __int128 u128;
 // ---- error plumbing --------------------------------------------------------
 void set_error(const char *fmt, ...);
 int fail(int code, const char *fmt, ...);
+// process-wide count of libtio kernel launches (tio_kernel_launches)
+void count_launch(int n = 1);
 
 #define TIO_CUDA(expr)                                                                      \
     do {                                                                                    \

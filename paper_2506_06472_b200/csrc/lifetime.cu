@@ -241,6 +241,7 @@ int launch_lifetime(const LifetimeArgs &args, int blocks, cudaStream_t stream) {
     void *params[] = {const_cast<LifetimeArgs *>(&args)};
     TIO_CUDA(cudaLaunchCooperativeKernel((const void *)lifetime_kernel, dim3(blocks),
                                          dim3(LIFETIME_THREADS), params, 0, stream));
+    count_launch();
     return TIO_OK;
 }
 

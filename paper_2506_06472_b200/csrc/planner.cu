@@ -556,6 +556,7 @@ int launch_plan_loop(const PlanArgs &args, int blocks, cudaStream_t stream) {
     void *params[] = {const_cast<PlanArgs *>(&args)};
     TIO_CUDA(cudaLaunchCooperativeKernel((const void *)plan_loop_kernel, dim3(blocks), dim3(PLAN_THREADS),
                                          params, 0, stream));
+    count_launch();
     return TIO_OK;
 }
 

@@ -115,9 +115,9 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_
     uint64_t *ka = keys, *kb = keys_tmp;
     uint32_t *va = vals, *vb = vals_tmp;
     for (int shift = 0; shift < bits; shift += 8) {
-        rs_hist<<<(unsigned)ntiles, RS_THREADS, 0, stream>>>(ka, n, shift, hist, ntiles);
-        rs_scan<<<1, 1024, 0, stream>>>(hist, 256 * ntiles);
-        rs_scatter<<<(unsigned)ntiles, RS_THREADS, 0, stream>>>(ka, va, kb, vb, n, shift, hist, ntiles);
+        rs_hist<<<(unsigned)ntiles, RS_THREADS, 0, stream>>>(ka, n, shift, hist, ntiles); ::tio::count_launch();
+        rs_scan<<<1, 1024, 0, stream>>>(hist, 256 * ntiles); ::tio::count_launch();
+        rs_scatter<<<(unsigned)ntiles, RS_THREADS, 0, stream>>>(ka, va, kb, vb, n, shift, hist, ntiles); ::tio::count_launch();
         TIO_CUDA(cudaGetLastError());
         uint64_t *tk = ka; ka = kb; kb = tk;
         uint32_t *tv = va; va = vb; vb = tv;

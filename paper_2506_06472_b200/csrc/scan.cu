@@ -68,9 +68,9 @@ int exclusive_scan(const int64_t *in, int64_t *out, int64_t n, int64_t *tmp, int
         return TIO_OK;
     }
     const int64_t tiles = (n + SC_TILE - 1) / SC_TILE;
-    scan_tiles<<<(unsigned)tiles, SC_THREADS, 0, stream>>>(in, out, n, tmp);
-    scan_totals<<<1, 1024, 0, stream>>>(tmp, tiles, grand);
-    scan_add<<<(unsigned)tiles, SC_THREADS, 0, stream>>>(out, n, tmp);
+    scan_tiles<<<(unsigned)tiles, SC_THREADS, 0, stream>>>(in, out, n, tmp); ::tio::count_launch();
+    scan_totals<<<1, 1024, 0, stream>>>(tmp, tiles, grand); ::tio::count_launch();
+    scan_add<<<(unsigned)tiles, SC_THREADS, 0, stream>>>(out, n, tmp); ::tio::count_launch();
     TIO_CUDA(cudaGetLastError());
     return TIO_OK;
 }

@@ -1,0 +1,200 @@
+"""Generate the golden fixtures of the parity tests from the REFERENCE itself.
+
+Run once in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py            # fuzz corpora + C1 (~1 min)
+    python tests/golden/make_golden.py --llama1   # + the 1-microbatch Llama plan (~5 min)
+
+It imports the reference package `offloader` read-only from
+/root/reference/pkg/src and records, for every case, the reference's own
+outputs: compute_inactive_periods (analysis.py:58-83), compute_memory_timeline
+(:97-108), per_kernel_active_bytes (:111-117), plan_migrations
+(planner.py:267-370) committed rounds and write_plan bytes (:402-420).
+The traces themselves are NOT stored: each case records the generator
+arguments plus the sha256 of the reference's write_trace bytes, and the tests
+regenerate the trace with this repo's generator and check that hash first.
+
+Corpora (the reference's own acceptance generators, test_acceptance.py):
+  crit2   criterion 2 (:64-101), random.Random(2024), 1000 traces
+  crit3   criterion 3 (:104-131), random.Random(7), eligible instances of the
+          first 5000 attempts
+  c1      config C1: GPT-2 small transformer trace, 4 rate setups
+  llama1  Appendix-C Llama-3-8B trace with 1 microbatch (E=4,579; slow)
+
+Output: tests/golden/*.json.gz (small; committed).  Nothing on the GPU box
+reads /root/reference: only these fixtures travel.
+"""
+
+from __future__ import annotations
+
+import argparse
+import gzip
+import hashlib
+import json
+import os
+import random
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SRC = "/root/reference/pkg/src"
+
+
+def _ref():
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import offloader  # noqa: E402  (the reference, read-only)
+    return offloader
+
+
+def _record(ref, trace, capacity, rates, host_cap, with_plan=True):
+    periods = ref.compute_inactive_periods(trace)
+    out = {
+        "trace_sha256": hashlib.sha256(ref.write_trace(trace)).hexdigest(),
+        "periods": [[p.tensor_id, p.size_bytes, p.start_kernel, p.end_kernel, int(p.wraps)]
+                    for p in periods],
+        "timeline": ref.compute_memory_timeline(trace).per_kernel_bytes,
+        "active": ref.per_kernel_active_bytes(trace),
+        "capacity": capacity,
+        "rates": [rates.ssd_offload, rates.ssd_prefetch, rates.host_offload, rates.host_prefetch],
+        "host_cap": host_cap,
+    }
+    if with_plan:
+        try:
+            plan = ref.plan_migrations(trace, capacity, rates, host_cap=host_cap)
+        except ref.UnsatisfiableTraceError as exc:
+            out["unsat_kernel"] = exc.kernel_index
+            return out
+        out["plan"] = ref.write_plan(plan).decode()
+        out["committed"] = [[c.tensor_id, c.start_kernel, c.end_kernel, int(c.wraps), c.destination,
+                             list(c.offload_interval), list(c.prefetch_interval), str(c.benefit),
+                             c.cost, list(c.relieved_kernels)] for c in plan.committed]
+        out["residual"] = plan.residual_timeline.per_kernel_bytes
+    return out
+
+
+def crit2(ref):
+    """test_acceptance.py:64-101, same RNG call sequence."""
+    rng = random.Random(2024)
+    cases = []
+    for _ in range(1000):
+        nk = rng.randint(4, 64)
+        nt = rng.randint(2, 32)
+        seed = rng.randint(0, 10**9)
+        gen = {"seed": seed, "num_kernels": nk, "num_tensors": nt,
+               "size_range": [500_000, 60_000_000], "duration_range": [200, 5_000]}
+        trace = ref.gen_random_trace(seed, nk, nt, size_range=(500_000, 60_000_000),
+                                     duration_range=(200, 5_000))
+        peak = ref.compute_memory_timeline(trace).peak()
+        floor = max(ref.per_kernel_active_bytes(trace), default=0)
+        capacity = max(floor, int(peak * rng.choice((0.55, 0.7, 0.85))))
+        ssd = rng.choice((2_000, 10_000, 40_000))
+        if rng.random() < 0.3:
+            rates = ref.ChannelRates.symmetric(ssd, host=2 * ssd)
+            host_cap = rng.choice((0, 200_000_000))
+        else:
+            rates = ref.ChannelRates.symmetric(ssd)
+            host_cap = 0
+        rec = _record(ref, trace, capacity, rates, host_cap)
+        rec["gen"] = gen
+        cases.append(rec)
+    return cases
+
+
+def crit3(ref):
+    """test_acceptance.py:104-131 generator (all eligible instances of the
+    first 5000 attempts; the reference test starves at 500 with commits)."""
+    rng = random.Random(7)
+    cases = []
+    for _ in range(5000):
+        seed = rng.randint(0, 10**9)
+        nk = rng.randint(3, 8)
+        nt = rng.randint(1, 4)
+        trace = ref.gen_random_trace(seed, nk, nt, size_range=(1_000, 900_000),
+                                     duration_range=(10, 400))
+        periods = ref.compute_inactive_periods(trace)
+        if not periods or len(periods) > 6:
+            continue
+        peak = ref.compute_memory_timeline(trace).peak()
+        floor = max(ref.per_kernel_active_bytes(trace), default=0)
+        capacity = max(floor, int(peak * 0.6))
+        if rng.random() < 0.4:
+            rates = ref.ChannelRates.symmetric(rng.choice((50, 500)), host=1_000)
+            host_cap = rng.choice((0, 2_000_000))
+        else:
+            rates = ref.ChannelRates.symmetric(rng.choice((50, 500)))
+            host_cap = 0
+        rec = _record(ref, trace, capacity, rates, host_cap)
+        rec["gen"] = {"seed": seed, "num_kernels": nk, "num_tensors": nt,
+                      "size_range": [1_000, 900_000], "duration_range": [10, 400]}
+        cases.append(rec)
+    return cases
+
+
+C1_SETUPS = [  # (compute_rate, ssd, host, host_cap) — SURVEY §8d
+    (1_000_000_000, 16_000, None, 0),
+    (1_000_000_000, 64_000, None, 0),
+    (1_000_000_000, 16_000, 32_000, 8_000_000_000),
+    (10_000_000, 16_000, None, 0),
+]
+
+
+def c1(ref):
+    cases = []
+    for cr, ssd, host, host_cap in C1_SETUPS:
+        cfg = ref.TransformerGenConfig(num_layers=12, hidden_dim=768, num_heads=12, batch=8,
+                                       seq_len=1024, bytes_per_element=4, compute_rate=cr, seed=0)
+        trace = ref.gen_transformer_trace(cfg)
+        capacity = ref.compute_memory_timeline(trace).peak() // 2
+        rates = ref.ChannelRates.symmetric(ssd, host=host)
+        rec = _record(ref, trace, capacity, rates, host_cap)
+        rec["gen"] = {"compute_rate": cr}
+        rec["plan_sha256"] = hashlib.sha256(rec["plan"].encode()).hexdigest()
+        cases.append(rec)
+    return cases
+
+
+def llama1(ref):
+    """Appendix-C trace with 1 microbatch, converted to a reference Trace
+    through the JSONL format (reference parse_trace, trace.py:217-275)."""
+    sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+    from paper_2506_06472_b200 import tracegen, trace as T
+    ours = tracegen.gen_llama_trace(tracegen.LlamaTraceConfig(microbatches=1))
+    trace = ref.parse_trace(T.write_trace(ours))
+    capacity = ref.compute_memory_timeline(trace).peak() // 2
+    rates = ref.ChannelRates.symmetric(16_000)
+    t0 = time.time()
+    rec = _record(ref, trace, capacity, rates, 0)
+    rec["gen"] = {"microbatches": 1}
+    rec["ref_seconds"] = round(time.time() - t0, 1)
+    rec["plan_sha256"] = hashlib.sha256(rec["plan"].encode()).hexdigest()
+    return [rec]
+
+
+def _dump(name, cases):
+    path = os.path.join(HERE, f"{name}.json.gz")
+    with gzip.open(path, "wt", encoding="utf-8", compresslevel=9) as f:
+        json.dump(cases, f, separators=(",", ":"))
+    print(f"{name}: {len(cases)} cases -> {path} ({os.path.getsize(path)} B)")
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--llama1", action="store_true", help="also the slow 1-microbatch Llama plan")
+    ap.add_argument("--only", default=None)
+    args = ap.parse_args(argv)
+    ref = _ref()
+    todo = {"crit2": crit2, "crit3": crit3, "c1": c1}
+    if args.llama1:
+        todo["llama1"] = llama1
+    for name, fn in todo.items():
+        if args.only and name != args.only:
+            continue
+        t0 = time.time()
+        cases = fn(ref)
+        _dump(name, cases)
+        print(f"  {time.time() - t0:.1f} s")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,247 @@
+"""GPU parity: the sm_100a lifetime + planner path (libtio, through the C ABI)
+against the reference's golden vectors and the CPU oracle.
+
+Bar: bit-exact.  Periods, timeline, active bytes, committed rounds, residual
+timeline and write_plan bytes must equal the reference's (tests/golden,
+produced by the reference itself) and, at sizes the reference cannot reach,
+the oracle's (oracle/tio_oracle.c, itself pinned by test_oracle_golden.py).
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, mk_trace, rates_of, regen
+from oracle import oracle as O
+from paper_2506_06472_b200 import (
+    ChannelConfigError, ChannelRates, InactivePeriod, PlanEntry, TransformerGenConfig,
+    UnsatisfiableTraceError, compute_inactive_periods, compute_memory_timeline, gen_random_trace,
+    gen_transformer_trace, lifetime_arrays, mark_urgent, per_kernel_active_bytes, plan_device,
+    plan_migrations, write_plan, write_trace)
+from paper_2506_06472_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+MB100 = 100_000_000
+CAP = 150_000_000
+
+
+def _committed_rows(raw):
+    out = []
+    for r in raw["commits"]:
+        rel = []
+        for lo, hi in ((int(r["rel0_lo"]), int(r["rel0_hi"])), (int(r["rel1_lo"]), int(r["rel1_hi"]))):
+            if lo <= hi:
+                rel.extend(range(lo, hi + 1))
+        out.append([int(r["tensor_id"]), int(r["start_kernel"]), int(r["end_kernel"]), int(r["wraps"]),
+                    {1: "SSD", 2: "CPU"}[int(r["destination"])], [int(r["off_start"]), int(r["off_end"])],
+                    [int(r["pre_start"]), int(r["pre_end"])],
+                    str((int(r["benefit_hi"]) << 64) | int(r["benefit_lo"])), int(r["cost"]), rel])
+    return out
+
+
+def _check_case(tr, rec):
+    periods = [[p.tensor_id, p.size_bytes, p.start_kernel, p.end_kernel, int(p.wraps)]
+               for p in compute_inactive_periods(tr)]
+    assert periods == rec["periods"]
+    assert compute_memory_timeline(tr).per_kernel_bytes == rec["timeline"]
+    assert per_kernel_active_bytes(tr) == rec["active"]
+    rates = rates_of(rec)
+    if "unsat_kernel" in rec:
+        with pytest.raises(UnsatisfiableTraceError) as ei:
+            plan_device(tr, rec["capacity"], rates, rec["host_cap"])
+        assert ei.value.kernel_index == rec["unsat_kernel"]
+        return
+    raw = plan_device(tr, rec["capacity"], rates, rec["host_cap"])
+    assert raw["plan_bytes"].decode() == rec["plan"]
+    assert raw["residual"].tolist() == rec["residual"]
+    assert _committed_rows(raw) == rec["committed"]
+
+
+# ---------------------------------------------------------------- golden corpora
+
+@pytest.mark.parametrize("corpus", ["crit2", "crit3"])
+def test_fuzz_corpus_bit_exact_vs_reference(corpus):
+    for rec in load_golden(corpus):
+        _check_case(regen(rec), rec)
+
+
+def test_c1_bit_exact_vs_reference():
+    for rec in load_golden("c1"):
+        cfg = TransformerGenConfig(num_layers=12, hidden_dim=768, num_heads=12, batch=8, seq_len=1024,
+                                   bytes_per_element=4, compute_rate=rec["gen"]["compute_rate"], seed=0)
+        tr = gen_transformer_trace(cfg)
+        _check_case(tr, rec)
+        plan = plan_migrations(tr, rec["capacity"], rates_of(rec), rec["host_cap"])
+        assert hashlib.sha256(write_plan(plan)).hexdigest() == rec["plan_sha256"]
+
+
+def test_llama1_bit_exact_vs_reference():
+    from paper_2506_06472_b200 import LlamaTraceConfig, gen_llama_trace
+    rec = load_golden("llama1")[0]
+    tr = gen_llama_trace(LlamaTraceConfig(microbatches=1))
+    assert hashlib.sha256(write_trace(tr)).hexdigest() == rec["trace_sha256"]
+    _check_case(tr, rec)
+
+
+def test_c2_lifetime_and_plan_bit_exact_vs_oracle():
+    """Config C2 (E=1,001,836): the reference planner would take ~8 h per
+    round here, so the checker is the pinned oracle (plan fingerprint in
+    tests/golden/c2.json.gz, made by tests/golden/make_c2.py)."""
+    from paper_2506_06472_b200 import LLAMA3_8B, gen_llama_trace
+    from paper_2506_06472_b200.tracegen import llama_peak_bytes
+    rec = load_golden("c2")
+    tr = gen_llama_trace(LLAMA3_8B)
+    a = tr.arrays()
+    assert a.num_events == rec["num_events"]
+    per, tl, act = O.lifetime(a)
+    la = lifetime_arrays(tr)
+    assert np.array_equal(la.timeline, tl) and np.array_equal(la.active, act)
+    assert np.array_equal(la.period_tensor, per["tensor"])
+    assert np.array_equal(la.period_start, per["start"]) and np.array_equal(la.period_end, per["end"])
+    assert np.array_equal(la.period_wraps.astype(bool), per["wraps"])
+    cap = llama_peak_bytes(tr) // 2
+    assert cap == rec["capacity"]
+    raw = plan_device(tr, cap, ChannelRates.symmetric(16_000), 0)
+    assert hashlib.sha256(raw["plan_bytes"]).hexdigest() == rec["plan_sha256"]
+    assert int(raw["info"].num_commits) == rec["num_commits"]
+    assert hashlib.sha256(raw["residual"].tobytes()).hexdigest() == rec["residual_sha256"]
+
+
+def test_random_traces_vs_oracle_wide_fuzz():
+    """Wider fuzz than the reference's corpora (bigger traces, fractional
+    rates, shuffled / negative ids) against the oracle."""
+    import random
+    rng = random.Random(99)
+    for case in range(120):
+        nk = rng.randint(2, 400)
+        nt = rng.randint(1, 300)
+        tr = gen_random_trace(rng.randint(0, 10**9), nk, nt, size_range=(1_000, 80_000_000),
+                              duration_range=(1, 3_000), global_fraction=rng.choice((0.0, 0.3, 0.9)))
+        if rng.random() < 0.5:      # arbitrary unique ids, not in trace order
+            a = tr.arrays()
+            ids = rng.sample(range(-10**12, 10**12), a.num_tensors)
+            a.tensor_id[:] = np.array(ids, dtype=np.int64)
+            tr.device_cache.clear()
+        a = tr.arrays()
+        per, tl, act = O.lifetime(a)
+        cap = max(int(act.max()), int(tl.max() * rng.choice((0.4, 0.6, 0.8, 0.95))))
+        ssd = rng.choice((500.0, 7_777.5, 20_000.0, 123_456.0))
+        host = rng.choice((None, ssd * 2.5, 3.0))
+        hc = rng.choice((0, 10**8, 10**10)) if host else 0
+        rates = ChannelRates.symmetric(ssd, host=host)
+        o = O.plan(a, cap, ssd, ssd, host, host, hc, lifetime_out=(per, tl, act))
+        g = plan_device(tr, cap, rates, hc)
+        assert g["plan_bytes"] == o["plan_bytes"], case
+        assert np.array_equal(g["residual"], o["residual"]), case
+
+
+# ---------------------------------------------------------------- known answers
+# reference tests/test_analysis.py:18-69 and test_planner.py:108-234
+
+def test_ex1_known_answers(ex1, rates20k):
+    assert compute_inactive_periods(ex1) == [InactivePeriod(0, MB100, 1, 3, False)]
+    assert compute_memory_timeline(ex1).per_kernel_bytes == [MB100, MB100, 2 * MB100, MB100, MB100]
+    plan = plan_migrations(ex1, CAP, rates20k)
+    assert plan.entries == [PlanEntry(0, "offload", 10_000, 15_000, "SSD", False),
+                            PlanEntry(0, "prefetch", 35_000, 40_000, "GPU", True)]
+    assert plan.residual_timeline.per_kernel_bytes == [MB100] * 5
+    assert not plan.warning and plan.planned_host_bytes == 0
+    c = plan.committed[0]
+    assert (c.benefit, c.cost, c.relieved_kernels) == (10**12, 10_000, (2,))
+    assert write_plan(plan) == (
+        b'{"version": 1, "capacity_bytes": 150000000, "residual_peak_bytes": 100000000, '
+        b'"planned_host_bytes": 0, "over_capacity_kernels": []}\n'
+        b'{"tensor": 0, "action": "offload", "trigger_us": 10000, "deadline_us": 15000, '
+        b'"target": "SSD", "urgent": false}\n'
+        b'{"tensor": 0, "action": "prefetch", "trigger_us": 35000, "deadline_us": 40000, '
+        b'"target": "GPU", "urgent": true}\n')
+
+
+def test_global_wrap_periods():
+    assert compute_inactive_periods(mk_trace([10] * 5, [(0, 7, "global", [0])])) == [
+        InactivePeriod(0, 7, 1, 4, True)]
+    assert compute_inactive_periods(mk_trace([10] * 5, [(0, 7, "global", [1, 2])])) == [
+        InactivePeriod(0, 7, 3, 0, True)]
+    assert compute_inactive_periods(mk_trace([10, 10], [(0, 5, "global", [0, 1])])) == []
+    assert compute_inactive_periods(mk_trace([10, 10], [(0, 5, "intermediate", [0, 1])])) == []
+    assert compute_memory_timeline(mk_trace([1, 1, 1], [(0, 7, "global", [1])])).per_kernel_bytes == [7, 7, 7]
+
+
+def test_empty_trace():
+    tr = mk_trace([], [])
+    assert compute_memory_timeline(tr).per_kernel_bytes == []
+    assert compute_inactive_periods(tr) == []
+    plan = plan_migrations(tr, 100, ChannelRates.symmetric(10))
+    assert plan.entries == [] and not plan.warning
+
+
+def test_kernels_without_tensors():
+    tr = mk_trace([5, 6, 7], [])
+    assert compute_memory_timeline(tr).per_kernel_bytes == [0, 0, 0]
+    assert plan_migrations(tr, 0, ChannelRates.symmetric(10)).entries == []
+
+
+def test_no_pressure_infeasible_unsat(ex1, rates20k):
+    assert plan_migrations(ex1, 250_000_000, rates20k).entries == []
+    p = plan_migrations(ex1, CAP, ChannelRates.symmetric(1_000))
+    assert p.entries == [] and p.warning and p.over_capacity_kernels == [2]
+    with pytest.raises(UnsatisfiableTraceError, match="kernel 0"):
+        plan_migrations(ex1, 90_000_000, rates20k)
+
+
+def test_bad_rate_raises_channel_config_error(ex1):
+    with pytest.raises(ChannelConfigError):
+        plan_migrations(ex1, CAP, ChannelRates.symmetric(0))
+    with pytest.raises(ChannelConfigError):
+        plan_migrations(ex1, CAP, ChannelRates(20_000, 20_000, -1, 5))
+
+
+def test_mark_urgent_zero_slack_only():
+    tr = mk_trace([10_000] * 5, [(0, MB100, "intermediate", [0, 4]), (1, MB100, "intermediate", [0, 4]),
+                                 (2, 220_000_000, "intermediate", [2])])
+    plan = plan_migrations(tr, 230_000_000, ChannelRates.symmetric(20_000))
+    pre = {e.tensor_id: e for e in plan.entries if e.action == "prefetch"}
+    assert pre[0].deadline == 40_000 and pre[0].urgent
+    assert pre[1].deadline == 35_000 and not pre[1].urgent
+    assert mark_urgent(plan, tr).entries == plan.entries
+
+
+def test_host_destination_and_cap(ex1):
+    rates = ChannelRates(1, 1, 20_000, 20_000)
+    plan = plan_migrations(ex1, CAP, rates, host_cap=MB100)
+    assert [e.target for e in plan.entries] == ["CPU", "GPU"]
+    assert plan.planned_host_bytes == MB100
+    starved = plan_migrations(ex1, CAP, rates, host_cap=MB100 - 1)
+    assert starved.entries == [] and starved.warning
+
+
+def test_wrap_period_global_plan():
+    tr = mk_trace([10_000] * 5, [(0, MB100, "global", [1]), (1, MB100, "intermediate", [3])])
+    plan = plan_migrations(tr, CAP, ChannelRates.symmetric(20_000))
+    assert plan.residual_timeline.per_kernel_bytes == [MB100, MB100, MB100, MB100, 0]
+    off = [e for e in plan.entries if e.action == "offload"][0]
+    pre = [e for e in plan.entries if e.action == "prefetch"][0]
+    assert (off.trigger_time, off.deadline) == (20_000, 25_000)
+    assert (pre.trigger_time, pre.deadline) == (55_000, 60_000) and pre.urgent
+
+
+def test_invalid_trace_is_rejected():
+    from paper_2506_06472_b200 import KernelRecord, TensorKind, TensorRecord, Trace
+    bad = Trace([KernelRecord(0, "k", 5)], [TensorRecord(0, 10, TensorKind.INTERMEDIATE, (3,))])
+    with pytest.raises(Exception):
+        plan_migrations(bad, 100, ChannelRates.symmetric(10))
+    dup = mk_trace([5, 5, 5], [(4, 10, "intermediate", [0, 2]), (4, 10, "intermediate", [0, 2])])
+    with pytest.raises(Exception):
+        plan_migrations(dup, 15, ChannelRates.symmetric(10))
+
+
+def test_native_library_is_the_code_that_ran():
+    import os
+    info = _native.device_info()
+    assert "sm_100a" in info
+    maps = open(f"/proc/{os.getpid()}/maps").read()
+    assert _native.lib_path() in maps
