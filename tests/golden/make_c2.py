@@ -1,0 +1,48 @@
+"""Fingerprint of the C2 plan computed by the CPU oracle (slow: tens of
+minutes on 8 cores; run once in the build container).
+
+The reference planner cannot run at C2 (~8 h per round), so the
+C2 checker is the oracle (oracle/tio_oracle.c), whose bit-exactness against
+the reference is pinned by tests/test_oracle_golden.py on the fuzz corpora,
+C1 and the 1-microbatch Llama trace.  Output: tests/golden/c2.json.gz.
+"""
+
+from __future__ import annotations
+
+import gzip
+import hashlib
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.abspath(os.path.join(HERE, "..", ".."))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    from oracle import oracle as O
+    from paper_2506_06472_b200 import LLAMA3_8B, gen_llama_trace, write_trace
+    from paper_2506_06472_b200.tracegen import llama_peak_bytes
+    tr = gen_llama_trace(LLAMA3_8B)
+    a = tr.arrays()
+    cap = llama_peak_bytes(tr) // 2
+    t0 = time.time()
+    p = O.plan(a, cap, 16000.0, 16000.0, verbose=True)
+    rec = {
+        "trace_sha256": hashlib.sha256(write_trace(tr)).hexdigest(),
+        "num_events": a.num_events, "capacity": cap, "rates": [16000, 16000, None, None], "host_cap": 0,
+        "rounds": int(p["rounds"]), "num_commits": len(p["committed"]),
+        "plan_sha256": hashlib.sha256(p["plan_bytes"]).hexdigest(),
+        "residual_sha256": hashlib.sha256(p["residual"].astype("<i8").tobytes()).hexdigest(),
+        "over_capacity_kernels": len(p["over_capacity_kernels"]),
+        "oracle_seconds": round(time.time() - t0, 1), "oracle_threads": int(O.lib().tio_oracle_threads()),
+    }
+    with gzip.open(os.path.join(HERE, "c2.json.gz"), "wt") as f:
+        json.dump(rec, f)
+    print(rec)
+
+
+if __name__ == "__main__":
+    main()

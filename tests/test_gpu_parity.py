@@ -234,8 +234,12 @@ def test_invalid_trace_is_rejected():
     bad = Trace([KernelRecord(0, "k", 5)], [TensorRecord(0, 10, TensorKind.INTERMEDIATE, (3,))])
     with pytest.raises(Exception):
         plan_migrations(bad, 100, ChannelRates.symmetric(10))
-    dup = mk_trace([5, 5, 5], [(4, 10, "intermediate", [0, 2]), (4, 10, "intermediate", [0, 2])])
-    with pytest.raises(Exception):
+    # duplicate ids pass straight to the device (no host validation): the
+    # library must refuse them (reference trace.py:136-141 invariant)
+    dup = Trace([KernelRecord(i, f"k{i}", 5) for i in range(3)],
+                [TensorRecord(4, 10, TensorKind.INTERMEDIATE, (0, 2)),
+                 TensorRecord(4, 10, TensorKind.INTERMEDIATE, (0, 2))])
+    with pytest.raises(_native.TioError, match="duplicate"):
         plan_migrations(dup, 15, ChannelRates.symmetric(10))
 
 
