@@ -406,12 +406,12 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     PlanArgs a;
     memset(&a, 0, sizeof(a));
     int64_t *c_size, *c_ready, *c_deadline, *c_d, *c_tid, *place;
-    int32_t *c_sk, *c_ek, *c_first, *c_last, *c_tpos, *rng, *list0, *list1;
+    int32_t *c_sk, *c_ek, *c_first, *c_last, *c_tpos, *rng;
     int8_t *c_wraps, *st;
     PTRY(A.alloc(&c_size, P)); PTRY(A.alloc(&c_ready, P)); PTRY(A.alloc(&c_deadline, P));
     PTRY(A.alloc(&c_d, 4 * P)); PTRY(A.alloc(&c_tid, P)); PTRY(A.alloc(&place, 4 * P));
     PTRY(A.alloc(&c_sk, P)); PTRY(A.alloc(&c_ek, P)); PTRY(A.alloc(&c_first, P)); PTRY(A.alloc(&c_last, P));
-    PTRY(A.alloc(&c_tpos, P)); PTRY(A.alloc(&rng, 4 * P)); PTRY(A.alloc(&list0, P)); PTRY(A.alloc(&list1, P));
+    PTRY(A.alloc(&c_tpos, P)); PTRY(A.alloc(&rng, 4 * P));
     PTRY(A.alloc(&c_wraps, P)); PTRY(A.alloc(&st, P));
     if (P > 0) {
         CandBuild cb;
@@ -427,6 +427,37 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
         k_build_candidates<<<grid_for(P), 256, 0, s>>>(cb); ::tio::count_launch();
         PCUDA(cudaGetLastError());
     }
+    // ---- tiles: candidates in ready-time order (planner.cu)
+    const int64_t ntiles = (P + TILE - 1) / TILE;
+    uint32_t *tcand;
+    int32_t *ctile, *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;
+    int64_t *t_lo, *t_hi;
+    Best *tile_best;
+    PTRY(A.alloc(&ctile, P));
+    PTRY(A.alloc(&t_lo, ntiles)); PTRY(A.alloc(&t_hi, ntiles));
+    PTRY(A.alloc(&t_ka_lo, ntiles)); PTRY(A.alloc(&t_ka_hi, ntiles));
+    PTRY(A.alloc(&t_kb_lo, ntiles)); PTRY(A.alloc(&t_kb_hi, ntiles));
+    PTRY(A.alloc(&tile_best, ntiles));
+    {
+        uint64_t *k0, *k1;
+        uint32_t *v0, *v1, *hist;
+        PTRY(A.alloc(&k0, P)); PTRY(A.alloc(&k1, P)); PTRY(A.alloc(&v0, P)); PTRY(A.alloc(&v1, P));
+        PTRY(A.alloc(&hist, radix_hist_elems(P)));
+        bool in_tmp = false;
+        if (P > 0) {
+            k_ready_keys<<<grid_for(P), 256, 0, s>>>(c_ready, P, k0, v0); ::tio::count_launch();
+            PTRY(radix_sort_pairs(k0, v0, k1, v1, hist, P, bitlen((uint64_t)(I > 0 ? I : 1)), s, &in_tmp));
+        }
+        tcand = in_tmp ? v1 : v0;
+        if (P > 0) {
+            k_tile_spans<<<grid_for(ntiles * 32), 256, 0, s>>>(tcand, P, ntiles, TILE, N, c_ready, c_deadline,
+                                                              c_wraps, c_sk, c_ek, c_first, c_last, ctile, t_lo,
+                                                              t_hi, t_ka_lo, t_ka_hi, t_kb_lo, t_kb_hi); ::tio::count_launch();
+        }
+        PCUDA(cudaGetLastError());
+    }
+    a.ntiles = ntiles; a.tcand = tcand; a.ctile = ctile; a.t_lo = t_lo; a.t_hi = t_hi;
+    a.t_ka_lo = t_ka_lo; a.t_ka_hi = t_ka_hi; a.t_kb_lo = t_kb_lo; a.t_kb_hi = t_kb_hi; a.tile_best = tile_best;
     int G = 0;
     PTRY(plan_loop_grid(&G));
     int64_t *resid, *local_cp, *chunk_sum;
@@ -455,7 +486,7 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     a.starts = t->starts; a.dur = t->dur; a.resid = resid; a.local_cp = local_cp; a.chunk_sum = chunk_sum;
     a.c_size = c_size; a.c_sk = c_sk; a.c_ek = c_ek; a.c_first = c_first; a.c_last = c_last; a.c_wraps = c_wraps;
     a.c_ready = c_ready; a.c_deadline = c_deadline; a.c_d = c_d;
-    a.st = st; a.place = place; a.rng = rng; a.list0 = list0; a.list1 = list1;
+    a.st = st; a.place = place; a.rng = rng;
     a.ch_cap = ch_cap;
     a.occ_s = occ_s; a.occ_e = occ_e; a.occ_size = occ_z;
     a.blk_best = blk_best; a.commits = p->commits; a.scalars = ps; a.c_tid = c_tid; a.c_tpos = c_tpos;

@@ -7,6 +7,7 @@
 //   over list / peak     planner.py:353, MemoryTimeline.peak
 //   planned host bytes   planner.py:354-358
 //   entries              planner.py:328-335 + sort :360-361 + mark_urgent :373-397
+#include <climits>
 #include "common.cuh"
 #include "block_scan.cuh"
 #include "planner.cuh"
@@ -94,6 +95,53 @@ __global__ void k_build_candidates(CandBuild a) {
         int8_t st = (int8_t)(ssd | (host << 2));
         if (ssd == S_DEAD && host == H_DEAD) st |= ST_GONE;
         a.st[c] = st;
+    }
+}
+
+// ---- tiles (planner.cu): ready-time order keys, then per-tile spans/hulls ----
+__global__ void k_ready_keys(const int64_t *ready, int64_t P, uint64_t *keys, uint32_t *vals) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < P; c += (int64_t)gridDim.x * blockDim.x) {
+        keys[c] = (uint64_t)ready[c];
+        vals[c] = (uint32_t)c;
+    }
+}
+
+// one warp per tile
+__global__ void k_tile_spans(const uint32_t *tcand, int64_t P, int64_t ntiles, int tile, int64_t N,
+                             const int64_t *ready, const int64_t *deadline, const int8_t *wraps,
+                             const int32_t *sk, const int32_t *ek, const int32_t *first, const int32_t *last,
+                             int32_t *ctile, int64_t *t_lo, int64_t *t_hi, int32_t *ka_lo, int32_t *ka_hi,
+                             int32_t *kb_lo, int32_t *kb_hi) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = warp; t < ntiles; t += nwarps) {
+        long long lo = LLONG_MAX, hi = LLONG_MIN;
+        int alo = INT_MAX, ahi = INT_MIN, blo = INT_MAX, bhi = INT_MIN;
+        for (int64_t p = t * tile + lane; p < (t + 1) * tile && p < P; p += 32) {
+            const uint32_t c = tcand[p];
+            ctile[c] = (int32_t)t;
+            lo = min(lo, (long long)ready[c]);
+            hi = max(hi, (long long)deadline[c]);
+            int a0, a1, b0 = 1, b1 = 0;
+            if (!wraps[c]) { a0 = sk[c]; a1 = ek[c]; }
+            else { a0 = last[c] + 1; a1 = (int)N - 1; b0 = 0; b1 = first[c] - 1; }
+            if (a0 <= a1) { alo = min(alo, a0); ahi = max(ahi, a1); }
+            if (b0 <= b1) { blo = min(blo, b0); bhi = max(bhi, b1); }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            alo = min(alo, __shfl_xor_sync(0xffffffffu, alo, o));
+            ahi = max(ahi, __shfl_xor_sync(0xffffffffu, ahi, o));
+            blo = min(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+            bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
+        }
+        if (lane == 0) {
+            t_lo[t] = lo; t_hi[t] = hi;
+            ka_lo[t] = alo <= ahi ? alo : 1; ka_hi[t] = alo <= ahi ? ahi : 0;
+            kb_lo[t] = blo <= bhi ? blo : 1; kb_hi[t] = blo <= bhi ? bhi : 0;
+        }
     }
 }
 

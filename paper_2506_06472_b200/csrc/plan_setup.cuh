@@ -37,6 +37,12 @@ __global__ void k_id_keys(const int64_t *tid, int64_t T, uint64_t *keys, uint32_
 __global__ void k_rank(const uint64_t *skeys, const uint32_t *order, int64_t T, const int64_t *tpp,
                        int32_t *rank, int64_t *cnt_by_rank, int64_t *flags);
 __global__ void k_build_candidates(CandBuild a);
+__global__ void k_ready_keys(const int64_t *ready, int64_t P, uint64_t *keys, uint32_t *vals);
+__global__ void k_tile_spans(const uint32_t *tcand, int64_t P, int64_t ntiles, int tile, int64_t N,
+                             const int64_t *ready, const int64_t *deadline, const int8_t *wraps,
+                             const int32_t *sk, const int32_t *ek, const int32_t *first, const int32_t *last,
+                             int32_t *ctile, int64_t *t_lo, int64_t *t_hi, int32_t *ka_lo, int32_t *ka_hi,
+                             int32_t *kb_lo, int32_t *kb_hi);
 __global__ void k_over_flags(const int64_t *resid, int64_t N, int64_t cap, int64_t *flag, long long *peak);
 __global__ void k_over_write(const int64_t *flag, const int64_t *pos, int64_t N, int64_t *over);
 __global__ void k_planned_host(const int64_t *os, const int64_t *oe, const int64_t *oz, int64_t h, int64_t *out);

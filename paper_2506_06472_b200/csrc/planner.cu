@@ -200,6 +200,28 @@ __device__ void block_best(Best &mine, Best *sm_best) {
 }
 
 // ---------------------------------------------------------------- the kernel
+//
+// Tiles.  Candidates are grouped into tiles of TILE consecutive candidates in
+// ready-time order (a permutation built by the setup; the candidate index,
+// i.e. the (tensor_id, start_kernel) rank, stays the tie-break key).  Every
+// tile has a static time span [min ready, max deadline) that contains every
+// placement its candidates can ever have, and two kernel hulls that contain
+// every kernel its candidates can ever cover.  A tile is re-evaluated in a
+// round only when it can have changed:
+//   * it held the last winner (the winner left the candidate set),
+//   * the last commit's bookings (with their +-iteration images) intersect
+//     its span (a cached placement may have moved or died),
+//   * kernels flipped from critical to non-critical inside one of its hulls
+//     (a cached benefit may have dropped),
+//   * a CPU commit's host occupancy intersects its span (host cap test).
+// Otherwise its cached tile best is provably the tile's current best.  A block
+// whose tiles are all clean keeps last round's block best as well.
+__device__ __forceinline__ bool spans_hit(int64_t lo, int64_t hi, const int64_t *s, const int64_t *e, int64_t nb) {
+    for (int q = 0; q < nb; ++q)
+        if (lo < e[q] && s[q] < hi) return true;
+    return false;
+}
+
 __global__ void __launch_bounds__(PLAN_THREADS)
 plan_loop_kernel(PlanArgs a) {
     cg::grid_group grid = cg::this_grid();
@@ -211,23 +233,27 @@ plan_loop_kernel(PlanArgs a) {
     __shared__ int64_t ch_n[4];
     __shared__ int32_t ch_par[4];
     __shared__ int64_t s_nocc;
-    __shared__ int64_t s_seg_len;
-    __shared__ int32_t s_list_par;
     __shared__ int64_t s_crit;
+    __shared__ int64_t s_flip[3];          // previous round: flipped count, lo, hi
+    __shared__ int64_t s_win_tile;
+    __shared__ int32_t s_dirty[PLAN_THREADS];
+    __shared__ int32_t s_ndirty;
 
-    const int64_t N = a.N, P = a.P, I = a.iteration, cap = a.capacity;
+    const int64_t N = a.N, I = a.iteration, cap = a.capacity;
     const int G = gridDim.x;
     const int b = blockIdx.x;
     const int64_t KC = a.chunk;
     const int64_t x0 = (int64_t)b * KC;                       // chunk over x in [0, N]
     const int64_t x1 = (x0 + KC < N + 1) ? x0 + KC : N + 1;
-    const int64_t seg0 = P * b / G, seg1 = P * (b + 1) / G;
     const int64_t period = I > 0 ? I : 0;
     const int64_t nb = period > 0 ? 3 : 1;
+    const int64_t NT = a.ntiles;
+    const int64_t my_tiles = NT > b ? (NT - 1 - b) / G + 1 : 0;   // tiles b, b+G, ...
+    int64_t *flip = &a.scalars[PS_FLIP];                       // [3 slots][cnt, lo, hi]
 
     if (ld_cg(&a.scalars[PS_STATUS]) != 0) return;  // unsatisfiable (set by setup)
 
-    // ---- setup: residual = timeline, chunk prefix of critical durations
+    // ---- setup: chunk prefix of critical durations
     auto rebuild_chunk = [&]() {
         int64_t run = 0;
         for (int64_t base = x0; base < x1; base += blockDim.x) {
@@ -249,22 +275,34 @@ plan_loop_kernel(PlanArgs a) {
         rebuild_chunk();
         int64_t tot = block_sum<int64_t>(crit, sm_scan);
         if (threadIdx.x == 0 && tot) atomic_add_i64(&a.scalars[PS_CRIT], tot);
-        for (int64_t i = seg0 + threadIdx.x; i < seg1; i += blockDim.x) a.list0[i] = (int32_t)i;
         if (threadIdx.x == 0) {
-            s_seg_len = seg1 - seg0;
-            s_list_par = 0;
             last.dest = 0;
             last.nb = nb;
             s_nocc = 0;
+            s_win_tile = -1;
             for (int q = 0; q < 4; ++q) { ch_n[q] = 0; ch_par[q] = 0; }
+            if (b == 0)
+                for (int q = 0; q < 3; ++q) { flip[3 * q] = 0; flip[3 * q + 1] = INT64_MAX; flip[3 * q + 2] = -1; }
         }
     }
     grid.sync();
 
     for (int64_t round = 0;; ++round) {
-        // ---- round prologue: crit count + chunk prefix (identical in every CTA)
-        if (threadIdx.x == 0) s_crit = ld_cg(&a.scalars[PS_CRIT]);
-        {
+        // ---- round prologue: crit count, last round's flips, chunk prefix
+        if (threadIdx.x == 0) {
+            s_crit = ld_cg(&a.scalars[PS_CRIT]);
+            if (round > 0) {
+                const int64_t *f = flip + 3 * ((round - 1) % 3);
+                s_flip[0] = ld_cg(f); s_flip[1] = ld_cg(f + 1); s_flip[2] = ld_cg(f + 2);
+            }
+            // slot of the next round's commit; nobody reads it this round
+            if (b == 0) {
+                int64_t *f = flip + 3 * ((round + 1) % 3);
+                f[0] = 0; f[1] = INT64_MAX; f[2] = -1;
+            }
+        }
+        __syncthreads();
+        if (round == 0 || s_flip[0] > 0) {
             int64_t v = 0;
             int nchunks = (int)((N + 1 + KC - 1) / KC);
             // exclusive prefix of chunk sums into cp_prefix[0..nchunks]
@@ -281,141 +319,166 @@ plan_loop_kernel(PlanArgs a) {
         __syncthreads();
         if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
 
-        // ---- phase E: evaluate live candidates of this block's segment
-        const int32_t *lin = s_list_par ? a.list1 : a.list0;
-        int32_t *lout = s_list_par ? a.list0 : a.list1;
+        // ---- phase E: re-evaluate the dirty tiles of this block
         ChanView cv[4];
         for (int q = 0; q < 4; ++q) {
             cv[q].s = a.ch_s[q][ch_par[q]];
             cv[q].e = a.ch_e[q][ch_par[q]];
             cv[q].n = ch_n[q];
         }
-        Best mine{};
-        mine.benefit = 0;
-        const int64_t seg_len = s_seg_len;
-        int64_t kept_total = 0;
-        for (int64_t base = 0; base < seg_len; base += blockDim.x) {
-            int64_t pos = base + threadIdx.x;
-            bool keep = false;
-            int32_t c = -1;
-            if (pos < seg_len) {
-                c = lin[seg0 + pos];
-                int8_t st = ld_cg(&a.st[c]);
-                if (!(st & ST_GONE)) {
-                    keep = true;
-                    int ssd = st & 3, host = (st >> 2) & 3;
-                    const int64_t size = __ldg(&a.c_size[c]);
-                    const int64_t ready = __ldg(&a.c_ready[c]), deadline = __ldg(&a.c_deadline[c]);
-                    const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
-                    bool moved = false;
-                    // SSD path
-                    int64_t h_off = ready, h_pre = deadline;
-                    if (ssd == S_OK) { h_off = ld_cg(&a.place[4 * c]); h_pre = ld_cg(&a.place[4 * c + 1]) + d1; }
-                    if (ssd == S_UNK ||
-                        (ssd == S_OK && last.dest == TIO_DEST_SSD &&
-                         (overlaps(h_off, d0, last.off_s, last.off_e, last.nb) ||
-                          overlaps(h_pre - d1, d1, last.pre_s, last.pre_e, last.nb)))) {
-                        int64_t os, ps;
-                        if (fit_pair(cv[0], cv[1], d0, d1, I, h_off, h_pre, &os, &ps)) {
-                            ssd = S_OK;
-                            a.place[4 * c] = os;
-                            a.place[4 * c + 1] = ps;
-                        } else {
-                            ssd = S_DEAD;
-                        }
-                        moved = true;
-                    }
-                    // host path (only consulted once the SSD path is dead: planner.py:211-227)
-                    if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
-                        const int64_t d2 = __ldg(&a.c_d[4 * c + 2]), d3 = __ldg(&a.c_d[4 * c + 3]);
-                        bool refit = host == H_UNK;
-                        bool recap = false;
-                        if (!refit && last.dest == TIO_DEST_CPU) {
-                            refit = overlaps(ld_cg(&a.place[4 * c + 2]), d2, last.off_s, last.off_e, last.nb) ||
-                                    overlaps(ld_cg(&a.place[4 * c + 3]), d3, last.pre_s, last.pre_e, last.nb);
-                            if (!refit && host == H_OK) {
-                                int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
-                                recap = last.occ_s <= hi && last.occ_e > lo;
-                            }
-                        }
-                        if (refit) {
-                            int64_t os, ps;
-                            int64_t g_off = ready, g_pre = deadline;
-                            if (host != H_UNK) { g_off = ld_cg(&a.place[4 * c + 2]); g_pre = ld_cg(&a.place[4 * c + 3]) + d3; }
-                            if (fit_pair(cv[2], cv[3], d2, d3, I, g_off, g_pre, &os, &ps)) {
-                                a.place[4 * c + 2] = os;
-                                a.place[4 * c + 3] = ps;
-                                recap = true;
-                                moved = true;
-                            } else {
-                                host = H_DEAD;
-                                moved = true;
-                            }
-                        }
-                        if (recap) {
-                            int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
-                            int64_t occ = host_peak(a.occ_s, a.occ_e, a.occ_size, s_nocc, lo, hi);
-                            host = (occ + size > a.host_cap) ? H_CAPFAIL : H_OK;
-                        }
-                    }
-                    int dest = ssd == S_OK ? TIO_DEST_SSD : (ssd == S_DEAD && host == H_OK ? TIO_DEST_CPU : 0);
-                    int8_t nst = (int8_t)(ssd | (host << 2));
-                    if (ssd == S_DEAD && (!a.has_host || host == H_DEAD)) {
-                        nst |= ST_GONE;
-                        keep = false;
-                    } else if (dest) {
-                        const int q0 = dest == TIO_DEST_SSD ? 0 : 2;
-                        const int64_t os = ld_cg(&a.place[4 * c + q0]);
-                        const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
-                        const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
-                        int32_t r[4];
-                        if (moved) {
-                            covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
-                                           __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
-                                           os + doff, ps, r);
-                            for (int q = 0; q < 4; ++q) a.rng[4 * c + q] = r[q];
-                        } else {
-                            for (int q = 0; q < 4; ++q) r[q] = ld_cg(&a.rng[4 * c + q]);
-                        }
-                        int64_t ct = 0;
-                        for (int q = 0; q < 4; q += 2) {
-                            if (r[q] <= r[q + 1]) {
-                                int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
-                                ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
-                                      (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
-                            }
-                        }
-                        if (ct == 0) {
-                            // benefit only ever shrinks on a host window or on an SSD
-                            // window without a host path to fall back to
-                            if (dest == TIO_DEST_CPU || !a.has_host) { nst |= ST_GONE; keep = false; }
-                        } else {
-                            Best cand;
-                            cand.benefit = (u128)(uint64_t)size * (uint64_t)ct;
-                            cand.cost = doff + dpre;
-                            cand.idx = c;
-                            cand.dest = dest;
-                            cand.off_s = os; cand.off_e = os + doff;
-                            cand.pre_s = ps; cand.pre_e = ps + dpre;
-                            cand.size = size;
-                            for (int q = 0; q < 4; ++q) cand.r[q] = r[q];
-                            if (better(cand, mine)) mine = cand;
-                        }
-                    }
-                    if (nst != st) a.st[c] = nst;
+        bool any_dirty = false;
+        for (int64_t j0 = 0; j0 < my_tiles; j0 += blockDim.x) {
+            // dirty test, one tile per thread
+            if (threadIdx.x == 0) s_ndirty = 0;
+            __syncthreads();
+            const int64_t j = j0 + threadIdx.x;
+            if (j < my_tiles) {
+                const int64_t t = b + j * G;
+                bool d = round == 0 || t == s_win_tile;
+                if (!d && last.dest) {
+                    const int64_t lo = __ldg(&a.t_lo[t]), hi = __ldg(&a.t_hi[t]);
+                    d = spans_hit(lo, hi, last.off_s, last.off_e, last.nb) ||
+                        spans_hit(lo, hi, last.pre_s, last.pre_e, last.nb) ||
+                        (last.dest == TIO_DEST_CPU && last.occ_s <= hi && last.occ_e > lo);
                 }
+                if (!d && round > 0 && s_flip[0] > 0) {
+                    const int64_t fl = s_flip[1], fh = s_flip[2];
+                    const int32_t alo = __ldg(&a.t_ka_lo[t]), ahi = __ldg(&a.t_ka_hi[t]);
+                    const int32_t blo = __ldg(&a.t_kb_lo[t]), bhi = __ldg(&a.t_kb_hi[t]);
+                    d = (alo <= ahi && alo <= fh && fl <= ahi) || (blo <= bhi && blo <= fh && fl <= bhi);
+                }
+                if (d) s_dirty[atomicAdd(&s_ndirty, 1)] = (int32_t)t;
             }
-            // stable in-block compaction of the live list into the other buffer
-            int64_t tot;
-            int64_t ex = block_exclusive_sum<int64_t>(keep ? 1 : 0, sm_scan, &tot);
-            if (keep) lout[seg0 + kept_total + ex] = c;
-            kept_total += tot;
+            __syncthreads();
+            const int nd = s_ndirty;
+            if (nd) any_dirty = true;
+            for (int di = 0; di < nd; ++di) {
+                const int64_t t = s_dirty[di];
+                const int64_t pos = t * TILE + threadIdx.x;
+                Best mine{};
+                mine.benefit = 0;
+                if (pos < a.P) {
+                    const int32_t c = (int32_t)__ldg(&a.tcand[pos]);
+                    int8_t st = ld_cg(&a.st[c]);
+                    if (!(st & ST_GONE)) {
+                        int ssd = st & 3, host = (st >> 2) & 3;
+                        const int64_t size = __ldg(&a.c_size[c]);
+                        const int64_t ready = __ldg(&a.c_ready[c]), deadline = __ldg(&a.c_deadline[c]);
+                        const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
+                        bool moved = false;
+                        // SSD path
+                        int64_t h_off = ready, h_pre = deadline;
+                        if (ssd == S_OK) { h_off = ld_cg(&a.place[4 * c]); h_pre = ld_cg(&a.place[4 * c + 1]) + d1; }
+                        if (ssd == S_UNK ||
+                            (ssd == S_OK && last.dest == TIO_DEST_SSD &&
+                             (overlaps(h_off, d0, last.off_s, last.off_e, last.nb) ||
+                              overlaps(h_pre - d1, d1, last.pre_s, last.pre_e, last.nb)))) {
+                            int64_t os, ps;
+                            if (fit_pair(cv[0], cv[1], d0, d1, I, h_off, h_pre, &os, &ps)) {
+                                ssd = S_OK;
+                                a.place[4 * c] = os;
+                                a.place[4 * c + 1] = ps;
+                            } else {
+                                ssd = S_DEAD;
+                            }
+                            moved = true;
+                        }
+                        // host path (only consulted once the SSD path is dead: planner.py:211-227)
+                        if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
+                            const int64_t d2 = __ldg(&a.c_d[4 * c + 2]), d3 = __ldg(&a.c_d[4 * c + 3]);
+                            bool refit = host == H_UNK;
+                            bool recap = false;
+                            if (!refit && last.dest == TIO_DEST_CPU) {
+                                refit = overlaps(ld_cg(&a.place[4 * c + 2]), d2, last.off_s, last.off_e, last.nb) ||
+                                        overlaps(ld_cg(&a.place[4 * c + 3]), d3, last.pre_s, last.pre_e, last.nb);
+                                if (!refit && host == H_OK) {
+                                    int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
+                                    recap = last.occ_s <= hi && last.occ_e > lo;
+                                }
+                            }
+                            if (refit) {
+                                int64_t os, ps;
+                                int64_t g_off = ready, g_pre = deadline;
+                                if (host != H_UNK) { g_off = ld_cg(&a.place[4 * c + 2]); g_pre = ld_cg(&a.place[4 * c + 3]) + d3; }
+                                if (fit_pair(cv[2], cv[3], d2, d3, I, g_off, g_pre, &os, &ps)) {
+                                    a.place[4 * c + 2] = os;
+                                    a.place[4 * c + 3] = ps;
+                                    recap = true;
+                                    moved = true;
+                                } else {
+                                    host = H_DEAD;
+                                    moved = true;
+                                }
+                            }
+                            if (recap) {
+                                int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
+                                int64_t occ = host_peak(a.occ_s, a.occ_e, a.occ_size, s_nocc, lo, hi);
+                                host = (occ + size > a.host_cap) ? H_CAPFAIL : H_OK;
+                            }
+                        }
+                        int dest = ssd == S_OK ? TIO_DEST_SSD : (ssd == S_DEAD && host == H_OK ? TIO_DEST_CPU : 0);
+                        int8_t nst = (int8_t)(ssd | (host << 2));
+                        if (ssd == S_DEAD && (!a.has_host || host == H_DEAD)) {
+                            nst |= ST_GONE;
+                        } else if (dest) {
+                            const int q0 = dest == TIO_DEST_SSD ? 0 : 2;
+                            const int64_t os = ld_cg(&a.place[4 * c + q0]);
+                            const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
+                            const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
+                            int32_t r[4];
+                            if (moved) {
+                                covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                                               __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
+                                               os + doff, ps, r);
+                                for (int q = 0; q < 4; ++q) a.rng[4 * c + q] = r[q];
+                            } else {
+                                for (int q = 0; q < 4; ++q) r[q] = ld_cg(&a.rng[4 * c + q]);
+                            }
+                            int64_t ct = 0;
+                            for (int q = 0; q < 4; q += 2) {
+                                if (r[q] <= r[q + 1]) {
+                                    int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
+                                    ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
+                                          (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
+                                }
+                            }
+                            if (ct == 0) {
+                                // benefit only ever shrinks on a host window or on an SSD
+                                // window without a host path to fall back to
+                                if (dest == TIO_DEST_CPU || !a.has_host) nst |= ST_GONE;
+                            } else {
+                                mine.benefit = (u128)(uint64_t)size * (uint64_t)ct;
+                                mine.cost = doff + dpre;
+                                mine.idx = c;
+                                mine.dest = dest;
+                                mine.off_s = os; mine.off_e = os + doff;
+                                mine.pre_s = ps; mine.pre_e = ps + dpre;
+                                mine.size = size;
+                                for (int q = 0; q < 4; ++q) mine.r[q] = r[q];
+                            }
+                        }
+                        if (nst != st) a.st[c] = nst;
+                    }
+                }
+                block_best(mine, sm_best);
+                if (threadIdx.x == 0) a.tile_best[t] = mine;
+            }
+            __syncthreads();
         }
-        block_best(mine, sm_best);
-        if (threadIdx.x == 0) {
-            a.blk_best[b] = mine;
-            s_seg_len = kept_total;
-            s_list_par ^= 1;
+        // block best over this block's tiles (unchanged when no tile was dirty)
+        if (any_dirty) {
+            Best mine{};
+            mine.benefit = 0;
+            for (int64_t j = threadIdx.x; j < my_tiles; j += blockDim.x) {
+                Best o = a.tile_best[b + j * G];
+                if (better(o, mine)) mine = o;
+            }
+            block_best(mine, sm_best);
+            if (threadIdx.x == 0) a.blk_best[b] = mine;
+        } else if (round == 0 && threadIdx.x == 0) {
+            Best none{};
+            none.benefit = 0;
+            a.blk_best[b] = none;
         }
         grid.sync();
 
@@ -476,6 +539,7 @@ plan_loop_kernel(PlanArgs a) {
         // residual update on this block's kernel chunk (planner.py:322-324)
         {
             int32_t flips = 0;
+            int64_t *fs = flip + 3 * (round % 3);
             for (int rq = 0; rq < 4; rq += 2) {
                 int64_t lo = w.r[rq], hi = w.r[rq + 1];
                 if (lo > hi) continue;
@@ -486,14 +550,21 @@ plan_loop_kernel(PlanArgs a) {
                     int64_t old = ld_cg(&a.resid[k]);
                     int64_t nw = old - w.size;
                     a.resid[k] = nw;
-                    if (old > cap && nw <= cap) ++flips;
+                    if (old > cap && nw <= cap) {
+                        ++flips;
+                        atomicMin(reinterpret_cast<unsigned long long *>(fs + 1), (unsigned long long)k);
+                        atomicMax(reinterpret_cast<long long *>(fs + 2), (long long)k);
+                    }
                 }
             }
             int32_t tf = block_sum<int32_t>(flips, reinterpret_cast<int32_t *>(sm_scan));
             __syncthreads();
             if (tf) {
                 rebuild_chunk();
-                if (threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_CRIT], -(int64_t)tf);
+                if (threadIdx.x == 0) {
+                    atomic_add_i64(&a.scalars[PS_CRIT], -(int64_t)tf);
+                    atomic_add_i64(fs, (int64_t)tf);
+                }
             }
         }
         // block 0: commit record, host occupancy, mark the winner gone
@@ -532,6 +603,7 @@ plan_loop_kernel(PlanArgs a) {
             if (w.dest == TIO_DEST_CPU) s_nocc += 1;
             ch_n[q0] += nb; ch_n[q0 + 1] += nb;
             ch_par[q0] ^= 1; ch_par[q0 + 1] ^= 1;
+            s_win_tile = __ldg(&a.ctile[w.idx]);
         }
         grid.sync();
     }

@@ -7,6 +7,7 @@
 namespace tio {
 
 constexpr int PLAN_THREADS = 256;
+constexpr int TILE = PLAN_THREADS;   // candidates per tile (one block pass)
 
 // candidate SSD/host evaluation state (2 bits each in st[c])
 enum : int { S_UNK = 0, S_OK = 1, S_DEAD = 2 };                   // SSD path
@@ -16,7 +17,8 @@ constexpr int8_t ST_GONE = (int8_t)0x40;  // committed or permanently useless
 // planner scalars[] slots
 enum {
     PS_COMMITS = 0, PS_ROUNDS = 1, PS_CRIT = 2, PS_STATUS = 3, PS_OCC = 4,
-    PS_UNSAT_K = 5, PS_UNSAT_B = 6, PS_INVARIANT = 7, PS_COUNT = 8
+    PS_UNSAT_K = 5, PS_UNSAT_B = 6, PS_INVARIANT = 7, PS_FLIP = 8 /* 3 slots x (cnt, lo, hi) */,
+    PS_COUNT = 17
 };
 
 // best candidate of a block (and, after the grid reduction, of the round)
@@ -51,7 +53,13 @@ struct PlanArgs {
     int8_t *st;                    // [P]
     int64_t *place;                // [4P] ssd_off_s, ssd_pre_s, host_off_s, host_pre_s
     int32_t *rng;                  // [4P]
-    int32_t *list0, *list1;        // [P] alive lists (per-block segments)
+    // tiles: candidates in ready-time order, TILE per tile
+    int64_t ntiles;
+    const uint32_t *tcand;         // [P] candidate at tile position
+    const int32_t *ctile;          // [P] tile of a candidate
+    const int64_t *t_lo, *t_hi;    // [ntiles] span [min ready, max deadline)
+    const int32_t *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;  // [ntiles] kernel hulls (lo > hi: empty)
+    Best *tile_best;               // [ntiles]
     // channels: 4 channels (ssd.off, ssd.pre, host.off, host.pre) x 2 buffers
     int64_t *ch_s[4][2];
     int64_t *ch_e[4][2];
