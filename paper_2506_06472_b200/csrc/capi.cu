@@ -523,6 +523,7 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     pi.num_commits = nc;
     pi.num_entries = 2 * nc;
     pi.rounds = hs[PS_ROUNDS];
+    for (int q = 0; q < 12; ++q) pi.dbg[q] = hs[PS_DBG + q];
 
     // ---- epilogue: over list, peak, planned host, sorted + urgent entries
     p->resid = resid;

@@ -216,6 +216,12 @@ __device__ void block_best(Best &mine, Best *sm_best) {
 //   * a CPU commit's host occupancy intersects its span (host cap test).
 // Otherwise its cached tile best is provably the tile's current best.  A block
 // whose tiles are all clean keeps last round's block best as well.
+__device__ __forceinline__ int64_t gtime() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (int64_t)t;
+}
+
 __device__ __forceinline__ bool spans_hit(int64_t lo, int64_t hi, const int64_t *s, const int64_t *e, int64_t nb) {
     for (int q = 0; q < nb; ++q)
         if (lo < e[q] && s[q] < hi) return true;
@@ -287,6 +293,10 @@ plan_loop_kernel(PlanArgs a) {
     }
     grid.sync();
 
+    int64_t dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t tprev = gtime();
+    const bool tb = (b == 0 && threadIdx.x == 0);
+#define TICK(slot) do { if (tb) { int64_t _t = gtime(); dbg[slot] += _t - tprev; tprev = _t; } } while (0)
     for (int64_t round = 0;; ++round) {
         // ---- round prologue: crit count, last round's flips, chunk prefix
         if (threadIdx.x == 0) {
@@ -319,6 +329,8 @@ plan_loop_kernel(PlanArgs a) {
         __syncthreads();
         if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
 
+        TICK(0);
+        const int64_t te0 = gtime();
         // ---- phase E: re-evaluate the dirty tiles of this block
         ChanView cv[4];
         for (int q = 0; q < 4; ++q) {
@@ -352,6 +364,7 @@ plan_loop_kernel(PlanArgs a) {
             __syncthreads();
             const int nd = s_ndirty;
             if (nd) any_dirty = true;
+            if (nd && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 8], nd);
             for (int di = 0; di < nd; ++di) {
                 const int64_t t = s_dirty[di];
                 const int64_t pos = t * TILE + threadIdx.x;
@@ -382,6 +395,7 @@ plan_loop_kernel(PlanArgs a) {
                                 ssd = S_DEAD;
                             }
                             moved = true;
+                            atomic_add_i64(&a.scalars[PS_DBG + 9], 1);
                         }
                         // host path (only consulted once the SSD path is dead: planner.py:211-227)
                         if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
@@ -465,6 +479,7 @@ plan_loop_kernel(PlanArgs a) {
             }
             __syncthreads();
         }
+        TICK(1);
         // block best over this block's tiles (unchanged when no tile was dirty)
         if (any_dirty) {
             Best mine{};
@@ -480,7 +495,15 @@ plan_loop_kernel(PlanArgs a) {
             none.benefit = 0;
             a.blk_best[b] = none;
         }
+        if (threadIdx.x == 0)
+            atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 15]), (long long)(gtime() - te0));
+        TICK(2);
         grid.sync();
+        TICK(3);
+        if (tb) {
+            a.scalars[PS_DBG + 10] += ld_cg(&a.scalars[PS_DBG + 15]);
+            a.scalars[PS_DBG + 15] = 0;
+        }
 
         // ---- phase C: global argmax (redundant per block) and commit
         {
@@ -498,6 +521,7 @@ plan_loop_kernel(PlanArgs a) {
             __syncthreads();
         }
         const Best w = s_win;
+        TICK(4);
         if (w.benefit == 0) break;  // planner.py:311-312 no viable candidate
         const int q0 = w.dest == TIO_DEST_SSD ? 0 : 2;
         // new bookings, sorted: (-period, 0, +period)
@@ -536,6 +560,7 @@ plan_loop_kernel(PlanArgs a) {
                 if (i < n) { ds[i + cnt] = si; de[i + cnt] = ei; }
             }
         }
+        TICK(5);
         // residual update on this block's kernel chunk (planner.py:322-324)
         {
             int32_t flips = 0;
@@ -567,6 +592,7 @@ plan_loop_kernel(PlanArgs a) {
                 }
             }
         }
+        TICK(6);
         // block 0: commit record, host occupancy, mark the winner gone
         if (b == 0 && threadIdx.x == 0) {
             int64_t j = a.scalars[PS_COMMITS];
@@ -606,7 +632,11 @@ plan_loop_kernel(PlanArgs a) {
             s_win_tile = __ldg(&a.ctile[w.idx]);
         }
         grid.sync();
+        TICK(7);
     }
+    if (tb)
+        for (int q = 0; q < 8; ++q) a.scalars[PS_DBG + q] = dbg[q];
+#undef TICK
 }
 
 int plan_loop_grid(int *blocks) {

@@ -18,7 +18,7 @@ constexpr int8_t ST_GONE = (int8_t)0x40;  // committed or permanently useless
 enum {
     PS_COMMITS = 0, PS_ROUNDS = 1, PS_CRIT = 2, PS_STATUS = 3, PS_OCC = 4,
     PS_UNSAT_K = 5, PS_UNSAT_B = 6, PS_INVARIANT = 7, PS_FLIP = 8 /* 3 slots x (cnt, lo, hi) */,
-    PS_COUNT = 17
+    PS_DBG = 17 /* 16 debug counters */, PS_COUNT = 33
 };
 
 // best candidate of a block (and, after the grid reduction, of the round)
