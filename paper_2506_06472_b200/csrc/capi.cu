@@ -432,7 +432,7 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     uint32_t *tcand;
     int32_t *ctile, *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;
     int64_t *t_lo, *t_hi;
-    Best *tile_best;
+    Key *tile_best;
     PTRY(A.alloc(&ctile, P));
     PTRY(A.alloc(&t_lo, ntiles)); PTRY(A.alloc(&t_hi, ntiles));
     PTRY(A.alloc(&t_ka_lo, ntiles)); PTRY(A.alloc(&t_ka_hi, ntiles));
@@ -477,7 +477,7 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
         }
     int64_t *occ_s, *occ_e, *occ_z;
     PTRY(A.alloc(&occ_s, has_host ? P : 1)); PTRY(A.alloc(&occ_e, has_host ? P : 1)); PTRY(A.alloc(&occ_z, has_host ? P : 1));
-    Best *blk_best;
+    Key *blk_best;
     PTRY(A.alloc(&blk_best, G));
     PTRY(A.alloc(&p->commits, P));
     a.N = N; a.P = P; a.iteration = I; a.capacity = capacity; a.host_cap = host_cap;

@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "block_scan.cuh"
 #include "planner.cuh"
+#include "warp_search.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -161,42 +162,53 @@ __device__ __forceinline__ bool overlaps(int64_t x, int64_t d, const int64_t *s,
     return false;
 }
 
-__device__ __forceinline__ bool better(const Best &a, const Best &b) {
-    if (a.benefit == 0) return false;
-    if (b.benefit == 0) return true;
-    if (ratio_gt(a.benefit, a.cost, b.benefit, b.cost)) return true;
-    if (ratio_gt(b.benefit, b.cost, a.benefit, a.cost)) return false;
-    return a.idx < b.idx;
+// ---------------------------------------------------------------- argmax keys
+// The round's argmax carries 4 words: the exact benefit (u128), the cost and
+// meta = 4 * candidate index + destination.  Everything else about the
+// winner is re-read from the candidate arrays once it is known.
+__device__ __forceinline__ bool kbetter(const Key &a, const Key &b) {
+    const bool az = (a.blo | a.bhi) == 0, bz = (b.blo | b.bhi) == 0;
+    if (az) return false;
+    if (bz) return true;
+    const u128 ab = ((u128)a.bhi << 64) | a.blo, bb = ((u128)b.bhi << 64) | b.blo;
+    if (ratio_gt(ab, a.cost, bb, b.cost)) return true;
+    if (ratio_gt(bb, b.cost, ab, a.cost)) return false;
+    return a.meta < b.meta;   // tie: lowest candidate index = first in (tensor_id, start_kernel) order
 }
 
-__device__ __forceinline__ void shfl_best(Best &dst, const Best &src, int lane) {
-    const int64_t *p = reinterpret_cast<const int64_t *>(&src);
-    int64_t *q = reinterpret_cast<int64_t *>(&dst);
-#pragma unroll
-    for (int i = 0; i < (int)(sizeof(Best) / 8); ++i) q[i] = __shfl_sync(0xffffffffu, p[i], lane);
+__device__ __forceinline__ Key kshfl(const Key &k, int src) {
+    Key o;
+    o.blo = __shfl_sync(0xffffffffu, k.blo, src);
+    o.bhi = __shfl_sync(0xffffffffu, k.bhi, src);
+    o.cost = __shfl_sync(0xffffffffu, k.cost, src);
+    o.meta = __shfl_sync(0xffffffffu, k.meta, src);
+    return o;
 }
 
-__device__ void block_best(Best &mine, Best *sm_best) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+__device__ __forceinline__ Key warp_best(Key mine) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        Best other;
-        shfl_best(other, mine, (lane + o) & 31);
-        if (lane + o < 32 && better(other, mine)) mine = other;
+        Key other = kshfl(mine, (threadIdx.x + o) & 31);
+        if (((threadIdx.x & 31) + o) < 32 && kbetter(other, mine)) mine = other;
     }
-    if (lane == 0) sm_best[warp] = mine;
+    return mine;   // valid in lane 0
+}
+
+// block-wide argmax; the result is returned to every thread
+__device__ Key block_best(Key mine, Key *sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    mine = warp_best(mine);
+    if (lane == 0) sm[warp] = mine;
     __syncthreads();
     if (warp == 0) {
-        mine = lane < nw ? sm_best[lane] : Best{};
-        if (lane >= nw) mine.benefit = 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            Best other;
-            shfl_best(other, mine, (lane + o) & 31);
-            if (lane + o < 32 && better(other, mine)) mine = other;
-        }
+        Key k = lane < nw ? sm[lane] : Key{0, 0, 1, 0};
+        k = warp_best(k);
+        if (lane == 0) sm[32] = k;
     }
     __syncthreads();
+    Key r = sm[32];
+    __syncthreads();
+    return r;
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -228,12 +240,21 @@ __device__ __forceinline__ bool spans_hit(int64_t lo, int64_t hi, const int64_t 
     return false;
 }
 
+constexpr int WARP_REFIT_MAX = 96;   // refits per tile served warp-cooperatively (else per thread)
+
+struct WinInfo {
+    int64_t idx, dest, size, cost;
+    int64_t off_s, off_e, pre_s, pre_e;
+    int32_t r[4];
+    uint64_t blo, bhi;
+};
+
 __global__ void __launch_bounds__(PLAN_THREADS)
 plan_loop_kernel(PlanArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ int64_t cp_prefix[MAXG + 1];
-    __shared__ Best sm_best[PLAN_THREADS / 32];
-    __shared__ Best s_win;
+    __shared__ Key sm_key[33];
+    __shared__ WinInfo s_win;
     __shared__ LastCommit last;
     __shared__ int64_t sm_scan[40];
     __shared__ int64_t ch_n[4];
@@ -244,10 +265,13 @@ plan_loop_kernel(PlanArgs a) {
     __shared__ int64_t s_win_tile;
     __shared__ int32_t s_dirty[PLAN_THREADS];
     __shared__ int32_t s_ndirty;
+    __shared__ int16_t s_refit[PLAN_THREADS];
+    __shared__ int32_t s_nrefit;
 
     const int64_t N = a.N, I = a.iteration, cap = a.capacity;
     const int G = gridDim.x;
     const int b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int64_t KC = a.chunk;
     const int64_t x0 = (int64_t)b * KC;                       // chunk over x in [0, N]
     const int64_t x1 = (x0 + KC < N + 1) ? x0 + KC : N + 1;
@@ -256,6 +280,7 @@ plan_loop_kernel(PlanArgs a) {
     const int64_t NT = a.ntiles;
     const int64_t my_tiles = NT > b ? (NT - 1 - b) / G + 1 : 0;   // tiles b, b+G, ...
     int64_t *flip = &a.scalars[PS_FLIP];                       // [3 slots][cnt, lo, hi]
+    const Key none{0, 0, 1, 0};
 
     if (ld_cg(&a.scalars[PS_STATUS]) != 0) return;  // unsatisfiable (set by setup)
 
@@ -328,9 +353,9 @@ plan_loop_kernel(PlanArgs a) {
         }
         __syncthreads();
         if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
-
         TICK(0);
         const int64_t te0 = gtime();
+
         // ---- phase E: re-evaluate the dirty tiles of this block
         ChanView cv[4];
         for (int q = 0; q < 4; ++q) {
@@ -368,131 +393,165 @@ plan_loop_kernel(PlanArgs a) {
             for (int di = 0; di < nd; ++di) {
                 const int64_t t = s_dirty[di];
                 const int64_t pos = t * TILE + threadIdx.x;
-                Best mine{};
-                mine.benefit = 0;
-                if (pos < a.P) {
-                    const int32_t c = (int32_t)__ldg(&a.tcand[pos]);
-                    int8_t st = ld_cg(&a.st[c]);
-                    if (!(st & ST_GONE)) {
-                        int ssd = st & 3, host = (st >> 2) & 3;
-                        const int64_t size = __ldg(&a.c_size[c]);
-                        const int64_t ready = __ldg(&a.c_ready[c]), deadline = __ldg(&a.c_deadline[c]);
+                const int32_t c = pos < a.P ? (int32_t)__ldg(&a.tcand[pos]) : -1;
+                int8_t st = c >= 0 ? ld_cg(&a.st[c]) : ST_GONE;
+                // pass 1: which candidates need an SSD re-search (planner.py:147-176)
+                bool need = false;
+                if (!(st & ST_GONE)) {
+                    const int ssd = st & 3;
+                    if (ssd == S_UNK) need = true;
+                    else if (ssd == S_OK && last.dest == TIO_DEST_SSD) {
                         const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
-                        bool moved = false;
-                        // SSD path
-                        int64_t h_off = ready, h_pre = deadline;
-                        if (ssd == S_OK) { h_off = ld_cg(&a.place[4 * c]); h_pre = ld_cg(&a.place[4 * c + 1]) + d1; }
-                        if (ssd == S_UNK ||
-                            (ssd == S_OK && last.dest == TIO_DEST_SSD &&
-                             (overlaps(h_off, d0, last.off_s, last.off_e, last.nb) ||
-                              overlaps(h_pre - d1, d1, last.pre_s, last.pre_e, last.nb)))) {
-                            int64_t os, ps;
-                            if (fit_pair(cv[0], cv[1], d0, d1, I, h_off, h_pre, &os, &ps)) {
-                                ssd = S_OK;
-                                a.place[4 * c] = os;
-                                a.place[4 * c + 1] = ps;
-                            } else {
-                                ssd = S_DEAD;
-                            }
-                            moved = true;
-                            atomic_add_i64(&a.scalars[PS_DBG + 9], 1);
-                        }
-                        // host path (only consulted once the SSD path is dead: planner.py:211-227)
-                        if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
-                            const int64_t d2 = __ldg(&a.c_d[4 * c + 2]), d3 = __ldg(&a.c_d[4 * c + 3]);
-                            bool refit = host == H_UNK;
-                            bool recap = false;
-                            if (!refit && last.dest == TIO_DEST_CPU) {
-                                refit = overlaps(ld_cg(&a.place[4 * c + 2]), d2, last.off_s, last.off_e, last.nb) ||
-                                        overlaps(ld_cg(&a.place[4 * c + 3]), d3, last.pre_s, last.pre_e, last.nb);
-                                if (!refit && host == H_OK) {
-                                    int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
-                                    recap = last.occ_s <= hi && last.occ_e > lo;
-                                }
-                            }
-                            if (refit) {
-                                int64_t os, ps;
-                                int64_t g_off = ready, g_pre = deadline;
-                                if (host != H_UNK) { g_off = ld_cg(&a.place[4 * c + 2]); g_pre = ld_cg(&a.place[4 * c + 3]) + d3; }
-                                if (fit_pair(cv[2], cv[3], d2, d3, I, g_off, g_pre, &os, &ps)) {
-                                    a.place[4 * c + 2] = os;
-                                    a.place[4 * c + 3] = ps;
-                                    recap = true;
-                                    moved = true;
-                                } else {
-                                    host = H_DEAD;
-                                    moved = true;
-                                }
-                            }
-                            if (recap) {
-                                int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
-                                int64_t occ = host_peak(a.occ_s, a.occ_e, a.occ_size, s_nocc, lo, hi);
-                                host = (occ + size > a.host_cap) ? H_CAPFAIL : H_OK;
-                            }
-                        }
-                        int dest = ssd == S_OK ? TIO_DEST_SSD : (ssd == S_DEAD && host == H_OK ? TIO_DEST_CPU : 0);
-                        int8_t nst = (int8_t)(ssd | (host << 2));
-                        if (ssd == S_DEAD && (!a.has_host || host == H_DEAD)) {
-                            nst |= ST_GONE;
-                        } else if (dest) {
-                            const int q0 = dest == TIO_DEST_SSD ? 0 : 2;
-                            const int64_t os = ld_cg(&a.place[4 * c + q0]);
-                            const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
-                            const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
-                            int32_t r[4];
-                            if (moved) {
-                                covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
-                                               __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
-                                               os + doff, ps, r);
-                                for (int q = 0; q < 4; ++q) a.rng[4 * c + q] = r[q];
-                            } else {
-                                for (int q = 0; q < 4; ++q) r[q] = ld_cg(&a.rng[4 * c + q]);
-                            }
-                            int64_t ct = 0;
-                            for (int q = 0; q < 4; q += 2) {
-                                if (r[q] <= r[q + 1]) {
-                                    int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
-                                    ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
-                                          (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
-                                }
-                            }
-                            if (ct == 0) {
-                                // benefit only ever shrinks on a host window or on an SSD
-                                // window without a host path to fall back to
-                                if (dest == TIO_DEST_CPU || !a.has_host) nst |= ST_GONE;
-                            } else {
-                                mine.benefit = (u128)(uint64_t)size * (uint64_t)ct;
-                                mine.cost = doff + dpre;
-                                mine.idx = c;
-                                mine.dest = dest;
-                                mine.off_s = os; mine.off_e = os + doff;
-                                mine.pre_s = ps; mine.pre_e = ps + dpre;
-                                mine.size = size;
-                                for (int q = 0; q < 4; ++q) mine.r[q] = r[q];
-                            }
-                        }
-                        if (nst != st) a.st[c] = nst;
+                        need = overlaps(ld_cg(&a.place[4 * c]), d0, last.off_s, last.off_e, last.nb) ||
+                               overlaps(ld_cg(&a.place[4 * c + 1]), d1, last.pre_s, last.pre_e, last.nb);
                     }
                 }
-                block_best(mine, sm_best);
-                if (threadIdx.x == 0) a.tile_best[t] = mine;
+                if (threadIdx.x == 0) s_nrefit = 0;
+                __syncthreads();
+                if (need) s_refit[atomicAdd(&s_nrefit, 1)] = (int16_t)threadIdx.x;
+                __syncthreads();
+                const int nref = s_nrefit;
+                const bool warp_mode = round > 0 && nref <= WARP_REFIT_MAX;
+                if (nref && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 9], nref);
+                if (warp_mode) {
+                    // one warp per refit: 32-ary searches, 32-wide fit walks
+                    for (int k = warp; k < nref; k += nwarps) {
+                        const int32_t cc = (int32_t)__ldg(&a.tcand[t * TILE + s_refit[k]]);
+                        const int8_t sc = ld_cg(&a.st[cc]);
+                        const int64_t d0 = __ldg(&a.c_d[4 * cc]), d1 = __ldg(&a.c_d[4 * cc + 1]);
+                        int64_t h_off = __ldg(&a.c_ready[cc]), h_pre = __ldg(&a.c_deadline[cc]);
+                        if ((sc & 3) == S_OK) { h_off = ld_cg(&a.place[4 * cc]); h_pre = ld_cg(&a.place[4 * cc + 1]) + d1; }
+                        int64_t os = 0, ps = 0;
+                        const bool ok = warp_fit_pair(cv[0].s, cv[0].e, cv[0].n, cv[1].s, cv[1].e, cv[1].n, d0, d1, I,
+                                                      h_off, h_pre, &os, &ps);
+                        int32_t r[4] = {1, 0, 1, 0};
+                        if (ok)
+                            warp_covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[cc]), __ldg(&a.c_sk[cc]),
+                                                __ldg(&a.c_ek[cc]), __ldg(&a.c_first[cc]), __ldg(&a.c_last[cc]),
+                                                os + d0, ps, r);
+                        if (lane == 0) {
+                            if (ok) {
+                                a.place[4 * cc] = os;
+                                a.place[4 * cc + 1] = ps;
+                                for (int q = 0; q < 4; ++q) a.rng[4 * cc + q] = r[q];
+                            }
+                            a.st[cc] = (int8_t)((sc & ~3) | (ok ? S_OK : S_DEAD));
+                        }
+                        __syncwarp();
+                    }
+                    __syncthreads();
+                    if (need) st = ld_cg(&a.st[c]);
+                }
+                // pass 2: per-candidate evaluation
+                Key mine = none;
+                if (!(st & ST_GONE)) {
+                    int ssd = st & 3, host = (st >> 2) & 3;
+                    const int64_t size = __ldg(&a.c_size[c]);
+                    const int64_t ready = __ldg(&a.c_ready[c]), deadline = __ldg(&a.c_deadline[c]);
+                    bool moved = false;
+                    if (need && !warp_mode) {
+                        const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
+                        int64_t h_off = ready, h_pre = deadline;
+                        if (ssd == S_OK) { h_off = ld_cg(&a.place[4 * c]); h_pre = ld_cg(&a.place[4 * c + 1]) + d1; }
+                        int64_t os, ps;
+                        if (fit_pair(cv[0], cv[1], d0, d1, I, h_off, h_pre, &os, &ps)) {
+                            ssd = S_OK;
+                            a.place[4 * c] = os;
+                            a.place[4 * c + 1] = ps;
+                        } else {
+                            ssd = S_DEAD;
+                        }
+                        moved = true;
+                    }
+                    // host path (only consulted once the SSD path is dead: planner.py:211-227)
+                    if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
+                        const int64_t d2 = __ldg(&a.c_d[4 * c + 2]), d3 = __ldg(&a.c_d[4 * c + 3]);
+                        bool refit = host == H_UNK;
+                        bool recap = false;
+                        if (!refit && last.dest == TIO_DEST_CPU) {
+                            refit = overlaps(ld_cg(&a.place[4 * c + 2]), d2, last.off_s, last.off_e, last.nb) ||
+                                    overlaps(ld_cg(&a.place[4 * c + 3]), d3, last.pre_s, last.pre_e, last.nb);
+                            if (!refit && host == H_OK) {
+                                int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
+                                recap = last.occ_s <= hi && last.occ_e > lo;
+                            }
+                        }
+                        if (refit) {
+                            int64_t os, ps;
+                            int64_t g_off = ready, g_pre = deadline;
+                            if (host != H_UNK) { g_off = ld_cg(&a.place[4 * c + 2]); g_pre = ld_cg(&a.place[4 * c + 3]) + d3; }
+                            if (fit_pair(cv[2], cv[3], d2, d3, I, g_off, g_pre, &os, &ps)) {
+                                a.place[4 * c + 2] = os;
+                                a.place[4 * c + 3] = ps;
+                                recap = true;
+                                moved = true;
+                            } else {
+                                host = H_DEAD;
+                                moved = true;
+                            }
+                        }
+                        if (recap) {
+                            int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
+                            int64_t occ = host_peak(a.occ_s, a.occ_e, a.occ_size, s_nocc, lo, hi);
+                            host = (occ + size > a.host_cap) ? H_CAPFAIL : H_OK;
+                        }
+                    }
+                    int dest = ssd == S_OK ? TIO_DEST_SSD : (ssd == S_DEAD && host == H_OK ? TIO_DEST_CPU : 0);
+                    int8_t nst = (int8_t)(ssd | (host << 2));
+                    if (ssd == S_DEAD && (!a.has_host || host == H_DEAD)) {
+                        nst |= ST_GONE;
+                    } else if (dest) {
+                        const int q0 = dest == TIO_DEST_SSD ? 0 : 2;
+                        const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
+                        int32_t r[4];
+                        if (moved) {
+                            const int64_t os = ld_cg(&a.place[4 * c + q0]);
+                            const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
+                            covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                                           __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
+                                           os + doff, ps, r);
+                            for (int q = 0; q < 4; ++q) a.rng[4 * c + q] = r[q];
+                        } else {
+                            for (int q = 0; q < 4; ++q) r[q] = ld_cg(&a.rng[4 * c + q]);
+                        }
+                        int64_t ct = 0;
+                        for (int q = 0; q < 4; q += 2) {
+                            if (r[q] <= r[q + 1]) {
+                                int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
+                                ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
+                                      (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
+                            }
+                        }
+                        if (ct == 0) {
+                            // benefit only ever shrinks on a host window or on an SSD
+                            // window without a host path to fall back to
+                            if (dest == TIO_DEST_CPU || !a.has_host) nst |= ST_GONE;
+                        } else {
+                            const u128 bf = (u128)(uint64_t)size * (uint64_t)ct;
+                            mine.blo = (uint64_t)bf;
+                            mine.bhi = (uint64_t)(bf >> 64);
+                            mine.cost = doff + dpre;
+                            mine.meta = 4 * (int64_t)c + dest;
+                        }
+                    }
+                    if (nst != st) a.st[c] = nst;
+                }
+                const Key tk = block_best(mine, sm_key);
+                if (threadIdx.x == 0) a.tile_best[t] = tk;
             }
             __syncthreads();
         }
         TICK(1);
         // block best over this block's tiles (unchanged when no tile was dirty)
         if (any_dirty) {
-            Best mine{};
-            mine.benefit = 0;
+            Key mine = none;
             for (int64_t j = threadIdx.x; j < my_tiles; j += blockDim.x) {
-                Best o = a.tile_best[b + j * G];
-                if (better(o, mine)) mine = o;
+                const Key o = a.tile_best[b + j * G];
+                if (kbetter(o, mine)) mine = o;
             }
-            block_best(mine, sm_best);
-            if (threadIdx.x == 0) a.blk_best[b] = mine;
+            const Key bk = block_best(mine, sm_key);
+            if (threadIdx.x == 0) a.blk_best[b] = bk;
         } else if (round == 0 && threadIdx.x == 0) {
-            Best none{};
-            none.benefit = 0;
             a.blk_best[b] = none;
         }
         if (threadIdx.x == 0)
@@ -507,22 +566,35 @@ plan_loop_kernel(PlanArgs a) {
 
         // ---- phase C: global argmax (redundant per block) and commit
         {
-            Best w{};
-            w.benefit = 0;
+            Key w = none;
             for (int j = threadIdx.x; j < G; j += blockDim.x) {
-                Best o = a.blk_best[j];
-                if (better(o, w)) w = o;
+                const Key o = a.blk_best[j];
+                if (kbetter(o, w)) w = o;
             }
-            block_best(w, sm_best);
+            w = block_best(w, sm_key);
             if (threadIdx.x == 0) {
-                s_win = w;
+                WinInfo wi;
+                wi.blo = w.blo; wi.bhi = w.bhi; wi.cost = w.cost;
+                wi.idx = w.meta >> 2;
+                wi.dest = w.meta & 3;
+                if ((w.blo | w.bhi) != 0) {
+                    const int64_t c = wi.idx;
+                    const int q0 = wi.dest == TIO_DEST_SSD ? 0 : 2;
+                    wi.size = __ldg(&a.c_size[c]);
+                    wi.off_s = ld_cg(&a.place[4 * c + q0]);
+                    wi.off_e = wi.off_s + __ldg(&a.c_d[4 * c + q0]);
+                    wi.pre_s = ld_cg(&a.place[4 * c + q0 + 1]);
+                    wi.pre_e = wi.pre_s + __ldg(&a.c_d[4 * c + q0 + 1]);
+                    for (int q = 0; q < 4; ++q) wi.r[q] = ld_cg(&a.rng[4 * c + q]);
+                }
+                s_win = wi;
                 if (b == 0) a.scalars[PS_ROUNDS] = round + 1;
             }
             __syncthreads();
         }
-        const Best w = s_win;
+        const WinInfo w = s_win;
         TICK(4);
-        if (w.benefit == 0) break;  // planner.py:311-312 no viable candidate
+        if ((w.blo | w.bhi) == 0) break;  // planner.py:311-312 no viable candidate
         const int q0 = w.dest == TIO_DEST_SSD ? 0 : 2;
         // new bookings, sorted: (-period, 0, +period)
         int64_t ns[2][3], ne[2][3];
@@ -605,8 +677,8 @@ plan_loop_kernel(PlanArgs a) {
             cm.destination = w.dest;
             cm.off_start = w.off_s; cm.off_end = w.off_e;
             cm.pre_start = w.pre_s; cm.pre_end = w.pre_e;
-            cm.benefit_lo = (uint64_t)w.benefit;
-            cm.benefit_hi = (uint64_t)(w.benefit >> 64);
+            cm.benefit_lo = w.blo;
+            cm.benefit_hi = w.bhi;
             cm.cost = w.cost;
             cm.rel0_lo = w.r[0]; cm.rel0_hi = w.r[1]; cm.rel1_lo = w.r[2]; cm.rel1_hi = w.r[3];
             a.commits[j] = cm;

@@ -21,15 +21,11 @@ enum {
     PS_DBG = 17 /* 16 debug counters */, PS_COUNT = 33
 };
 
-// best candidate of a block (and, after the grid reduction, of the round)
-struct Best {
-    u128 benefit;          // 0 = none
-    int64_t cost;
-    int64_t idx;           // candidate index (planner order); tie-break
-    int64_t dest;          // TIO_DEST_*
-    int64_t off_s, off_e, pre_s, pre_e;
-    int64_t size;
-    int32_t r[4];
+// argmax key of a candidate (benefit 0 = none); meta = 4 * index + destination
+struct Key {
+    uint64_t blo, bhi;     // benefit = size x critical duration (u128)
+    int64_t cost;          // offload + prefetch duration
+    int64_t meta;
 };
 
 struct PlanArgs {
@@ -59,7 +55,7 @@ struct PlanArgs {
     const int32_t *ctile;          // [P] tile of a candidate
     const int64_t *t_lo, *t_hi;    // [ntiles] span [min ready, max deadline)
     const int32_t *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;  // [ntiles] kernel hulls (lo > hi: empty)
-    Best *tile_best;               // [ntiles]
+    Key *tile_best;                // [ntiles]
     // channels: 4 channels (ssd.off, ssd.pre, host.off, host.pre) x 2 buffers
     int64_t *ch_s[4][2];
     int64_t *ch_e[4][2];
@@ -67,7 +63,7 @@ struct PlanArgs {
     // host occupancy intervals (CPU commits)
     int64_t *occ_s, *occ_e, *occ_size;
     // reduction + outputs
-    Best *blk_best;                // [grid]
+    Key *blk_best;                 // [grid]
     tio_commit *commits;           // [P]
     int64_t *scalars;              // [PS_COUNT]
     const int64_t *c_tid;          // [P] tensor id per candidate (for commit records)
