@@ -326,6 +326,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                     "dirty_tiles_per_round": info.dbg[8] / max(1, rounds),
                     "refits_per_round": info.dbg[9] / max(1, rounds),
                     "max_evaluate_us_per_round": info.dbg[10] / 1e3 / max(1, rounds),
+                    "thread_mode_tiles": info.dbg[11], "thread_mode_refits": info.dbg[12],
+                    "max_dirty_tiles_in_a_block_per_round": info.dbg[13] / max(1, rounds),
                     "share_of_step": loop_ms / tot_ms},
         "e2e": {"value": world * E * K / (e2e_ms / 1e3), "unit": "events/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "tio_plan_host (C ABI), pinned host buffers"},

@@ -106,8 +106,10 @@ typedef struct tio_plan_info {
     int64_t loop_ns;               /* CUDA-event time of the round-loop kernel */
     /* round-loop phase profile (block 0, ns): prologue, evaluate, block
      * reduce, barrier 1, argmax, channel merge, residual, commit+barrier 2;
-     * then dirty tiles, refits, sum of per-round max evaluate time, unused */
-    int64_t dbg[12];
+     * then dirty tiles, refits, sum of per-round max evaluate time,
+     * per-thread-mode tiles, their refits, sum of per-round max dirty tiles
+     * of one block */
+    int64_t dbg[14];
 } tio_plan_info;
 
 /* One CommittedMigration (planner.py:97-111), commit order.  Relieved

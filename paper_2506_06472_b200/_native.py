@@ -71,7 +71,7 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [(n, _i64) for n in ("num_commits", "num_entries", "num_over", "capacity_bytes",
                                     "residual_peak_bytes", "planned_host_bytes", "num_candidates",
                                     "rounds", "unsat_kernel", "unsat_bytes", "loop_ns")] + [
-        ("dbg", _i64 * 12)]
+        ("dbg", _i64 * 14)]
 
 
 COMMIT_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("start_kernel", "<i8"),

@@ -412,6 +412,8 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     PTRY(A.alloc(&c_d, 4 * P)); PTRY(A.alloc(&c_tid, P)); PTRY(A.alloc(&place, 4 * P));
     PTRY(A.alloc(&c_sk, P)); PTRY(A.alloc(&c_ek, P)); PTRY(A.alloc(&c_first, P)); PTRY(A.alloc(&c_last, P));
     PTRY(A.alloc(&c_tpos, P)); PTRY(A.alloc(&rng, 4 * P));
+    int32_t *hidx, *hver;
+    PTRY(A.alloc(&hidx, 2 * P)); PTRY(A.alloc(&hver, P));
     PTRY(A.alloc(&c_wraps, P)); PTRY(A.alloc(&st, P));
     if (P > 0) {
         CandBuild cb;
@@ -486,7 +488,7 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     a.starts = t->starts; a.dur = t->dur; a.resid = resid; a.local_cp = local_cp; a.chunk_sum = chunk_sum;
     a.c_size = c_size; a.c_sk = c_sk; a.c_ek = c_ek; a.c_first = c_first; a.c_last = c_last; a.c_wraps = c_wraps;
     a.c_ready = c_ready; a.c_deadline = c_deadline; a.c_d = c_d;
-    a.st = st; a.place = place; a.rng = rng;
+    a.st = st; a.place = place; a.rng = rng; a.hidx = hidx; a.hver = hver;
     a.ch_cap = ch_cap;
     a.occ_s = occ_s; a.occ_e = occ_e; a.occ_size = occ_z;
     a.blk_best = blk_best; a.commits = p->commits; a.scalars = ps; a.c_tid = c_tid; a.c_tpos = c_tpos;
@@ -523,7 +525,7 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     pi.num_commits = nc;
     pi.num_entries = 2 * nc;
     pi.rounds = hs[PS_ROUNDS];
-    for (int q = 0; q < 12; ++q) pi.dbg[q] = hs[PS_DBG + q];
+    for (int q = 0; q < 14; ++q) pi.dbg[q] = hs[PS_DBG + q];
 
     // ---- epilogue: over list, peak, planned host, sorted + urgent entries
     p->resid = resid;

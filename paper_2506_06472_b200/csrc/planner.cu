@@ -49,34 +49,86 @@ struct ChanView {
     int64_t n;
 };
 
-// ---------------------------------------------------------------- channels
-// bandwidth.py:88-100 reserve_earliest
-__device__ int64_t ch_earliest(const ChanView &c, int64_t ready, int64_t d) {
-    int64_t lo = 0, hi = c.n;
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (ld_cg(c.e + mid) > ready) hi = mid; else lo = mid + 1;
+// ---------------------------------------------------------------- searches
+// first k in [lo, hi) with pred(k) (monotone false..true), hi if none;
+// exponential probing upward from lo, then bisection.
+template <typename Pred>
+__device__ __forceinline__ int64_t gallop_up(int64_t lo, int64_t hi, Pred pred) {
+    if (lo >= hi || pred(lo)) return lo;
+    int64_t f = lo, step = 1;          // pred(f) false
+    int64_t t = hi;                    // pred(t) true (hi by convention)
+    while (true) {
+        const int64_t x = f + step;
+        if (x >= hi) break;
+        if (pred(x)) { t = x; break; }
+        f = x;
+        step <<= 1;
     }
+    while (t - f > 1) {
+        const int64_t m = f + ((t - f) >> 1);
+        if (pred(m)) t = m; else f = m;
+    }
+    return t;
+}
+
+// same, probing downward from hi - 1 (the answer is expected near hi)
+template <typename Pred>
+__device__ __forceinline__ int64_t gallop_down(int64_t lo, int64_t hi, Pred pred) {
+    if (lo >= hi || !pred(hi - 1)) return hi;
+    int64_t t = hi - 1, step = 1;      // pred(t) true
+    int64_t f = lo - 1;                // pred(f) false (lo - 1 by convention)
+    while (true) {
+        const int64_t x = t - step;
+        if (x < lo) break;
+        if (!pred(x)) { f = x; break; }
+        t = x;
+        step <<= 1;
+    }
+    while (t - f > 1) {
+        const int64_t m = f + ((t - f) >> 1);
+        if (pred(m)) t = m; else f = m;
+    }
+    return t;
+}
+
+// bisection for a cold search, galloping from lo for a hinted one
+template <typename Pred>
+__device__ __forceinline__ int64_t first_true(int64_t lo, int64_t hi, bool cold, Pred pred) {
+    if (!cold) return gallop_up(lo, hi, pred);
+    while (lo < hi) {
+        const int64_t m = (lo + hi) >> 1;
+        if (pred(m)) hi = m; else lo = m + 1;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------- channels
+// bandwidth.py:88-100 reserve_earliest.  The first booking that can matter
+// (end > ready) lies in [lo_idx, hi_idx] (0..n for a cold search; a window
+// from the candidate's last fit for a refit).  *p = index where the walk
+// stopped: every booking before it ends at or before the fit.
+__device__ int64_t ch_earliest(const ChanView &c, int64_t ready, int64_t d, int64_t lo_idx, int64_t hi_idx,
+                               bool cold, int64_t *p) {
+    int64_t i = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return ld_cg(c.e + j) > ready; });
     int64_t t = ready;
-    for (int64_t i = lo; i < c.n; ++i) {
+    for (; i < c.n; ++i) {
         int64_t s = ld_cg(c.s + i);
         if (s >= t + d) break;
         int64_t e = ld_cg(c.e + i);
         if (e > t) t = e;
     }
+    *p = i;
     return t;
 }
 
-// bandwidth.py:102-120 reserve_latest; false = None
+// bandwidth.py:102-120 reserve_latest; false = None.  The first booking at or
+// after the deadline lies in [lo_idx, hi_idx]; *q = first booking after the fit.
 __device__ bool ch_latest(const ChanView &c, int64_t deadline, int64_t not_before, int64_t d,
-                          int64_t *out) {
+                          int64_t lo_idx, int64_t hi_idx, bool cold, int64_t *out, int64_t *q) {
     int64_t start = deadline - d;
-    int64_t lo = 0, hi = c.n;
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (ld_cg(c.s + mid) < deadline) lo = mid + 1; else hi = mid;
-    }
-    for (int64_t i = lo - 1; i >= 0; --i) {
+    const int64_t lo = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return ld_cg(c.s + j) >= deadline; });
+    int64_t i = lo - 1;
+    for (; i >= 0; --i) {
         if (start < not_before) return false;
         int64_t s = ld_cg(c.s + i);
         if (s >= start + d) continue;
@@ -86,6 +138,7 @@ __device__ bool ch_latest(const ChanView &c, int64_t deadline, int64_t not_befor
     }
     if (start < not_before) return false;
     *out = start;
+    *q = i + 1;
     return true;
 }
 
@@ -95,17 +148,29 @@ __device__ bool ch_latest(const ChanView &c, int64_t deadline, int64_t not_befor
 // searches restart from the cached placement (hint_off / hint_pre_end) instead
 // of from ready / deadline, which gives the same optimum without re-walking
 // the packed prefix.  First fits pass hint_off = ready, hint_pre_end = deadline.
+// Index hints: (hp, hq) from the last fit at channel size hn; since then at
+// most n - hn bookings were inserted, so the searched indices lie in
+// [hp, hp + n - hn] and [hq, hq + n - hn].  hn < 0: cold search.
 __device__ bool fit_pair(const ChanView &off, const ChanView &pre, int64_t d_off, int64_t d_pre,
                          int64_t iteration, int64_t hint_off, int64_t hint_pre_end,
-                         int64_t *off_s, int64_t *pre_s) {
+                         int64_t *off_s, int64_t *pre_s, int64_t hp = 0, int64_t hq = 0, int64_t hn = -1,
+                         int64_t *np_ = nullptr, int64_t *nq_ = nullptr) {
     if (d_off > iteration || d_pre > iteration) return false;
-    int64_t o = ch_earliest(off, hint_off, d_off);
+    int64_t plo = 0, phi = off.n, qlo = 0, qhi = pre.n;
+    if (hn >= 0) {
+        const int64_t delta = off.n - hn;
+        plo = hp; phi = hp + delta < off.n ? hp + delta : off.n;
+        qlo = hq; qhi = hq + delta < pre.n ? hq + delta : pre.n;
+    }
+    int64_t p, q;
+    int64_t o = ch_earliest(off, hint_off, d_off, plo, phi, hn < 0, &p);
     int64_t t_off = o + d_off;
     int64_t f;
-    if (!ch_latest(pre, hint_pre_end, t_off, d_pre, &f)) return false;
+    if (!ch_latest(pre, hint_pre_end, t_off, d_pre, qlo, qhi, hn < 0, &f, &q)) return false;
     if (!(t_off < f)) return false;
     *off_s = o;
     *pre_s = f;
+    if (np_) { *np_ = p; *nq_ = q; }
     return true;
 }
 
@@ -153,6 +218,22 @@ __device__ void covered_ranges(const int64_t *__restrict__ starts, int64_t N, in
     } else {
         if (last + 1 <= N - 1) range(last + 1, N - 1, 0, r[0], r[1]);
         if (first - 1 >= 0) range(0, first - 1, iteration, r[2], r[3]);
+    }
+}
+
+// Refit version: the new window [lo_t, hi_t] lies inside the old one, so each
+// new range lies inside the old range r_old (planner.py:232-250 restated);
+// gallop inward from the old endpoints.
+__device__ void covered_ranges_shrunk(const int64_t *__restrict__ starts, int64_t iteration, int wraps,
+                                      int64_t lo_t, int64_t hi_t, const int32_t r_old[4], int32_t r[4]) {
+    for (int q = 0; q < 4; q += 2) {
+        const int64_t a = r_old[q], bnd = r_old[q + 1];
+        if (a > bnd) { r[q] = r_old[q]; r[q + 1] = r_old[q + 1]; continue; }
+        const int64_t sh = (wraps && q == 2) ? iteration : 0;
+        const int64_t klo = gallop_up(a, bnd + 1, [&](int64_t k) { return __ldg(starts + k) + sh >= lo_t; });
+        const int64_t kend = gallop_down(klo, bnd + 1, [&](int64_t k) { return __ldg(starts + k + 1) + sh > hi_t; });
+        r[q] = (int32_t)klo;
+        r[q + 1] = (int32_t)(kend - 1);
     }
 }
 
@@ -389,6 +470,7 @@ plan_loop_kernel(PlanArgs a) {
             __syncthreads();
             const int nd = s_ndirty;
             if (nd) any_dirty = true;
+            if (nd && threadIdx.x == 0) atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 14]), (long long)nd);
             if (nd && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 8], nd);
             for (int di = 0; di < nd; ++di) {
                 const int64_t t = s_dirty[di];
@@ -412,6 +494,10 @@ plan_loop_kernel(PlanArgs a) {
                 __syncthreads();
                 const int nref = s_nrefit;
                 const bool warp_mode = round > 0 && nref <= WARP_REFIT_MAX;
+                if (!warp_mode && nref && threadIdx.x == 0) {
+                    atomic_add_i64(&a.scalars[PS_DBG + 11], 1);
+                    atomic_add_i64(&a.scalars[PS_DBG + 12], nref);
+                }
                 if (nref && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 9], nref);
                 if (warp_mode) {
                     // one warp per refit: 32-ary searches, 32-wide fit walks
@@ -420,20 +506,39 @@ plan_loop_kernel(PlanArgs a) {
                         const int8_t sc = ld_cg(&a.st[cc]);
                         const int64_t d0 = __ldg(&a.c_d[4 * cc]), d1 = __ldg(&a.c_d[4 * cc + 1]);
                         int64_t h_off = __ldg(&a.c_ready[cc]), h_pre = __ldg(&a.c_deadline[cc]);
-                        if ((sc & 3) == S_OK) { h_off = ld_cg(&a.place[4 * cc]); h_pre = ld_cg(&a.place[4 * cc + 1]) + d1; }
-                        int64_t os = 0, ps = 0;
+                        const bool hinted = (sc & 3) == S_OK;
+                        int64_t plo = 0, phi = cv[0].n, qlo = 0, qhi = cv[1].n;
+                        int32_t ro[4] = {1, 0, 1, 0};
+                        if (hinted) {
+                            h_off = ld_cg(&a.place[4 * cc]);
+                            h_pre = ld_cg(&a.place[4 * cc + 1]) + d1;
+                            const int64_t delta = cv[0].n - ld_cg(&a.hver[cc]);
+                            plo = ld_cg(&a.hidx[2 * cc]);
+                            qlo = ld_cg(&a.hidx[2 * cc + 1]);
+                            phi = plo + delta < phi ? plo + delta : phi;
+                            qhi = qlo + delta < qhi ? qlo + delta : qhi;
+                            for (int q = 0; q < 4; ++q) ro[q] = ld_cg(&a.rng[4 * cc + q]);
+                        }
+                        int64_t os = 0, ps = 0, np = 0, nq = 0;
                         const bool ok = warp_fit_pair(cv[0].s, cv[0].e, cv[0].n, cv[1].s, cv[1].e, cv[1].n, d0, d1, I,
-                                                      h_off, h_pre, &os, &ps);
+                                                      h_off, h_pre, plo, phi, qlo, qhi, &os, &ps, &np, &nq);
                         int32_t r[4] = {1, 0, 1, 0};
-                        if (ok)
-                            warp_covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[cc]), __ldg(&a.c_sk[cc]),
-                                                __ldg(&a.c_ek[cc]), __ldg(&a.c_first[cc]), __ldg(&a.c_last[cc]),
-                                                os + d0, ps, r);
+                        if (ok) {
+                            if (hinted)
+                                warp_covered_ranges_shrunk(a.starts, I, __ldg(&a.c_wraps[cc]), os + d0, ps, ro, r);
+                            else
+                                warp_covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[cc]), __ldg(&a.c_sk[cc]),
+                                                    __ldg(&a.c_ek[cc]), __ldg(&a.c_first[cc]), __ldg(&a.c_last[cc]),
+                                                    os + d0, ps, r);
+                        }
                         if (lane == 0) {
                             if (ok) {
                                 a.place[4 * cc] = os;
                                 a.place[4 * cc + 1] = ps;
                                 for (int q = 0; q < 4; ++q) a.rng[4 * cc + q] = r[q];
+                                a.hidx[2 * cc] = (int32_t)np;
+                                a.hidx[2 * cc + 1] = (int32_t)nq;
+                                a.hver[cc] = (int32_t)cv[0].n;
                             }
                             a.st[cc] = (int8_t)((sc & ~3) | (ok ? S_OK : S_DEAD));
                         }
@@ -452,16 +557,36 @@ plan_loop_kernel(PlanArgs a) {
                     if (need && !warp_mode) {
                         const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
                         int64_t h_off = ready, h_pre = deadline;
-                        if (ssd == S_OK) { h_off = ld_cg(&a.place[4 * c]); h_pre = ld_cg(&a.place[4 * c + 1]) + d1; }
-                        int64_t os, ps;
-                        if (fit_pair(cv[0], cv[1], d0, d1, I, h_off, h_pre, &os, &ps)) {
+                        const bool hinted = ssd == S_OK;
+                        int64_t hp = 0, hq = 0, hn = -1;
+                        if (hinted) {
+                            h_off = ld_cg(&a.place[4 * c]);
+                            h_pre = ld_cg(&a.place[4 * c + 1]) + d1;
+                            hp = ld_cg(&a.hidx[2 * c]); hq = ld_cg(&a.hidx[2 * c + 1]); hn = ld_cg(&a.hver[c]);
+                        }
+                        int64_t os, ps, np, nq;
+                        if (fit_pair(cv[0], cv[1], d0, d1, I, h_off, h_pre, &os, &ps, hp, hq, hn, &np, &nq)) {
+                            int32_t r[4];
+                            if (hinted) {
+                                int32_t ro[4];
+                                for (int q = 0; q < 4; ++q) ro[q] = ld_cg(&a.rng[4 * c + q]);
+                                covered_ranges_shrunk(a.starts, I, __ldg(&a.c_wraps[c]), os + d0, ps, ro, r);
+                            } else {
+                                covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                                               __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
+                                               os + d0, ps, r);
+                            }
+                            for (int q = 0; q < 4; ++q) a.rng[4 * c + q] = r[q];
                             ssd = S_OK;
                             a.place[4 * c] = os;
                             a.place[4 * c + 1] = ps;
+                            a.hidx[2 * c] = (int32_t)np;
+                            a.hidx[2 * c + 1] = (int32_t)nq;
+                            a.hver[c] = (int32_t)cv[0].n;
                         } else {
                             ssd = S_DEAD;
+                            moved = true;
                         }
-                        moved = true;
                     }
                     // host path (only consulted once the SSD path is dead: planner.py:211-227)
                     if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
@@ -554,14 +679,17 @@ plan_loop_kernel(PlanArgs a) {
         } else if (round == 0 && threadIdx.x == 0) {
             a.blk_best[b] = none;
         }
-        if (threadIdx.x == 0)
+        if (threadIdx.x == 0) {
             atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 15]), (long long)(gtime() - te0));
+        }
         TICK(2);
         grid.sync();
         TICK(3);
         if (tb) {
             a.scalars[PS_DBG + 10] += ld_cg(&a.scalars[PS_DBG + 15]);
             a.scalars[PS_DBG + 15] = 0;
+            a.scalars[PS_DBG + 13] += ld_cg(&a.scalars[PS_DBG + 14]);
+            a.scalars[PS_DBG + 14] = 0;
         }
 
         // ---- phase C: global argmax (redundant per block) and commit

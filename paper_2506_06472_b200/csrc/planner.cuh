@@ -49,6 +49,8 @@ struct PlanArgs {
     int8_t *st;                    // [P]
     int64_t *place;                // [4P] ssd_off_s, ssd_pre_s, host_off_s, host_pre_s
     int32_t *rng;                  // [4P]
+    int32_t *hidx;                 // [2P] SSD channel index hints of the last fit (p, q)
+    int32_t *hver;                 // [P]  SSD channel size at the last fit
     // tiles: candidates in ready-time order, TILE per tile
     int64_t ntiles;
     const uint32_t *tcand;         // [P] candidate at tile position

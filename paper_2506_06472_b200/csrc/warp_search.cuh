@@ -39,10 +39,13 @@ __device__ __forceinline__ int64_t warp_lower_bound(int64_t lo, int64_t hi, Pred
 }
 
 // reserve_earliest (bandwidth.py:88-100) on sorted disjoint [s, e) arrays.
+// The first booking that can matter lies in [lo_idx, hi_idx]; *p = index
+// where the walk stopped (every booking before it ends at or before the fit).
 __device__ __forceinline__ int64_t warp_earliest(const int64_t *cs, const int64_t *ce, int64_t n,
-                                                 int64_t ready, int64_t d) {
+                                                 int64_t ready, int64_t d, int64_t lo_idx, int64_t hi_idx,
+                                                 int64_t *p) {
     const int lane = threadIdx.x & 31;
-    int64_t i = warp_lower_bound(0, n, [&](int64_t j) { return ld_cg(ce + j) > ready; });
+    int64_t i = warp_lower_bound(lo_idx, hi_idx, [&](int64_t j) { return ld_cg(ce + j) > ready; });
     int64_t t = ready;
     while (i < n) {
         const int64_t j = i + lane;
@@ -56,21 +59,26 @@ __device__ __forceinline__ int64_t warp_earliest(const int64_t *cs, const int64_
         const unsigned m = __ballot_sync(0xffffffffu, gap);
         if (m) {
             const int f = __ffs(m) - 1;
+            *p = i + f;
             return __shfl_sync(0xffffffffu, tj, f);
         }
         const int64_t last_e = __shfl_sync(0xffffffffu, e, 31);
         t = last_e > t ? last_e : t;
         i += 32;
     }
+    *p = n;
     return t;
 }
 
 // reserve_latest (bandwidth.py:102-120); false = None.
+// The first booking at or after the deadline lies in [lo_idx, hi_idx];
+// *q = first booking after the fit.
 __device__ __forceinline__ bool warp_latest(const int64_t *cs, const int64_t *ce, int64_t n, int64_t deadline,
-                                            int64_t not_before, int64_t d, int64_t *out) {
+                                            int64_t not_before, int64_t d, int64_t lo_idx, int64_t hi_idx,
+                                            int64_t *out, int64_t *q) {
     const int lane = threadIdx.x & 31;
     // last index with s < deadline = (first index with s >= deadline) - 1
-    int64_t i = warp_lower_bound(0, n, [&](int64_t j) { return ld_cg(cs + j) >= deadline; }) - 1;
+    int64_t i = warp_lower_bound(lo_idx, hi_idx, [&](int64_t j) { return ld_cg(cs + j) >= deadline; }) - 1;
     int64_t start = deadline - d;
     // Walking down from i: every visited booking starts before start + d
     // (sorted, disjoint), so the reference's `continue` branch never fires;
@@ -89,6 +97,7 @@ __device__ __forceinline__ bool warp_latest(const int64_t *cs, const int64_t *ce
             const int64_t st = __shfl_sync(0xffffffffu, sj, f);
             if (st < not_before) return false;
             *out = st;
+            *q = i - f + 1;
             return true;
         }
         start = __shfl_sync(0xffffffffu, s, 31) - d;
@@ -96,6 +105,7 @@ __device__ __forceinline__ bool warp_latest(const int64_t *cs, const int64_t *ce
     }
     if (start < not_before) return false;
     *out = start;
+    *q = 0;
     return true;
 }
 
@@ -104,12 +114,14 @@ __device__ __forceinline__ bool warp_latest(const int64_t *cs, const int64_t *ce
 __device__ __forceinline__ bool warp_fit_pair(const int64_t *os_, const int64_t *oe_, int64_t on,
                                               const int64_t *ps_, const int64_t *pe_, int64_t pn,
                                               int64_t d_off, int64_t d_pre, int64_t iteration, int64_t hint_off,
-                                              int64_t hint_pre_end, int64_t *off_s, int64_t *pre_s) {
+                                              int64_t hint_pre_end, int64_t plo, int64_t phi, int64_t qlo,
+                                              int64_t qhi, int64_t *off_s, int64_t *pre_s, int64_t *np,
+                                              int64_t *nq) {
     if (d_off > iteration || d_pre > iteration) return false;
-    const int64_t o = warp_earliest(os_, oe_, on, hint_off, d_off);
+    const int64_t o = warp_earliest(os_, oe_, on, hint_off, d_off, plo, phi, np);
     const int64_t t_off = o + d_off;
     int64_t f;
-    if (!warp_latest(ps_, pe_, pn, hint_pre_end, t_off, d_pre, &f)) return false;
+    if (!warp_latest(ps_, pe_, pn, hint_pre_end, t_off, d_pre, qlo, qhi, &f, nq)) return false;
     if (!(t_off < f)) return false;
     *off_s = o;
     *pre_s = f;
@@ -134,6 +146,22 @@ __device__ __forceinline__ void warp_covered_ranges(const int64_t *__restrict__ 
     } else {
         if (last + 1 <= N - 1) range(last + 1, N - 1, 0, r[0], r[1]);
         if (first - 1 >= 0) range(0, first - 1, iteration, r[2], r[3]);
+    }
+}
+
+// Refit version of warp_covered_ranges: the window only shrank, so each new
+// range lies inside the old one.
+__device__ __forceinline__ void warp_covered_ranges_shrunk(const int64_t *__restrict__ starts, int64_t iteration,
+                                                           int wraps, int64_t lo_t, int64_t hi_t,
+                                                           const int32_t r_old[4], int32_t r[4]) {
+    for (int q = 0; q < 4; q += 2) {
+        const int64_t a = r_old[q], b = r_old[q + 1];
+        if (a > b) { r[q] = r_old[q]; r[q + 1] = r_old[q + 1]; continue; }
+        const int64_t sh = (wraps && q == 2) ? iteration : 0;
+        const int64_t klo = warp_lower_bound(a, b + 1, [&](int64_t k) { return __ldg(starts + k) + sh >= lo_t; });
+        const int64_t kend = warp_lower_bound(klo, b + 1, [&](int64_t k) { return __ldg(starts + k + 1) + sh > hi_t; });
+        r[q] = (int32_t)klo;
+        r[q + 1] = (int32_t)(kend - 1);
     }
 }
 
