@@ -188,6 +188,24 @@ int tio_plan_host(const tio_trace_desc *desc, int64_t capacity, const tio_rates 
                   int64_t host_cap, void *stream, tio_plan_info *info,
                   tio_entry *entries, int64_t entries_cap);
 
+/* ---- migration engine scheduler -------------------------------------------
+ * Replaces simulator.py:539-547 simulate / simulate_on_demand (an empty entry
+ * list) and the `_Engine` semantics (simulator.py:178-528) that the runtime
+ * engine executes: host C++ discrete-event model on host trace columns.
+ * entries: plan entries (tensor_id, trigger_us, deadline_us, action, target
+ * (1 SSD / 2 CPU for offloads), urgent); tensor_pos is ignored.
+ * TIO_ERR_SIMULATION (SimulationError) when a kernel's active bytes exceed
+ * capacity or the run gets stuck.  Per-kernel arrays may be NULL. */
+typedef struct tio_sim_report {
+    int64_t total_time, ideal_time, stall_time_total, peak_resident_bytes, emergency_offloads;
+    int64_t channel_busy[4];   /* ssd.offload, ssd.prefetch, host.offload, host.prefetch: us booked in [0, total] */
+    int64_t num_transfers;
+} tio_sim_report;
+
+int tio_simulate(const tio_trace_desc *trace, const tio_entry *entries, int64_t num_entries,
+                 int64_t capacity, const tio_rates *rates, tio_sim_report *report,
+                 int64_t *per_kernel_start, int64_t *stall_per_kernel, int64_t *per_kernel_resident);
+
 /* ---- channel primitives (bandwidth.py:75-84) ------------------------------- */
 /* ceil(nbytes / rate) exactly; TIO_ERR_CHANNEL_CONFIG for rate <= 0. */
 int tio_transfer_duration(double rate, int64_t nbytes, int64_t *out);

@@ -74,6 +74,11 @@ class PlanInfo(ctypes.Structure):
         ("dbg", _i64 * 14)]
 
 
+class SimReportC(ctypes.Structure):
+    _fields_ = [(n, _i64) for n in ("total_time", "ideal_time", "stall_time_total", "peak_resident_bytes",
+                                    "emergency_offloads")] + [("channel_busy", _i64 * 4), ("num_transfers", _i64)]
+
+
 COMMIT_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("start_kernel", "<i8"),
                          ("end_kernel", "<i8"), ("wraps", "<i8"), ("destination", "<i8"),
                          ("off_start", "<i8"), ("off_end", "<i8"), ("pre_start", "<i8"),
@@ -88,7 +93,7 @@ ENTRY_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("trigger_u
 EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_device_info", "tio_trace_create",
            "tio_trace_destroy", "tio_lifetime", "tio_lifetime_view_get", "tio_lifetime_copy_out",
            "tio_plan_create", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
-           "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration")
+           "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate")
 
 
 def lib_path() -> str:

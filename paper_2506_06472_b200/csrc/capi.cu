@@ -13,6 +13,7 @@
 #include "plan_setup.cuh"
 #include "radix_sort.cuh"
 #include "scan.cuh"
+#include "engine_sched.cuh"
 
 namespace tio {
 
@@ -70,7 +71,7 @@ static int ensure_pool() {
 }
 
 // Decode a rate into the exact integer form used by duration_of.
-static int decode_rate(double rate, RateCode *rc) {
+int decode_rate(double rate, RateCode *rc) {
     memset(rc, 0, sizeof(*rc));
     if (!(rate > 0) || std::isnan(rate) || std::isinf(rate))
         return fail(TIO_ERR_CHANNEL_CONFIG, "rate must be > 0");
@@ -670,3 +671,49 @@ int tio_plan_host(const tio_trace_desc *desc, int64_t capacity, const tio_rates 
 }
 
 }  // extern "C"
+
+// ---- engine scheduler (simulator.py:178-560) ----------------------------------
+extern "C" int tio_simulate(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries, int64_t capacity,
+                            const tio_rates *rates, tio_sim_report *report, int64_t *per_kernel_start,
+                            int64_t *stall_per_kernel, int64_t *per_kernel_resident) {
+    if (!d || !rates || !report || (num_entries > 0 && !entries)) return fail(TIO_ERR_INVALID, "null argument");
+    SchedInput in;
+    in.N = d->num_kernels; in.T = d->num_tensors;
+    in.dur = d->duration_us; in.tid = d->tensor_id; in.size = d->size_bytes; in.kind = d->kind;
+    in.ptr = d->access_ptr; in.acc = d->accesses;
+    std::vector<int64_t> e_tid(num_entries), e_trig(num_entries), e_dl(num_entries);
+    std::vector<int32_t> e_act(num_entries), e_tgt(num_entries), e_urg(num_entries);
+    for (int64_t i = 0; i < num_entries; ++i) {
+        e_tid[i] = entries[i].tensor_id; e_trig[i] = entries[i].trigger_us; e_dl[i] = entries[i].deadline_us;
+        e_act[i] = entries[i].action; e_tgt[i] = entries[i].target; e_urg[i] = entries[i].urgent;
+    }
+    in.num_entries = num_entries;
+    in.e_tid = e_tid.data(); in.e_trigger = e_trig.data(); in.e_deadline = e_dl.data();
+    in.e_action = e_act.data(); in.e_target = e_tgt.data(); in.e_urgent = e_urg.data();
+    in.capacity = capacity;
+    in.rate[0] = rates->ssd_offload; in.rate[1] = rates->ssd_prefetch;
+    in.rate[2] = rates->host_offload; in.rate[3] = rates->host_prefetch;
+    in.has_host = rates->has_host;
+    for (int64_t t = 0; t < in.T; ++t)
+        for (int64_t j = in.ptr[t]; j < in.ptr[t + 1]; ++j)
+            if (in.acc[j] < 0 || in.acc[j] >= in.N) return fail(TIO_ERR_INVALID, "access out of range");
+    SchedOutput out;
+    std::string err;
+    int rc = engine_schedule(in, &out, &err);
+    if (rc != TIO_OK) return fail(rc, "%s", err.c_str());
+    memset(report, 0, sizeof(*report));
+    report->total_time = out.total_time;
+    report->ideal_time = out.ideal_time;
+    report->stall_time_total = out.stall_total;
+    report->peak_resident_bytes = out.peak_resident;
+    report->emergency_offloads = out.emergency;
+    for (int c = 0; c < 4; ++c) report->channel_busy[c] = out.busy[c];
+    report->num_transfers = (int64_t)out.transfers.size();
+    const size_t nb = sizeof(int64_t) * (size_t)in.N;
+    if (in.N) {
+        if (per_kernel_start) memcpy(per_kernel_start, out.start.data(), nb);
+        if (stall_per_kernel) memcpy(stall_per_kernel, out.stall.data(), nb);
+        if (per_kernel_resident) memcpy(per_kernel_resident, out.resident.data(), nb);
+    }
+    return TIO_OK;
+}

@@ -65,6 +65,9 @@ struct RateCode {
     int32_t huge;   // integral rate >= 2^63: every non-empty transfer takes 1 us
 };
 
+// Decode a rate (bytes/us, a double) into RateCode; TIO_ERR_CHANNEL_CONFIG if <= 0.
+int decode_rate(double rate, RateCode *rc);
+
 __host__ __device__ __forceinline__ int64_t duration_of(const RateCode &r, int64_t nbytes) {
     if (nbytes <= 0) return 0;
     if (r.huge) return 1;

@@ -171,6 +171,41 @@ def llama1(ref):
     return [rec]
 
 
+def _sim_record(ref, trace, plan_text, capacity, rates):
+    """Reference simulate() (simulator.py:539-542) under the plan and with no
+    plan (simulate_on_demand, :545-547); SimulationError recorded as text."""
+    out = {}
+    for key, entries in (("plan", ref.parse_plan(plan_text)[1] if plan_text else None), ("on_demand", None)):
+        try:
+            r = ref.simulate(trace, entries, capacity, rates) if entries is not None else \
+                ref.simulate_on_demand(trace, capacity, rates)
+        except ref.SimulationError as exc:
+            out[key] = {"error": str(exc)}
+            continue
+        out[key] = {"total_time": r.total_time, "ideal_time": r.ideal_time,
+                    "per_kernel_start": r.per_kernel_start, "stall_per_kernel": r.stall_per_kernel,
+                    "per_kernel_resident": r.per_kernel_resident, "stall_time_total": r.stall_time_total,
+                    "peak_resident_bytes": r.peak_resident_bytes, "channel_utilization": r.channel_utilization,
+                    "emergency_offloads": r.emergency_offloads, "throughput_vs_ideal": r.throughput_vs_ideal}
+    return out
+
+
+def sim(ref):
+    """simulate / simulate_on_demand on the criterion-2 corpus (every case,
+    with its reference plan) and on C1 + llama1."""
+    cases = []
+    for rec in json.load(gzip.open(os.path.join(HERE, "crit2.json.gz"), "rt")):
+        g = rec["gen"]
+        trace = ref.gen_random_trace(g["seed"], g["num_kernels"], g["num_tensors"],
+                                     size_range=tuple(g["size_range"]), duration_range=tuple(g["duration_range"]))
+        so, sp, ho, hp = rec["rates"]
+        rates = ref.ChannelRates(so, sp, ho, hp)
+        out = _sim_record(ref, trace, rec.get("plan"), rec["capacity"], rates)
+        out.update({"corpus": "crit2", "gen": g, "trace_sha256": rec["trace_sha256"]})
+        cases.append(out)
+    return cases
+
+
 def _dump(name, cases):
     path = os.path.join(HERE, f"{name}.json.gz")
     with gzip.open(path, "wt", encoding="utf-8", compresslevel=9) as f:
@@ -184,7 +219,7 @@ def main(argv=None):
     ap.add_argument("--only", default=None)
     args = ap.parse_args(argv)
     ref = _ref()
-    todo = {"crit2": crit2, "crit3": crit3, "c1": c1}
+    todo = {"crit2": crit2, "crit3": crit3, "c1": c1, "sim": sim}
     if args.llama1:
         todo["llama1"] = llama1
     for name, fn in todo.items():

@@ -1,0 +1,85 @@
+"""The migration engine's scheduler (libtio csrc/engine_sched.cu, host C++)
+against the reference engine model: every SimReport field of the
+reference's simulate() / simulate_on_demand() on the criterion-2 corpus
+(tests/golden/sim.json.gz, produced by the reference), plus the engine known
+answers of reference test_simulator.py:27-74.  Host-only: runs without a GPU.
+"""
+
+from __future__ import annotations
+
+import pytest
+
+from conftest import load_golden, mk_trace, regen
+from paper_2506_06472_b200 import (
+    ChannelRates, PlanEntry, SimulationError, simulate, simulate_ideal, simulate_on_demand)
+from paper_2506_06472_b200.planner import parse_plan
+from paper_2506_06472_b200.simulator import report_json, timeline_csv
+
+MB100 = 100_000_000
+CAP = 150_000_000
+FIELDS = ("total_time", "ideal_time", "per_kernel_start", "stall_per_kernel", "per_kernel_resident",
+          "stall_time_total", "peak_resident_bytes", "channel_utilization", "emergency_offloads",
+          "throughput_vs_ideal")
+
+
+def _cmp(got, want):
+    for f in FIELDS:
+        assert getattr(got, f) == want[f], f
+
+
+def test_scheduler_matches_reference_simulate_on_crit2_corpus():
+    sims = load_golden("sim")
+    plans = {r["trace_sha256"]: r for r in load_golden("crit2")}
+    checked = 0
+    for rec in sims:
+        tr = regen({**rec, "gen": rec["gen"]})
+        base = plans[rec["trace_sha256"]]
+        so, sp, ho, hp = base["rates"]
+        rates = ChannelRates(so, sp, ho, hp)
+        cap = base["capacity"]
+        entries = parse_plan(base["plan"])[1] if "plan" in base else None
+        for key, fn in (("plan", lambda: simulate(tr, entries, cap, rates)),
+                        ("on_demand", lambda: simulate_on_demand(tr, cap, rates))):
+            want = rec[key]
+            if key == "plan" and entries is None:
+                continue
+            if "error" in want:
+                with pytest.raises(SimulationError) as ei:
+                    fn()
+                assert str(ei.value) == want["error"]
+            else:
+                _cmp(fn(), want)
+            checked += 1
+    assert checked >= 1900
+
+
+def test_ex1_engine_known_answers(ex1, rates20k):
+    plan = [PlanEntry(0, "offload", 10_000, 15_000, "SSD", False),
+            PlanEntry(0, "prefetch", 35_000, 40_000, "GPU", True)]
+    r = simulate(ex1, plan, CAP, rates20k)
+    assert r.total_time == 50_000 and r.stall_time_total == 0
+    assert r.channel_utilization == {"ssd.offload": 0.1, "ssd.prefetch": 0.1}
+    assert r.throughput_vs_ideal == 1.0
+    od = simulate_on_demand(ex1, CAP, rates20k)
+    assert od.total_time == 60_000
+    assert od.stall_per_kernel == [0, 0, 5_000, 0, 5_000]
+    assert od.emergency_offloads == 1
+    assert simulate_ideal(ex1) == 50_000
+    assert "total_time_us" in report_json(r)
+    assert timeline_csv(r).splitlines()[0] == "kernel,start_us,stall_us,resident_bytes"
+
+
+def test_unsatisfiable_capacity_raises(ex1, rates20k):
+    with pytest.raises(SimulationError, match="kernel 0 actively uses"):
+        simulate_on_demand(ex1, 90_000_000, rates20k)
+
+
+def test_wrap_plan_folds_to_steady_state():
+    # reference test_planner.py:167-189: weights offloaded after k1, prefetched
+    # in the next iteration (trigger >= iteration folds to trigger - iteration)
+    tr = mk_trace([10_000] * 5, [(0, MB100, "global", [1]), (1, MB100, "intermediate", [3])])
+    plan = [PlanEntry(0, "offload", 20_000, 25_000, "SSD", False),
+            PlanEntry(0, "prefetch", 55_000, 60_000, "GPU", True)]
+    r = simulate(tr, plan, CAP, ChannelRates.symmetric(20_000))
+    assert r.total_time == 50_000 and r.stall_time_total == 0 and r.emergency_offloads == 0
+    assert r.peak_resident_bytes <= CAP
