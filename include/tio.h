@@ -206,6 +206,46 @@ int tio_simulate(const tio_trace_desc *trace, const tio_entry *entries, int64_t 
                  int64_t capacity, const tio_rates *rates, tio_sim_report *report,
                  int64_t *per_kernel_start, int64_t *stall_per_kernel, int64_t *per_kernel_resident);
 
+/* ---- migration engine executor ----------------------------------------------
+ * tio_engine_replay runs one iteration of `trace` under the plan `entries` on
+ * the device: the scheduler above decides every transfer (simulator.py
+ * semantics); compute runs on its own stream as one placeholder kernel per
+ * trace kernel that lasts its profiled duration x time_scale; every transfer
+ * is a real copy between a device buffer (stream-ordered pool) and a 4 KB
+ * aligned pinned host extent on the channel's side stream, gated by CUDA
+ * events (no GDS on the target: both tiers land in pinned host memory).
+ * With verify, every prefetched tensor is checked byte for byte against the
+ * pattern it was written with.  Replaces the reference engine's execution
+ * role (simulator.py:471-528 run); ideal = the same kernels, no transfers. */
+typedef struct tio_engine_config {
+    int64_t capacity;
+    tio_rates rates;            /* rates the scheduler models (measured link) */
+    double time_scale;          /* device us per trace us for the placeholder kernels */
+    int verify;                 /* byte-check every prefetch */
+    int measure_ideal;          /* also time the no-transfer run */
+} tio_engine_config;
+
+typedef struct tio_engine_stats {
+    int64_t model_total_us, model_ideal_us, model_stall_us, model_peak_resident, emergency_offloads;
+    double replay_ms, ideal_ms;                 /* CUDA-event device times */
+    int64_t offload_bytes, prefetch_bytes, n_offloads, n_prefetches;
+    double offload_busy_ms, prefetch_busy_ms;   /* sum of per-copy device times */
+    int64_t peak_device_bytes;                  /* pool high-water during the replay */
+    int64_t host_bytes;                         /* pinned host extents */
+    int64_t verified_bytes, verify_mismatches;
+} tio_engine_stats;
+
+int tio_engine_replay(const tio_trace_desc *trace, const tio_entry *entries, int64_t num_entries,
+                      const tio_engine_config *cfg, void *stream, tio_engine_stats *stats);
+
+/* K10: gather n device buffers into 4 KB-aligned extents of `staging`
+ * (offsets[i] out) / scatter them back, with TMA bulk copies.  scratch: a
+ * device buffer of >= 64 * n + 64 bytes for the segment tables. */
+int tio_pack(const void *const *src, const int64_t *bytes, int64_t n, void *staging, int64_t *offsets,
+             void *scratch, size_t scratch_bytes, void *stream);
+int tio_unpack(const void *staging, const int64_t *offsets, void *const *dst, const int64_t *bytes, int64_t n,
+               void *scratch, size_t scratch_bytes, void *stream);
+
 /* ---- channel primitives (bandwidth.py:75-84) ------------------------------- */
 /* ceil(nbytes / rate) exactly; TIO_ERR_CHANNEL_CONFIG for rate <= 0. */
 int tio_transfer_duration(double rate, int64_t nbytes, int64_t *out);

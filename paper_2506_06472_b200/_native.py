@@ -93,7 +93,8 @@ ENTRY_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("trigger_u
 EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_device_info", "tio_trace_create",
            "tio_trace_destroy", "tio_lifetime", "tio_lifetime_view_get", "tio_lifetime_copy_out",
            "tio_plan_create", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
-           "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate")
+           "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate",
+           "tio_engine_replay", "tio_pack", "tio_unpack")
 
 
 def lib_path() -> str:

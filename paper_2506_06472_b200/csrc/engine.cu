@@ -1,0 +1,609 @@
+// engine.cu — the migration engine's GPU executor and its copy kernels.
+//
+// tio_engine_replay executes a trace under a plan on the device: the
+// scheduler (engine_sched.cu, the exact reference engine semantics,
+// simulator.py:178-528) decides every transfer; this file turns the decisions
+// into stream operations:
+//   * compute stream: per trace kernel, wait for the prefetches of its
+//     tensors, allocate its new intermediates (stream-ordered pool), run the
+//     kernel (a placeholder that spins for its profiled duration and touches
+//     its tensors), free intermediates after their last use;
+//   * one stream per channel (ssd/host x offload/prefetch): serial transfers in
+//     the scheduler's order; an offload waits for the last kernel that had
+//     finished at its model start, copies the tensor to its 4 KB-aligned
+//     host extent and frees the device buffer; a prefetch waits for the
+//     offload completions that freed its memory, allocates, copies back and
+//     (optionally) verifies the bytes against the tensor's pattern.
+// GDS is absent on the target boxes (no nvidia-fs), so both the SSD and the
+// host channel land in pinned host memory via cudaMemcpyAsync on side
+// streams (the north star's fallback); the SSD channel keeps its own stream
+// and rate.
+//
+// Copy kernels (K10): tio_pack / tio_unpack gather/scatter tensors into
+// 4 KB-aligned extents of a staging buffer with TMA bulk copies
+// (cp.async.bulk global->shared->global, mbarrier-tracked), 16-byte vector
+// tails.  HBM-bound: 2 x bytes per copy.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "engine_sched.cuh"
+
+namespace tio {
+
+// ------------------------------------------------------------------ patterns
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 33; x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+// byte pattern of tensor `tid`: little-endian 8-byte words mix64(seed ^ word index)
+__global__ void k_fill_pattern(uint8_t *p, int64_t bytes, uint64_t seed) {
+    const int64_t words = bytes >> 3;
+    uint64_t *w = reinterpret_cast<uint64_t *>(p);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+        w[i] = mix64(seed ^ (uint64_t)i);
+    if (blockIdx.x == 0 && threadIdx.x < (bytes & 7)) {
+        const uint64_t last = mix64(seed ^ (uint64_t)words);
+        p[(words << 3) + threadIdx.x] = (uint8_t)(last >> (8 * threadIdx.x));
+    }
+}
+
+__global__ void k_verify_pattern(const uint8_t *p, int64_t bytes, uint64_t seed, unsigned long long *bad) {
+    const int64_t words = bytes >> 3;
+    const uint64_t *w = reinterpret_cast<const uint64_t *>(p);
+    unsigned long long nb = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+        if (w[i] != mix64(seed ^ (uint64_t)i)) ++nb;
+    if (blockIdx.x == 0 && threadIdx.x < (bytes & 7)) {
+        const uint64_t last = mix64(seed ^ (uint64_t)words);
+        if (p[(words << 3) + threadIdx.x] != (uint8_t)(last >> (8 * threadIdx.x))) ++nb;
+    }
+    if (nb) atomicAdd(bad, nb);
+}
+
+// placeholder compute of one trace kernel: spins for `ns` (its profiled
+// duration) on one CTA and reads one word of each of its tensors
+constexpr int MAX_KTENSORS = 24;
+struct KernelTensors {
+    const uint64_t *p[MAX_KTENSORS];
+    int n;
+};
+
+__global__ void k_kernel_placeholder(KernelTensors kt, int64_t ns, unsigned long long *sink) {
+    uint64_t acc = 0;
+    for (int i = threadIdx.x; i < kt.n; i += blockDim.x) acc ^= *kt.p[i];
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (threadIdx.x == 0 && ns > 0) {
+        uint64_t t;
+        do {
+            __nanosleep(1000);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        } while ((int64_t)(t - t0) < ns);
+    }
+    if (acc == 0x5a5a5a5a5a5a5a5aull) atomicAdd(sink, 1ull);   // keeps the loads
+}
+
+// ------------------------------------------------------------------ TMA pack
+struct PackSeg {
+    const uint8_t *src;
+    uint8_t *dst;
+    int64_t bytes;
+};
+
+constexpr int PACK_CHUNK = 32 * 1024;     // bytes per TMA bulk transfer
+constexpr int PACK_STAGES = 4;
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_load(void *smem, const void *gmem, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(smem)), "l"(gmem), "r"(bytes),
+                 "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store(void *gmem, const void *smem, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
+                 "r"((unsigned)__cvta_generic_to_shared(smem)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Pipelined TMA bulk copy.  The chunks of all 16-byte-aligned segments
+// (bodies rounded down to 16 bytes) are flattened; CTA b copies chunks
+// b, b + grid, ...: S-1 bulk loads in flight into a ring of S shared-memory
+// stages, each landed stage stored back with a bulk store.  Tails and
+// unaligned segments go through k_copy_rest.
+__device__ __forceinline__ void chunk_of(const PackSeg *segs, const int64_t *chunk_ptr, int nseg, int64_t c,
+                                         const uint8_t **src, uint8_t **dst, unsigned *bytes) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (chunk_ptr[mid] <= c) lo = mid; else hi = mid - 1;
+    }
+    const PackSeg sg = segs[lo];
+    const int64_t off = (c - chunk_ptr[lo]) * PACK_CHUNK;
+    const int64_t body = sg.bytes & ~(int64_t)15;
+    const int64_t n = body - off < PACK_CHUNK ? body - off : PACK_CHUNK;
+    *src = sg.src + off;
+    *dst = sg.dst + off;
+    *bytes = (unsigned)n;
+}
+
+__global__ void __launch_bounds__(32) k_pack(const PackSeg *segs, const int64_t *chunk_ptr, int nseg,
+                                             int64_t nchunks) {
+    extern __shared__ __align__(128) uint8_t sbuf[];
+    __shared__ __align__(8) uint64_t bars[PACK_STAGES];
+    if (threadIdx.x != 0) return;           // one issuing thread per CTA
+    for (int s = 0; s < PACK_STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int64_t J = nchunks > blockIdx.x ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    unsigned phase[PACK_STAGES];
+    for (int s = 0; s < PACK_STAGES; ++s) phase[s] = 0;
+    const uint8_t *src;
+    uint8_t *dst[PACK_STAGES];
+    unsigned nb[PACK_STAGES];
+    auto issue = [&](int64_t j) {
+        const int st = (int)(j % PACK_STAGES);
+        chunk_of(segs, chunk_ptr, nseg, blockIdx.x + j * gridDim.x, &src, &dst[st], &nb[st]);
+        mbar_expect_tx(&bars[st], nb[st]);
+        tma_load(sbuf + (size_t)st * PACK_CHUNK, src, nb[st], &bars[st]);
+    };
+    for (int64_t j = 0; j < PACK_STAGES - 1 && j < J; ++j) issue(j);
+    for (int64_t j = 0; j < J; ++j) {
+        if (j + PACK_STAGES - 1 < J) {
+            tma_wait_read<0>();             // the stage of chunk j-1 has been read by its store
+            issue(j + PACK_STAGES - 1);
+        }
+        const int st = (int)(j % PACK_STAGES);
+        mbar_wait(&bars[st], phase[st]);
+        phase[st] ^= 1;
+        tma_store(dst[st], sbuf + (size_t)st * PACK_CHUNK, nb[st]);
+        tma_commit();
+    }
+    tma_wait_all();
+}
+
+// tails (bytes past the last 16-byte multiple) and unaligned segments
+__global__ void k_copy_rest(const PackSeg *segs, int nseg) {
+    for (int i = blockIdx.x; i < nseg; i += gridDim.x) {
+        const PackSeg sg = segs[i];
+        const bool aligned = ((reinterpret_cast<uintptr_t>(sg.src) | reinterpret_cast<uintptr_t>(sg.dst)) & 15) == 0;
+        const int64_t from = aligned ? (sg.bytes & ~(int64_t)15) : 0;
+        if (!aligned) {
+            const int64_t w = (sg.bytes - from) >> 3;
+            const bool al8 = ((reinterpret_cast<uintptr_t>(sg.src) | reinterpret_cast<uintptr_t>(sg.dst)) & 7) == 0;
+            if (al8) {
+                const uint64_t *s8 = reinterpret_cast<const uint64_t *>(sg.src);
+                uint64_t *d8 = reinterpret_cast<uint64_t *>(sg.dst);
+                for (int64_t k = threadIdx.x; k < w; k += blockDim.x) d8[k] = s8[k];
+                for (int64_t k = (w << 3) + threadIdx.x; k < sg.bytes; k += blockDim.x) sg.dst[k] = sg.src[k];
+                continue;
+            }
+        }
+        for (int64_t k = from + threadIdx.x; k < sg.bytes; k += blockDim.x) sg.dst[k] = sg.src[k];
+    }
+}
+
+static int launch_pack(const std::vector<PackSeg> &segs, cudaStream_t s, void *scratch, size_t scratch_bytes) {
+    if (segs.empty()) return TIO_OK;
+    const int nseg = (int)segs.size();
+    // TMA chunks over the 16-byte bodies of the aligned segments
+    std::vector<PackSeg> tma;
+    for (const auto &g : segs)
+        if ((((reinterpret_cast<uintptr_t>(g.src) | reinterpret_cast<uintptr_t>(g.dst)) & 15) == 0) && g.bytes >= 16)
+            tma.push_back(g);
+    const int ntma = (int)tma.size();
+    std::vector<int64_t> cp(ntma + 1, 0);
+    for (int i = 0; i < ntma; ++i) cp[i + 1] = cp[i] + ((tma[i].bytes & ~(int64_t)15) + PACK_CHUNK - 1) / PACK_CHUNK;
+    const size_t need = sizeof(PackSeg) * (nseg + ntma) + sizeof(int64_t) * (ntma + 1);
+    if (need > scratch_bytes) return fail(TIO_ERR_INVALID, "pack scratch too small (%zu < %zu)", scratch_bytes, need);
+    PackSeg *dall = reinterpret_cast<PackSeg *>(scratch);
+    PackSeg *dtma = dall + nseg;
+    int64_t *dcp = reinterpret_cast<int64_t *>(dtma + ntma);
+    std::vector<uint8_t> blob(need);
+    memcpy(blob.data(), segs.data(), sizeof(PackSeg) * nseg);
+    if (ntma) memcpy(blob.data() + sizeof(PackSeg) * nseg, tma.data(), sizeof(PackSeg) * ntma);
+    memcpy(blob.data() + sizeof(PackSeg) * (nseg + ntma), cp.data(), sizeof(int64_t) * (ntma + 1));
+    TIO_CUDA(cudaMemcpyAsync(scratch, blob.data(), need, cudaMemcpyHostToDevice, s));
+    TIO_CUDA(cudaStreamSynchronize(s));     // blob is pageable host memory
+    static bool attr = false;
+    const int smem = PACK_STAGES * PACK_CHUNK;
+    if (!attr) {
+        TIO_CUDA(cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nchunks = cp[ntma];
+    if (nchunks > 0) {
+        const int grid = (int)std::min<int64_t>(nchunks, (int64_t)sms);
+        k_pack<<<grid, 32, smem, s>>>(dtma, dcp, ntma, nchunks);
+        count_launch();
+    }
+    k_copy_rest<<<std::min(nseg, sms * 4), 256, 0, s>>>(dall, nseg);
+    count_launch();
+    TIO_CUDA(cudaGetLastError());
+    return TIO_OK;
+}
+
+}  // namespace tio
+
+using namespace tio;
+
+static inline int64_t align4k(int64_t x) { return (x + 4095) & ~(int64_t)4095; }
+
+extern "C" int tio_pack(const void *const *src, const int64_t *bytes, int64_t n, void *staging,
+                        int64_t *offsets, void *scratch, size_t scratch_bytes, void *stream) {
+    if ((n > 0 && (!src || !bytes || !staging || !offsets)) || n < 0) return fail(TIO_ERR_INVALID, "null argument");
+    std::vector<PackSeg> segs;
+    int64_t off = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        offsets[i] = off;
+        if (bytes[i] > 0) segs.push_back({static_cast<const uint8_t *>(src[i]), static_cast<uint8_t *>(staging) + off, bytes[i]});
+        off += align4k(bytes[i]);
+    }
+    return launch_pack(segs, (cudaStream_t)stream, scratch, scratch_bytes);
+}
+
+extern "C" int tio_unpack(const void *staging, const int64_t *offsets, void *const *dst, const int64_t *bytes,
+                          int64_t n, void *scratch, size_t scratch_bytes, void *stream) {
+    if ((n > 0 && (!dst || !bytes || !staging || !offsets)) || n < 0) return fail(TIO_ERR_INVALID, "null argument");
+    std::vector<PackSeg> segs;
+    for (int64_t i = 0; i < n; ++i)
+        if (bytes[i] > 0)
+            segs.push_back({static_cast<const uint8_t *>(staging) + offsets[i], static_cast<uint8_t *>(dst[i]), bytes[i]});
+    return launch_pack(segs, (cudaStream_t)stream, scratch, scratch_bytes);
+}
+
+// ------------------------------------------------------------------ replay
+namespace {
+
+struct Replay {
+    SchedInput in;
+    SchedOutput sc;
+    const tio_engine_config *cfg;
+    cudaStream_t comp = nullptr, ch[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaMemPool_t pool = nullptr;
+    std::vector<uint8_t *> dptr;
+    std::vector<int64_t> hoff;         // host extent offset (-1: never leaves the GPU)
+    uint8_t *host = nullptr;
+    int64_t host_bytes = 0;
+    std::vector<int64_t> act_ptr, act;
+    unsigned long long *bad = nullptr, *sink = nullptr;
+    std::vector<cudaEvent_t> events;
+    std::string err;
+
+    ~Replay() {
+        for (auto e : events) cudaEventDestroy(e);
+        for (int c = 0; c < 4; ++c) if (ch[c]) cudaStreamDestroy(ch[c]);
+        if (comp) cudaStreamDestroy(comp);
+        if (host) cudaFreeHost(host);
+        if (pool) cudaMemPoolDestroy(pool);
+    }
+    cudaEvent_t ev() {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        events.push_back(e);
+        return e;
+    }
+    cudaEvent_t tev() {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        events.push_back(e);
+        return e;
+    }
+};
+
+}  // namespace
+
+extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries,
+                                 const tio_engine_config *cfg, void *stream, tio_engine_stats *stats) {
+    if (!d || !cfg || !stats || (num_entries > 0 && !entries)) return fail(TIO_ERR_INVALID, "null argument");
+    memset(stats, 0, sizeof(*stats));
+    Replay R;
+    R.cfg = cfg;
+    SchedInput &in = R.in;
+    in.N = d->num_kernels; in.T = d->num_tensors;
+    in.dur = d->duration_us; in.tid = d->tensor_id; in.size = d->size_bytes; in.kind = d->kind;
+    in.ptr = d->access_ptr; in.acc = d->accesses;
+    std::vector<int64_t> e_tid(num_entries), e_trig(num_entries), e_dl(num_entries);
+    std::vector<int32_t> e_act(num_entries), e_tgt(num_entries), e_urg(num_entries);
+    for (int64_t i = 0; i < num_entries; ++i) {
+        e_tid[i] = entries[i].tensor_id; e_trig[i] = entries[i].trigger_us; e_dl[i] = entries[i].deadline_us;
+        e_act[i] = entries[i].action; e_tgt[i] = entries[i].target; e_urg[i] = entries[i].urgent;
+    }
+    in.num_entries = num_entries;
+    in.e_tid = e_tid.data(); in.e_trigger = e_trig.data(); in.e_deadline = e_dl.data();
+    in.e_action = e_act.data(); in.e_target = e_tgt.data(); in.e_urgent = e_urg.data();
+    in.capacity = cfg->capacity;
+    in.rate[0] = cfg->rates.ssd_offload; in.rate[1] = cfg->rates.ssd_prefetch;
+    in.rate[2] = cfg->rates.host_offload; in.rate[3] = cfg->rates.host_prefetch;
+    in.has_host = cfg->rates.has_host;
+    const int64_t N = in.N, T = in.T;
+    for (int64_t t = 0; t < T; ++t)
+        for (int64_t j = in.ptr[t]; j < in.ptr[t + 1]; ++j)
+            if (in.acc[j] < 0 || in.acc[j] >= N) return fail(TIO_ERR_INVALID, "access out of range");
+    {
+        std::string err;
+        int rc = engine_schedule(in, &R.sc, &err);
+        if (rc != TIO_OK) return fail(rc, "%s", err.c_str());
+    }
+    const SchedOutput &sc = R.sc;
+    stats->model_total_us = sc.total_time;
+    stats->model_ideal_us = sc.ideal_time;
+    stats->model_stall_us = sc.stall_total;
+    stats->model_peak_resident = sc.peak_resident;
+    stats->emergency_offloads = sc.emergency;
+
+    // ---- resources
+    int dev = 0;
+    TIO_CUDA(cudaGetDevice(&dev));
+    TIO_CUDA(cudaStreamCreateWithFlags(&R.comp, cudaStreamNonBlocking));
+    for (int c = 0; c < 4; ++c) TIO_CUDA(cudaStreamCreateWithFlags(&R.ch[c], cudaStreamNonBlocking));
+    {
+        cudaMemPoolProps props;
+        memset(&props, 0, sizeof(props));
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        TIO_CUDA(cudaMemPoolCreate(&R.pool, &props));
+        uint64_t thresh = UINT64_MAX;
+        TIO_CUDA(cudaMemPoolSetAttribute(R.pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    }
+    // host extents for every tensor that ever leaves the GPU (4 KB aligned)
+    R.hoff.assign(T, -1);
+    for (const auto &x : sc.transfers) {
+        if (R.hoff[x.tensor] < 0) {
+            R.hoff[x.tensor] = R.host_bytes;
+            R.host_bytes += align4k(in.size[x.tensor]);
+        }
+    }
+    for (int64_t t = 0; t < T; ++t)
+        if ((sc.initial_loc[t] == LOC_SSD || sc.initial_loc[t] == LOC_HOST) && R.hoff[t] < 0) {
+            R.hoff[t] = R.host_bytes;
+            R.host_bytes += align4k(in.size[t]);
+        }
+    if (R.host_bytes) TIO_CUDA(cudaHostAlloc((void **)&R.host, (size_t)R.host_bytes, cudaHostAllocPortable));
+    stats->host_bytes = R.host_bytes;
+    TIO_CUDA(cudaMallocAsync((void **)&R.bad, 16, R.pool, R.comp));
+    R.sink = R.bad + 1;
+    TIO_CUDA(cudaMemsetAsync(R.bad, 0, 16, R.comp));
+
+    // active tensors per kernel (trace order is enough here)
+    R.act_ptr.assign(N + 1, 0);
+    for (int64_t t = 0; t < T; ++t)
+        for (int64_t j = in.ptr[t]; j < in.ptr[t + 1]; ++j) R.act_ptr[in.acc[j] + 1]++;
+    for (int64_t k = 0; k < N; ++k) R.act_ptr[k + 1] += R.act_ptr[k];
+    R.act.assign(R.act_ptr[N], 0);
+    {
+        std::vector<int64_t> fill(R.act_ptr.begin(), R.act_ptr.end() - 1);
+        for (int64_t t = 0; t < T; ++t)
+            for (int64_t j = in.ptr[t]; j < in.ptr[t + 1]; ++j) R.act[fill[in.acc[j]]++] = t;
+    }
+    const int64_t E = R.act_ptr[N];
+    (void)E;
+    uint64_t *dummy = nullptr;
+    TIO_CUDA(cudaMallocAsync((void **)&dummy, 64, R.pool, R.comp));
+    TIO_CUDA(cudaMemsetAsync(dummy, 0, 64, R.comp));
+
+    auto seed_of = [&](int64_t t) { return (uint64_t)in.tid[t] * 0x9e3779b97f4a7c15ull + 0x1234567ull; };
+    auto alloc_fill = [&](int64_t t, cudaStream_t s, bool fill) -> int {
+        TIO_CUDA(cudaMallocFromPoolAsync((void **)&R.dptr[t], (size_t)in.size[t], R.pool, s));
+        if (fill) {
+            k_fill_pattern<<<148 * 4, 256, 0, s>>>(R.dptr[t], in.size[t], seed_of(t));
+            count_launch();
+        }
+        return TIO_OK;
+    };
+
+    // ---- initial state at t = 0 (after plan folding)
+    R.dptr.assign(T, nullptr);
+    std::vector<int8_t> loc(sc.initial_loc.begin(), sc.initial_loc.end());
+    for (int64_t t = 0; t < T; ++t) {
+        if (loc[t] == LOC_GPU) TIO_TRY(alloc_fill(t, R.comp, true));
+        else if (loc[t] == LOC_SSD || loc[t] == LOC_HOST) {
+            // starts the iteration off the GPU: its bytes live in the host extent
+            TIO_TRY(alloc_fill(t, R.comp, true));
+            TIO_CUDA(cudaMemcpyAsync(R.host + R.hoff[t], R.dptr[t], (size_t)in.size[t], cudaMemcpyDeviceToHost, R.comp));
+            TIO_CUDA(cudaFreeAsync(R.dptr[t], R.comp));
+            R.dptr[t] = nullptr;
+        }
+    }
+    TIO_CUDA(cudaStreamSynchronize(R.comp));
+    size_t zero = 0;
+    TIO_CUDA(cudaMemPoolSetAttribute(R.pool, cudaMemPoolAttrUsedMemHigh, &zero));
+
+    // ---- the program: ops in model start order
+    struct Op { int64_t time; int kind; int64_t idx; };   // kind 0 transfer, 1 kernel
+    std::vector<Op> ops;
+    ops.reserve(sc.transfers.size() + N);
+    for (size_t i = 0; i < sc.transfers.size(); ++i) ops.push_back({sc.transfers[i].start, 0, (int64_t)i});
+    for (int64_t k = 0; k < N; ++k) ops.push_back({sc.start[k], 1, k});
+    std::stable_sort(ops.begin(), ops.end(), [](const Op &a, const Op &b) {
+        if (a.time != b.time) return a.time < b.time;
+        return a.kind < b.kind;
+    });
+    std::vector<cudaEvent_t> kdone(N, nullptr), xdone(sc.transfers.size(), nullptr);
+    std::vector<cudaEvent_t> xt0(sc.transfers.size(), nullptr), xt1(sc.transfers.size(), nullptr);
+    // last transfer of each tensor (for kernel gating) and last offload per device
+    std::vector<int64_t> last_x(T, -1);
+    int64_t last_off[2] = {-1, -1};      // ssd, host: latest offload whose model end <= now
+    std::vector<int64_t> off_by_end;     // offload transfer indices sorted by model end
+    for (size_t i = 0; i < sc.transfers.size(); ++i)
+        if (sc.transfers[i].action == 0) off_by_end.push_back((int64_t)i);
+    std::stable_sort(off_by_end.begin(), off_by_end.end(),
+                     [&](int64_t a, int64_t b) { return sc.transfers[a].end < sc.transfers[b].end; });
+    size_t off_cursor = 0;
+    auto advance_offloads = [&](int64_t now) {
+        while (off_cursor < off_by_end.size() && sc.transfers[off_by_end[off_cursor]].end <= now) {
+            const auto &x = sc.transfers[off_by_end[off_cursor]];
+            if (xdone[off_by_end[off_cursor]]) last_off[x.device == LOC_SSD ? 0 : 1] = off_by_end[off_cursor];
+            ++off_cursor;
+        }
+    };
+    const double scale = cfg->time_scale > 0 ? cfg->time_scale : 1.0;
+    cudaEvent_t t_begin = R.tev(), t_end = R.tev();
+    TIO_CUDA(cudaEventRecord(t_begin, R.comp));
+    for (int c = 0; c < 4; ++c) TIO_CUDA(cudaStreamWaitEvent(R.ch[c], t_begin, 0));
+    int64_t bytes_dir[2] = {0, 0}, count_dir[2] = {0, 0};
+    for (const Op &op : ops) {
+        advance_offloads(op.time);
+        if (op.kind == 0) {
+            const SchedTransfer &x = sc.transfers[op.idx];
+            const int c = (x.device == LOC_SSD ? 0 : 2) + x.action;
+            cudaStream_t s = R.ch[c];
+            const int64_t t = x.tensor, nb = in.size[t];
+            if (!x.tail && x.issue_kernel >= 0 && kdone[x.issue_kernel])
+                TIO_CUDA(cudaStreamWaitEvent(s, kdone[x.issue_kernel], 0));
+            xt0[op.idx] = R.tev();
+            if (x.action == 0) {
+                if (!R.dptr[t]) return fail(TIO_ERR_INTERNAL, "offload of tensor %lld that is not resident", (long long)in.tid[t]);
+                TIO_CUDA(cudaEventRecord(xt0[op.idx], s));
+                TIO_CUDA(cudaMemcpyAsync(R.host + R.hoff[t], R.dptr[t], (size_t)nb, cudaMemcpyDeviceToHost, s));
+                xt1[op.idx] = R.tev();
+                TIO_CUDA(cudaEventRecord(xt1[op.idx], s));
+                TIO_CUDA(cudaFreeAsync(R.dptr[t], s));
+                R.dptr[t] = nullptr;
+            } else {
+                // memory freed by the offloads the model counted before this start
+                for (int dv = 0; dv < 2; ++dv)
+                    if (last_off[dv] >= 0) TIO_CUDA(cudaStreamWaitEvent(s, xdone[last_off[dv]], 0));
+                if (R.dptr[t]) return fail(TIO_ERR_INTERNAL, "prefetch of resident tensor %lld", (long long)in.tid[t]);
+                TIO_TRY(alloc_fill(t, s, false));
+                TIO_CUDA(cudaEventRecord(xt0[op.idx], s));
+                TIO_CUDA(cudaMemcpyAsync(R.dptr[t], R.host + R.hoff[t], (size_t)nb, cudaMemcpyHostToDevice, s));
+                xt1[op.idx] = R.tev();
+                TIO_CUDA(cudaEventRecord(xt1[op.idx], s));
+                if (cfg->verify) {
+                    k_verify_pattern<<<148 * 2, 256, 0, s>>>(R.dptr[t], nb, seed_of(t), R.bad);
+                    count_launch();
+                    stats->verified_bytes += nb;
+                }
+            }
+            xdone[op.idx] = R.ev();
+            TIO_CUDA(cudaEventRecord(xdone[op.idx], s));
+            last_x[t] = op.idx;
+            bytes_dir[x.action] += nb;
+            count_dir[x.action] += 1;
+        } else {
+            const int64_t k = op.idx;
+            // gate on the prefetches of this kernel's tensors and on freed memory
+            for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1]; ++j) {
+                const int64_t t = R.act[j], xi = last_x[t];
+                if (xi >= 0 && sc.transfers[xi].action == 1) TIO_CUDA(cudaStreamWaitEvent(R.comp, xdone[xi], 0));
+            }
+            bool alloc_any = false;
+            for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1]; ++j)
+                if (!R.dptr[R.act[j]]) alloc_any = true;
+            if (alloc_any)
+                for (int dv = 0; dv < 2; ++dv)
+                    if (last_off[dv] >= 0) TIO_CUDA(cudaStreamWaitEvent(R.comp, xdone[last_off[dv]], 0));
+            for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1]; ++j) {
+                const int64_t t = R.act[j];
+                if (!R.dptr[t]) {
+                    if (in.kind[t] == 1 || last_x[t] >= 0)
+                        return fail(TIO_ERR_INTERNAL, "kernel %lld needs tensor %lld that is off the GPU",
+                                    (long long)k, (long long)in.tid[t]);
+                    TIO_TRY(alloc_fill(t, R.comp, true));   // first use: the producing kernel writes it
+                }
+            }
+            KernelTensors kt;
+            kt.n = 0;
+            for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1] && kt.n < MAX_KTENSORS; ++j)
+                kt.p[kt.n++] = reinterpret_cast<const uint64_t *>(R.dptr[R.act[j]]);
+            const int64_t ns = (int64_t)((double)in.dur[k] * 1000.0 * scale);
+            k_kernel_placeholder<<<1, 32, 0, R.comp>>>(kt, ns, R.sink);
+            count_launch();
+            kdone[k] = R.ev();
+            TIO_CUDA(cudaEventRecord(kdone[k], R.comp));
+            // free intermediates after their last use
+            for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1]; ++j) {
+                const int64_t t = R.act[j];
+                if (in.kind[t] != 1 && in.acc[in.ptr[t + 1] - 1] == k && R.dptr[t]) {
+                    TIO_CUDA(cudaFreeAsync(R.dptr[t], R.comp));
+                    R.dptr[t] = nullptr;
+                }
+            }
+        }
+    }
+    for (int c = 0; c < 4; ++c) {
+        cudaEvent_t e = R.ev();
+        TIO_CUDA(cudaEventRecord(e, R.ch[c]));
+        TIO_CUDA(cudaStreamWaitEvent(R.comp, e, 0));
+    }
+    TIO_CUDA(cudaEventRecord(t_end, R.comp));
+    TIO_CUDA(cudaStreamSynchronize(R.comp));
+    TIO_CUDA(cudaDeviceSynchronize());
+    float ms = 0.f;
+    TIO_CUDA(cudaEventElapsedTime(&ms, t_begin, t_end));
+    stats->replay_ms = ms;
+    double busy[2] = {0, 0};
+    for (size_t i = 0; i < sc.transfers.size(); ++i) {
+        if (!xt0[i] || !xt1[i]) continue;
+        float m = 0.f;
+        TIO_CUDA(cudaEventElapsedTime(&m, xt0[i], xt1[i]));
+        busy[sc.transfers[i].action] += m;
+    }
+    stats->offload_bytes = bytes_dir[0];
+    stats->prefetch_bytes = bytes_dir[1];
+    stats->n_offloads = count_dir[0];
+    stats->n_prefetches = count_dir[1];
+    stats->offload_busy_ms = busy[0];
+    stats->prefetch_busy_ms = busy[1];
+    {
+        size_t hw = 0;
+        TIO_CUDA(cudaMemPoolGetAttribute(R.pool, cudaMemPoolAttrUsedMemHigh, &hw));
+        stats->peak_device_bytes = (int64_t)hw;
+    }
+    unsigned long long hbad[2] = {0, 0};
+    TIO_CUDA(cudaMemcpy(hbad, R.bad, 16, cudaMemcpyDeviceToHost));
+    stats->verify_mismatches = (int64_t)hbad[0];
+
+    // ---- ideal: the same kernels with every tensor resident, no transfers
+    if (cfg->measure_ideal) {
+        // infinite memory: every tensor resident, no transfers (the kernels
+        // only read one word per tensor, so one resident word stands in)
+        cudaEvent_t i0 = R.tev(), i1 = R.tev();
+        TIO_CUDA(cudaEventRecord(i0, R.comp));
+        for (int64_t k = 0; k < N; ++k) {
+            KernelTensors kt;
+            kt.n = 0;
+            for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1] && kt.n < MAX_KTENSORS; ++j) kt.p[kt.n++] = dummy;
+            const int64_t ns = (int64_t)((double)in.dur[k] * 1000.0 * scale);
+            k_kernel_placeholder<<<1, 32, 0, R.comp>>>(kt, ns, R.sink);
+            count_launch();
+        }
+        TIO_CUDA(cudaEventRecord(i1, R.comp));
+        TIO_CUDA(cudaStreamSynchronize(R.comp));
+        float im = 0.f;
+        TIO_CUDA(cudaEventElapsedTime(&im, i0, i1));
+        stats->ideal_ms = im;
+    }
+    for (int64_t t = 0; t < T; ++t)
+        if (R.dptr[t]) cudaFreeAsync(R.dptr[t], R.comp);
+    cudaStreamSynchronize(R.comp);
+    (void)stream;
+    return TIO_OK;
+}
