@@ -336,7 +336,46 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, rounds, sample_rounds=args.ref_rounds)
+    if not args.no_migration:
+        line["migration"] = migration_bench(args.microbatches)
     print(json.dumps(line), flush=True)
+
+
+def migration_bench(microbatches: int = 4, verify: bool = True, link: dict | None = None) -> dict:
+    """Configs C4 (BASELINE.json): the migration engine executing a
+    Llama-3-8B plan on 1 B200 (Appendix-C trace with `microbatches`
+    microbatches of 8,192 tokens, real tensor sizes, capacity = peak // 2,
+    the plan's channel rates = the measured pinned link, both directions at
+    once).  Device time of the iteration with every transfer executed vs the
+    same kernels with no migration; link GB/s vs the measured link."""
+    from paper_2506_06472_b200 import engine, plan_migrations, ChannelRates
+    from paper_2506_06472_b200 import tracegen as G
+    link = link or engine.measure_link()
+    rate = float(int(link["bidir_gbs_each"] * 1e3))        # bytes/us, integral
+    tr = G.gen_llama_trace(G.LlamaTraceConfig(microbatches=microbatches))
+    cap = G.llama_peak_bytes(tr) // 2
+    rates = ChannelRates.symmetric(rate)
+    t0 = time.perf_counter()
+    plan = plan_migrations(tr, cap, rates)
+    t_plan = time.perf_counter() - t0
+    r = engine.replay(tr, plan, cap, rates, time_scale=1.0, verify=verify)
+    link_each = link["bidir_gbs_each"]
+    return {
+        "workload": f"Llama-3-8B Appendix-C trace, {microbatches} microbatches x 8192 tokens, "
+                    f"E={tr.arrays().num_events}, capacity=peak//2={cap}",
+        "plan": {"entries": len(plan.entries), "warning": plan.warning, "over_capacity_kernels":
+                 len(plan.over_capacity_kernels), "seconds": t_plan},
+        "step_ms": r.replay_ms, "ideal_ms": r.ideal_ms, "step_vs_ideal": r.step_vs_ideal,
+        "model_step_vs_ideal": r.model_total_us / r.model_ideal_us,
+        "offload_gbs": r.offload_gbs, "prefetch_gbs": r.prefetch_gbs,
+        "link": link, "offload_frac_of_link": r.offload_gbs / link_each if link_each else None,
+        "prefetch_frac_of_link": r.prefetch_gbs / link_each if link_each else None,
+        "bytes": {"offload": r.offload_bytes, "prefetch": r.prefetch_bytes, "host_extents": r.host_bytes},
+        "transfers": {"offloads": r.n_offloads, "prefetches": r.n_prefetches, "emergency": r.emergency_offloads},
+        "peak_device_bytes": r.peak_device_bytes, "capacity": cap,
+        "verify": {"bytes": r.verified_bytes, "mismatches": r.verify_mismatches},
+        "tier": "pinned host (no GDS: nvidia-fs absent); plan rates = measured bidirectional pinned link",
+    }
 
 
 def main(argv=None):
@@ -347,6 +386,8 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "llama1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-migration", action="store_true", help="skip the C4 engine replay leg")
+    ap.add_argument("--microbatches", type=int, default=4, help="C4 replay microbatches")
     ap.add_argument("--ref-rounds", type=int, default=40, help="planner rounds in the CPU sample")
     ap.add_argument("--ref-rounds-total", type=int, default=None,
                     help="total rounds of the full plan (for the reference arm's extrapolation)")

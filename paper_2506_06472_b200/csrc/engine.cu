@@ -477,6 +477,9 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
             const int64_t t = x.tensor, nb = in.size[t];
             if (!x.tail && x.issue_kernel >= 0 && kdone[x.issue_kernel])
                 TIO_CUDA(cudaStreamWaitEvent(s, kdone[x.issue_kernel], 0));
+            // transfers of one tensor are ordered (a prefetched tensor can be
+            // evicted again before any kernel touched it)
+            if (last_x[t] >= 0) TIO_CUDA(cudaStreamWaitEvent(s, xdone[last_x[t]], 0));
             xt0[op.idx] = R.tev();
             if (x.action == 0) {
                 if (!R.dptr[t]) return fail(TIO_ERR_INTERNAL, "offload of tensor %lld that is not resident", (long long)in.tid[t]);
