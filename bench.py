@@ -337,11 +337,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, rounds, sample_rounds=args.ref_rounds)
     if not args.no_migration:
-        line["migration"] = migration_bench(args.microbatches)
+        from paper_2506_06472_b200 import engine
+        link = engine.measure_link()
+        line["migration"] = [migration_bench(args.microbatches, link=link, cap_frac=f) for f in (0.5, 0.9)]
     print(json.dumps(line), flush=True)
 
 
-def migration_bench(microbatches: int = 4, verify: bool = True, link: dict | None = None) -> dict:
+def migration_bench(microbatches: int = 8, verify: bool = True, link: dict | None = None,
+                    cap_frac: float = 0.5) -> dict:
     """Configs C4 (BASELINE.json): the migration engine executing a
     Llama-3-8B plan on 1 B200 (Appendix-C trace with `microbatches`
     microbatches of 8,192 tokens, real tensor sizes, capacity = peak // 2,
@@ -353,7 +356,8 @@ def migration_bench(microbatches: int = 4, verify: bool = True, link: dict | Non
     link = link or engine.measure_link()
     rate = float(int(link["bidir_gbs_each"] * 1e3))        # bytes/us, integral
     tr = G.gen_llama_trace(G.LlamaTraceConfig(microbatches=microbatches))
-    cap = G.llama_peak_bytes(tr) // 2
+    peak = G.llama_peak_bytes(tr)
+    cap = peak // 2 if cap_frac == 0.5 else int(peak * cap_frac)
     rates = ChannelRates.symmetric(rate)
     t0 = time.perf_counter()
     plan = plan_migrations(tr, cap, rates)
@@ -362,7 +366,7 @@ def migration_bench(microbatches: int = 4, verify: bool = True, link: dict | Non
     link_each = link["bidir_gbs_each"]
     return {
         "workload": f"Llama-3-8B Appendix-C trace, {microbatches} microbatches x 8192 tokens, "
-                    f"E={tr.arrays().num_events}, capacity=peak//2={cap}",
+                    f"E={tr.arrays().num_events}, peak={peak}, capacity={cap_frac}*peak={cap}",
         "plan": {"entries": len(plan.entries), "warning": plan.warning, "over_capacity_kernels":
                  len(plan.over_capacity_kernels), "seconds": t_plan},
         "step_ms": r.replay_ms, "ideal_ms": r.ideal_ms, "step_vs_ideal": r.step_vs_ideal,

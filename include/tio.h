@@ -206,6 +206,25 @@ int tio_simulate(const tio_trace_desc *trace, const tio_entry *entries, int64_t 
                  int64_t capacity, const tio_rates *rates, tio_sim_report *report,
                  int64_t *per_kernel_start, int64_t *stall_per_kernel, int64_t *per_kernel_resident);
 
+/* The engine program behind a run: every transfer the scheduler starts (in
+ * start order) and every kernel's start time, model microseconds.
+ * initial_loc[t]: 0 unallocated, 1 GPU, 2 SSD, 3 host at t = 0 (after plan
+ * folding).  Call with transfers = NULL to get the count. */
+typedef struct tio_transfer_rec {
+    int64_t tensor_pos, tensor_id;
+    int32_t action;             /* 0 offload, 1 prefetch */
+    int32_t device;             /* TIO_DEST_SSD / TIO_DEST_CPU */
+    int32_t urgent, emergency;
+    int64_t start_us, end_us;
+    int64_t after_kernel;       /* last kernel finished at start_us (-1: none) */
+    int64_t tail;               /* 1: running at t = 0 (boundary-straddling, folded plan) */
+    int64_t seq;                /* position in the engine's processing order (shared with kernel launches) */
+} tio_transfer_rec;
+
+int tio_schedule(const tio_trace_desc *trace, const tio_entry *entries, int64_t num_entries, int64_t capacity,
+                 const tio_rates *rates, tio_transfer_rec *transfers, int64_t transfers_cap,
+                 int64_t *num_transfers, int64_t *kernel_start, int64_t *kernel_seq, int8_t *initial_loc);
+
 /* ---- migration engine executor ----------------------------------------------
  * tio_engine_replay runs one iteration of `trace` under the plan `entries` on
  * the device: the scheduler above decides every transfer (simulator.py

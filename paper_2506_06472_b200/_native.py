@@ -85,6 +85,9 @@ COMMIT_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("start_ke
                          ("pre_end", "<i8"), ("benefit_lo", "<u8"), ("benefit_hi", "<u8"),
                          ("cost", "<i8"), ("rel0_lo", "<i8"), ("rel0_hi", "<i8"),
                          ("rel1_lo", "<i8"), ("rel1_hi", "<i8")])
+TRANSFER_DTYPE = np.dtype([("tensor_pos", "<i8"), ("tensor_id", "<i8"), ("action", "<i4"), ("device", "<i4"),
+                           ("urgent", "<i4"), ("emergency", "<i4"), ("start_us", "<i8"), ("end_us", "<i8"),
+                           ("after_kernel", "<i8"), ("tail", "<i8"), ("seq", "<i8")])
 ENTRY_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("trigger_us", "<i8"),
                         ("deadline_us", "<i8"), ("action", "<i4"), ("target", "<i4"),
                         ("urgent", "<i4"), ("pad", "<i4")])
@@ -94,7 +97,7 @@ EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_devi
            "tio_trace_destroy", "tio_lifetime", "tio_lifetime_view_get", "tio_lifetime_copy_out",
            "tio_plan_create", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
            "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate",
-           "tio_engine_replay", "tio_pack", "tio_unpack")
+           "tio_engine_replay", "tio_pack", "tio_unpack", "tio_schedule")
 
 
 def lib_path() -> str:

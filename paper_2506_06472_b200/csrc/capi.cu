@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -486,6 +487,8 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     a.N = N; a.P = P; a.iteration = I; a.capacity = capacity; a.host_cap = host_cap;
     a.has_host = has_host;
     a.chunk = (int32_t)((N + 1 + G - 1) / G);
+    a.warp_refit_max = 96;
+    if (const char *e = getenv("TIO_WARP_REFIT_MAX")) a.warp_refit_max = atoi(e);
     a.starts = t->starts; a.dur = t->dur; a.resid = resid; a.local_cp = local_cp; a.chunk_sum = chunk_sum;
     a.c_size = c_size; a.c_sk = c_sk; a.c_ek = c_ek; a.c_first = c_first; a.c_last = c_last; a.c_wraps = c_wraps;
     a.c_ready = c_ready; a.c_deadline = c_deadline; a.c_d = c_d;
@@ -715,5 +718,51 @@ extern "C" int tio_simulate(const tio_trace_desc *d, const tio_entry *entries, i
         if (stall_per_kernel) memcpy(stall_per_kernel, out.stall.data(), nb);
         if (per_kernel_resident) memcpy(per_kernel_resident, out.resident.data(), nb);
     }
+    return TIO_OK;
+}
+
+// The engine program: the scheduler's transfers (start order per run) and
+// kernel start times, as the executor consumes them.
+extern "C" int tio_schedule(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries, int64_t capacity,
+                            const tio_rates *rates, tio_transfer_rec *transfers, int64_t transfers_cap,
+                            int64_t *num_transfers, int64_t *kernel_start, int64_t *kernel_seq,
+                            int8_t *initial_loc) {
+    if (!d || !rates || !num_transfers) return fail(TIO_ERR_INVALID, "null argument");
+    SchedInput in;
+    in.N = d->num_kernels; in.T = d->num_tensors;
+    in.dur = d->duration_us; in.tid = d->tensor_id; in.size = d->size_bytes; in.kind = d->kind;
+    in.ptr = d->access_ptr; in.acc = d->accesses;
+    std::vector<int64_t> e_tid(num_entries), e_trig(num_entries), e_dl(num_entries);
+    std::vector<int32_t> e_act(num_entries), e_tgt(num_entries), e_urg(num_entries);
+    for (int64_t i = 0; i < num_entries; ++i) {
+        e_tid[i] = entries[i].tensor_id; e_trig[i] = entries[i].trigger_us; e_dl[i] = entries[i].deadline_us;
+        e_act[i] = entries[i].action; e_tgt[i] = entries[i].target; e_urg[i] = entries[i].urgent;
+    }
+    in.num_entries = num_entries;
+    in.e_tid = e_tid.data(); in.e_trigger = e_trig.data(); in.e_deadline = e_dl.data();
+    in.e_action = e_act.data(); in.e_target = e_tgt.data(); in.e_urgent = e_urg.data();
+    in.capacity = capacity;
+    in.rate[0] = rates->ssd_offload; in.rate[1] = rates->ssd_prefetch;
+    in.rate[2] = rates->host_offload; in.rate[3] = rates->host_prefetch;
+    in.has_host = rates->has_host;
+    SchedOutput out;
+    std::string err;
+    int rc = engine_schedule(in, &out, &err);
+    if (rc != TIO_OK) return fail(rc, "%s", err.c_str());
+    *num_transfers = (int64_t)out.transfers.size();
+    if (transfers) {
+        if (transfers_cap < *num_transfers) return fail(TIO_ERR_INVALID, "transfers buffer too small");
+        for (size_t i = 0; i < out.transfers.size(); ++i) {
+            const SchedTransfer &s = out.transfers[i];
+            tio_transfer_rec &r = transfers[i];
+            r.tensor_pos = s.tensor; r.tensor_id = in.tid[s.tensor]; r.action = s.action;
+            r.device = s.device == LOC_SSD ? TIO_DEST_SSD : TIO_DEST_CPU;
+            r.urgent = s.urgent; r.emergency = s.emergency; r.start_us = s.start; r.end_us = s.end;
+            r.after_kernel = s.issue_kernel; r.tail = s.tail; r.seq = s.seq;
+        }
+    }
+    if (kernel_start && in.N) memcpy(kernel_start, out.start.data(), sizeof(int64_t) * in.N);
+    if (kernel_seq && in.N) memcpy(kernel_seq, out.kseq.data(), sizeof(int64_t) * in.N);
+    if (initial_loc && in.T) memcpy(initial_loc, out.initial_loc.data(), (size_t)in.T);
     return TIO_OK;
 }

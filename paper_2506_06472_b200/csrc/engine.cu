@@ -24,6 +24,7 @@
 // (cp.async.bulk global->shared->global, mbarrier-tracked), 16-byte vector
 // tails.  HBM-bound: 2 x bytes per copy.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -371,6 +372,11 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
         TIO_CUDA(cudaMemPoolCreate(&R.pool, &props));
         uint64_t thresh = UINT64_MAX;
         TIO_CUDA(cudaMemPoolSetAttribute(R.pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+        if (getenv("TIO_POOL_STRICT")) {
+            int off = 0;
+            TIO_CUDA(cudaMemPoolSetAttribute(R.pool, cudaMemPoolReuseAllowOpportunistic, &off));
+            TIO_CUDA(cudaMemPoolSetAttribute(R.pool, cudaMemPoolReuseAllowInternalDependencies, &off));
+        }
     }
     // host extents for every tensor that ever leaves the GPU (4 KB aligned)
     R.hoff.assign(T, -1);
@@ -435,33 +441,30 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
     size_t zero = 0;
     TIO_CUDA(cudaMemPoolSetAttribute(R.pool, cudaMemPoolAttrUsedMemHigh, &zero));
 
-    // ---- the program: ops in model start order
-    struct Op { int64_t time; int kind; int64_t idx; };   // kind 0 transfer, 1 kernel
+    // ---- the program: ops in the model's processing order.  The reference
+    // engine processes a late issue event with its own (earlier) timestamp,
+    // so a transfer can start "at" a time before the kernel launch that
+    // preceded it; the processing order, not the timestamp, is the truth.
+    struct Op { int64_t seq; int kind; int64_t idx; };   // kind 0 transfer, 1 kernel
     std::vector<Op> ops;
     ops.reserve(sc.transfers.size() + N);
-    for (size_t i = 0; i < sc.transfers.size(); ++i) ops.push_back({sc.transfers[i].start, 0, (int64_t)i});
-    for (int64_t k = 0; k < N; ++k) ops.push_back({sc.start[k], 1, k});
-    std::stable_sort(ops.begin(), ops.end(), [](const Op &a, const Op &b) {
-        if (a.time != b.time) return a.time < b.time;
-        return a.kind < b.kind;
-    });
+    for (size_t i = 0; i < sc.transfers.size(); ++i) ops.push_back({sc.transfers[i].seq, 0, (int64_t)i});
+    for (int64_t k = 0; k < N; ++k) ops.push_back({sc.kseq[k], 1, k});
+    std::sort(ops.begin(), ops.end(), [](const Op &a, const Op &b) { return a.seq < b.seq; });
     std::vector<cudaEvent_t> kdone(N, nullptr), xdone(sc.transfers.size(), nullptr);
     std::vector<cudaEvent_t> xt0(sc.transfers.size(), nullptr), xt1(sc.transfers.size(), nullptr);
-    // last transfer of each tensor (for kernel gating) and last offload per device
-    std::vector<int64_t> last_x(T, -1);
-    int64_t last_off[2] = {-1, -1};      // ssd, host: latest offload whose model end <= now
-    std::vector<int64_t> off_by_end;     // offload transfer indices sorted by model end
-    for (size_t i = 0; i < sc.transfers.size(); ++i)
-        if (sc.transfers[i].action == 0) off_by_end.push_back((int64_t)i);
-    std::stable_sort(off_by_end.begin(), off_by_end.end(),
-                     [&](int64_t a, int64_t b) { return sc.transfers[a].end < sc.transfers[b].end; });
-    size_t off_cursor = 0;
-    auto advance_offloads = [&](int64_t now) {
-        while (off_cursor < off_by_end.size() && sc.transfers[off_by_end[off_cursor]].end <= now) {
-            const auto &x = sc.transfers[off_by_end[off_cursor]];
-            if (xdone[off_by_end[off_cursor]]) last_off[x.device == LOC_SSD ? 0 : 1] = off_by_end[off_cursor];
-            ++off_cursor;
+    std::vector<int64_t> last_x(T, -1);      // last transfer of each tensor
+    std::vector<int64_t> last_k(T, -1);      // last launched kernel that accesses each tensor
+    // processed offloads per device (serial channel: ends increase), for memory gating
+    std::vector<std::pair<int64_t, int64_t>> offs_done[2];   // (model end, transfer index)
+    auto latest_off_before = [&](int dv, int64_t t) -> int64_t {
+        const auto &v = offs_done[dv];
+        int64_t lo = 0, hi = (int64_t)v.size();
+        while (lo < hi) {
+            const int64_t m = (lo + hi) >> 1;
+            if (v[m].first <= t) lo = m + 1; else hi = m;
         }
+        return lo > 0 ? v[lo - 1].second : -1;
     };
     const double scale = cfg->time_scale > 0 ? cfg->time_scale : 1.0;
     cudaEvent_t t_begin = R.tev(), t_end = R.tev();
@@ -469,7 +472,6 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
     for (int c = 0; c < 4; ++c) TIO_CUDA(cudaStreamWaitEvent(R.ch[c], t_begin, 0));
     int64_t bytes_dir[2] = {0, 0}, count_dir[2] = {0, 0};
     for (const Op &op : ops) {
-        advance_offloads(op.time);
         if (op.kind == 0) {
             const SchedTransfer &x = sc.transfers[op.idx];
             const int c = (x.device == LOC_SSD ? 0 : 2) + x.action;
@@ -478,8 +480,10 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
             if (!x.tail && x.issue_kernel >= 0 && kdone[x.issue_kernel])
                 TIO_CUDA(cudaStreamWaitEvent(s, kdone[x.issue_kernel], 0));
             // transfers of one tensor are ordered (a prefetched tensor can be
-            // evicted again before any kernel touched it)
+            // evicted again before any kernel touched it), and an offload
+            // waits for every kernel already launched on the tensor
             if (last_x[t] >= 0) TIO_CUDA(cudaStreamWaitEvent(s, xdone[last_x[t]], 0));
+            if (x.action == 0 && last_k[t] >= 0) TIO_CUDA(cudaStreamWaitEvent(s, kdone[last_k[t]], 0));
             xt0[op.idx] = R.tev();
             if (x.action == 0) {
                 if (!R.dptr[t]) return fail(TIO_ERR_INTERNAL, "offload of tensor %lld that is not resident", (long long)in.tid[t]);
@@ -491,8 +495,10 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
                 R.dptr[t] = nullptr;
             } else {
                 // memory freed by the offloads the model counted before this start
-                for (int dv = 0; dv < 2; ++dv)
-                    if (last_off[dv] >= 0) TIO_CUDA(cudaStreamWaitEvent(s, xdone[last_off[dv]], 0));
+                for (int dv = 0; dv < 2; ++dv) {
+                    const int64_t lo = latest_off_before(dv, x.start);
+                    if (lo >= 0) TIO_CUDA(cudaStreamWaitEvent(s, xdone[lo], 0));
+                }
                 if (R.dptr[t]) return fail(TIO_ERR_INTERNAL, "prefetch of resident tensor %lld", (long long)in.tid[t]);
                 TIO_TRY(alloc_fill(t, s, false));
                 TIO_CUDA(cudaEventRecord(xt0[op.idx], s));
@@ -508,6 +514,7 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
             xdone[op.idx] = R.ev();
             TIO_CUDA(cudaEventRecord(xdone[op.idx], s));
             last_x[t] = op.idx;
+            if (x.action == 0) offs_done[x.device == LOC_SSD ? 0 : 1].push_back({x.end, op.idx});
             bytes_dir[x.action] += nb;
             count_dir[x.action] += 1;
         } else {
@@ -521,8 +528,10 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
             for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1]; ++j)
                 if (!R.dptr[R.act[j]]) alloc_any = true;
             if (alloc_any)
-                for (int dv = 0; dv < 2; ++dv)
-                    if (last_off[dv] >= 0) TIO_CUDA(cudaStreamWaitEvent(R.comp, xdone[last_off[dv]], 0));
+                for (int dv = 0; dv < 2; ++dv) {
+                    const int64_t lo = latest_off_before(dv, sc.start[k]);
+                    if (lo >= 0) TIO_CUDA(cudaStreamWaitEvent(R.comp, xdone[lo], 0));
+                }
             for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1]; ++j) {
                 const int64_t t = R.act[j];
                 if (!R.dptr[t]) {
@@ -541,6 +550,7 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
             count_launch();
             kdone[k] = R.ev();
             TIO_CUDA(cudaEventRecord(kdone[k], R.comp));
+            for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1]; ++j) last_k[R.act[j]] = k;
             // free intermediates after their last use
             for (int64_t j = R.act_ptr[k]; j < R.act_ptr[k + 1]; ++j) {
                 const int64_t t = R.act[j];

@@ -66,6 +66,7 @@ struct Engine {
     std::vector<int64_t> tr_sched;              // transfer -> index in out.transfers
     std::priority_queue<Ev, std::vector<Ev>, EvLess> events;
     int64_t seq = 0, resident = 0, peak = 0;
+    int64_t order = 0;                          // processing order of transfer starts and kernel launches
 
     Engine(const SchedInput &i, SchedOutput &o, std::string &e)
         : in(i), out(o), err(e), N(i.N), T(i.T), cap(i.capacity) {}
@@ -108,6 +109,7 @@ struct Engine {
         s.tensor = tr.t; s.action = tr.action; s.device = tr.device;
         s.urgent = tr.urgent; s.emergency = tr.emergency;
         s.start = now; s.end = tr.end; s.issue_kernel = -1; s.tail = tail ? 1 : 0; s.pad = 0;
+        s.seq = order++;
         tr_sched[x] = (int64_t)out.transfers.size();
         out.transfers.push_back(s);
     }
@@ -416,6 +418,7 @@ struct Engine {
         out.start.assign(N, 0);
         out.stall.assign(N, 0);
         out.resident.assign(N, 0);
+        out.kseq.assign(N, 0);
         int64_t now = 0;
         for (int64_t k = 0; k < N; ++k) {
             const int64_t ready = now;
@@ -434,6 +437,7 @@ struct Engine {
             }
             out.stall[k] = now - ready;
             out.start[k] = now;
+            out.kseq[k] = order++;
             for (int64_t j = act_ptr[k]; j < act_ptr[k + 1]; ++j) {
                 const int64_t t = act[j];
                 if (loc[t] == LOC_NONE) { loc[t] = LOC_GPU; grow(in.size[t]); }

@@ -27,6 +27,7 @@ struct SchedTransfer {
     int64_t issue_kernel;  // kernel index whose start the transfer may not precede (-1: before kernel 0)
     int32_t tail;          // 1 = installed running at t=0 (boundary-straddling, plan folding)
     int32_t pad;
+    int64_t seq;           // position in the model's processing order (shared with kernel launches)
 };
 
 struct SchedInput {
@@ -51,6 +52,7 @@ struct SchedOutput {
     int64_t total_time = 0, ideal_time = 0, stall_total = 0, peak_resident = 0, emergency = 0;
     int64_t busy[4] = {0, 0, 0, 0};   // per channel: booked time inside [0, total]
     std::vector<int64_t> start, stall, resident;     // per kernel
+    std::vector<int64_t> kseq;                      // per kernel: launch position in the processing order
     std::vector<SchedTransfer> transfers;           // in start order per channel
     std::vector<int8_t> initial_loc;                // location at t = 0 (after plan folding)
 };

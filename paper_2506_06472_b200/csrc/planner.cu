@@ -321,7 +321,6 @@ __device__ __forceinline__ bool spans_hit(int64_t lo, int64_t hi, const int64_t 
     return false;
 }
 
-constexpr int WARP_REFIT_MAX = 96;   // refits per tile served warp-cooperatively (else per thread)
 
 struct WinInfo {
     int64_t idx, dest, size, cost;
@@ -493,7 +492,7 @@ plan_loop_kernel(PlanArgs a) {
                 if (need) s_refit[atomicAdd(&s_nrefit, 1)] = (int16_t)threadIdx.x;
                 __syncthreads();
                 const int nref = s_nrefit;
-                const bool warp_mode = round > 0 && nref <= WARP_REFIT_MAX;
+                const bool warp_mode = round > 0 && nref <= a.warp_refit_max;
                 if (!warp_mode && nref && threadIdx.x == 0) {
                     atomic_add_i64(&a.scalars[PS_DBG + 11], 1);
                     atomic_add_i64(&a.scalars[PS_DBG + 12], nref);

@@ -107,6 +107,31 @@ def _run(trace: Trace, entries: np.ndarray, capacity: int, rates: ChannelRates) 
         throughput_vs_ideal=1.0 if total == ideal else ideal / total)
 
 
+def schedule(trace: Trace, plan, capacity: int, rates: ChannelRates):
+    """The engine program the GPU executor runs: (transfers as a
+    TRANSFER_DTYPE array in start order, kernel start times, kernel launch
+    positions in the processing order, initial tensor locations)."""
+    lib = _native.load()
+    cols = _native.HostColumns(trace.arrays())
+    desc = cols.desc()
+    ents = entries_array(_entries_of(plan))
+    r = _rates_struct(rates)
+    n = ctypes.c_int64()
+    args = (ctypes.byref(desc), _native._ptr(ents), ctypes.c_int64(ents.shape[0]), ctypes.c_int64(capacity),
+            ctypes.byref(r))
+    rc = lib.tio_schedule(*args, None, ctypes.c_int64(0), ctypes.byref(n), None, None, None)
+    if rc == _native.TIO_ERR_SIMULATION:
+        raise SimulationError(_native.last_error())
+    _native.check(rc)
+    xs = np.zeros(n.value, _native.TRANSFER_DTYPE)
+    starts = np.zeros(cols.dur.shape[0], np.int64)
+    kseq = np.zeros(cols.dur.shape[0], np.int64)
+    loc = np.zeros(cols.tid.shape[0], np.int8)
+    _native.check(lib.tio_schedule(*args, _native._ptr(xs), ctypes.c_int64(n.value), ctypes.byref(n),
+                                   _native._ptr(starts), _native._ptr(kseq), _native._ptr(loc)))
+    return xs, starts, kseq, loc
+
+
 def simulate(trace: Trace, plan, capacity: int, rates: ChannelRates) -> SimReport:
     """Execute the trace under a migration plan (a MigrationPlan, a list of
     entries, or None for no planned transfers) in the engine model."""
