@@ -1,0 +1,90 @@
+"""Multi-process (gloo, world size 2 and 3, CPU) test of the tensor-id
+sharded lifetime stage (paper_2506_06472_b200/distributed.py): the merged
+timeline, active bytes and period list equal the unsharded result.  The
+per-shard compute here is the CPU oracle (the GPU path runs the libtio
+kernel per shard; the host-side sharding, the all_reduce and the all_gather
+merge are what this test covers)."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _oracle_local(sub):
+    from oracle import oracle as O
+    per, tl, act = O.lifetime(sub)
+    return {"timeline": tl, "active": act, "period_tensor": per["tensor"], "period_start": per["start"],
+            "period_end": per["end"], "period_wraps": per["wraps"].astype(np.int8)}
+
+
+def _worker(rank, world, port, cases, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    from paper_2506_06472_b200 import gen_random_trace, LlamaTraceConfig, gen_llama_trace
+    from paper_2506_06472_b200.distributed import sharded_lifetime
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for kind, arg in cases:
+            tr = gen_llama_trace(LlamaTraceConfig(microbatches=arg)) if kind == "llama" else \
+                gen_random_trace(arg, 3 + arg % 50, 1 + arg % 37)
+            r = sharded_lifetime(tr.arrays(), rank, world, local_fn=_oracle_local)
+            out.append({k: (v.tolist() if isinstance(v, np.ndarray) else v) for k, v in r.items()})
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_lifetime_equals_unsharded(world):
+    from oracle import oracle as O
+    from paper_2506_06472_b200 import gen_random_trace, LlamaTraceConfig, gen_llama_trace
+    cases = [("random", s) for s in (1, 7, 42, 99, 123)] + [("llama", 1), ("llama", 2)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for ci, (kind, arg) in enumerate(cases):
+        tr = gen_llama_trace(LlamaTraceConfig(microbatches=arg)) if kind == "llama" else \
+            gen_random_trace(arg, 3 + arg % 50, 1 + arg % 37)
+        per, tl, act = O.lifetime(tr.arrays())
+        for r in range(world):
+            got = results[r][ci]
+            assert got["timeline"] == tl.tolist()
+            assert got["active"] == act.tolist()
+            assert got["period_tensor"] == per["tensor"].tolist()
+            assert got["period_start"] == per["start"].tolist()
+            assert got["period_end"] == per["end"].tolist()
+            assert got["period_wraps"] == per["wraps"].astype(int).tolist()
+
+
+def test_shard_bounds_balanced_and_contiguous():
+    from paper_2506_06472_b200.distributed import shard_bounds
+    ptr = np.cumsum([0] + [3, 1, 4, 1, 5, 9, 2, 6, 5, 3])
+    for world in (1, 2, 3, 4, 8, 16):
+        b = shard_bounds(ptr, world)
+        assert b[0][0] == 0 and b[-1][1] == 10
+        assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
