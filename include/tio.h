@@ -265,6 +265,23 @@ int tio_pack(const void *const *src, const int64_t *bytes, int64_t n, void *stag
 int tio_unpack(const void *staging, const int64_t *offsets, void *const *dst, const int64_t *bytes, int64_t n,
                void *scratch, size_t scratch_bytes, void *stream);
 
+/* ---- trace ingest (trace.py:160-275 parse_trace) ------------------------------
+ * Multi-threaded host parse of a JSONL trace straight into columns.  Fast
+ * format only: TIO_ERR_INVALID with *err_line for anything else (the caller
+ * then uses the reference-exact parser for the error).  Model invariants are
+ * checked by the caller.  threads <= 0: hardware concurrency. */
+typedef struct tio_parsed_trace tio_parsed_trace;
+int tio_trace_parse(const char *buf, size_t len, int threads, tio_parsed_trace **out, int64_t *err_line);
+int tio_parsed_sizes(const tio_parsed_trace *p, int64_t *n_kernels, int64_t *n_tensors, int64_t *n_events,
+                     int64_t *n_names, int64_t *names_bytes, int64_t *meta_bytes);
+/* name table: names[name_off[i] .. name_off[i+1]) raw JSON string contents,
+ * name_esc[i] = contains escapes; meta: raw JSON text of the header's meta. */
+int tio_parsed_copy(const tio_parsed_trace *p, int64_t *k_index, int64_t *k_dur, int32_t *k_code,
+                    int64_t *k_stage, int64_t *k_layer, int64_t *t_id, int64_t *t_size, int8_t *t_kind,
+                    int64_t *t_layer, int64_t *ptr, int64_t *acc, char *names, int64_t *name_off,
+                    uint8_t *name_esc, char *meta);
+int tio_parsed_destroy(tio_parsed_trace *p);
+
 /* ---- channel primitives (bandwidth.py:75-84) ------------------------------- */
 /* ceil(nbytes / rate) exactly; TIO_ERR_CHANNEL_CONFIG for rate <= 0. */
 int tio_transfer_duration(double rate, int64_t nbytes, int64_t *out);

@@ -97,7 +97,8 @@ EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_devi
            "tio_trace_destroy", "tio_lifetime", "tio_lifetime_view_get", "tio_lifetime_copy_out",
            "tio_plan_create", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
            "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate",
-           "tio_engine_replay", "tio_pack", "tio_unpack", "tio_schedule")
+           "tio_engine_replay", "tio_pack", "tio_unpack", "tio_schedule", "tio_trace_parse",
+           "tio_parsed_sizes", "tio_parsed_copy", "tio_parsed_destroy")
 
 
 def lib_path() -> str:

@@ -470,8 +470,78 @@ def _as_text(data) -> str:
     return raw.decode("utf-8") if isinstance(raw, bytes) else raw
 
 
+def _as_bytes(data) -> bytes:
+    if isinstance(data, bytes):
+        return data
+    if isinstance(data, str):
+        return data.encode("utf-8")
+    raw = data.read()
+    return raw if isinstance(raw, bytes) else raw.encode("utf-8")
+
+
+def _fast_parse(raw: bytes):
+    """Multi-threaded C++ parse (libtio csrc/jsonl.cu) into columns; None
+    when the file is not in the writer's fast format (the exact parser then
+    decides, with the reference's error messages)."""
+    import ctypes
+    from . import _native
+    try:
+        lib = _native.load()
+    except Exception:
+        return None
+    h = ctypes.c_void_p()
+    line = ctypes.c_int64()
+    if lib.tio_trace_parse(raw, ctypes.c_size_t(len(raw)), ctypes.c_int(0), ctypes.byref(h),
+                           ctypes.byref(line)) != 0:
+        return None
+    try:
+        n = [ctypes.c_int64() for _ in range(6)]
+        _native.check(lib.tio_parsed_sizes(h, *[ctypes.byref(x) for x in n]))
+        N, T, E, NN, NB, MB = (x.value for x in n)
+        k_index, k_dur, k_stage, k_layer = (np.empty(N, np.int64) for _ in range(4))
+        k_code = np.empty(N, np.int32)
+        t_id, t_size, t_layer = (np.empty(T, np.int64) for _ in range(3))
+        t_kind = np.empty(T, np.int8)
+        ptr = np.empty(T + 1, np.int64)
+        acc = np.empty(E, np.int64)
+        names = ctypes.create_string_buffer(max(1, NB))
+        name_off = np.empty(NN + 1, np.int64)
+        name_esc = np.empty(max(1, NN), np.uint8)
+        meta = ctypes.create_string_buffer(max(1, MB))
+        p = _native._ptr
+        _native.check(lib.tio_parsed_copy(h, p(k_index), p(k_dur), p(k_code), p(k_stage), p(k_layer), p(t_id),
+                                          p(t_size), p(t_kind), p(t_layer), p(ptr), p(acc), names,
+                                          p(name_off), p(name_esc), meta))
+    finally:
+        lib.tio_parsed_destroy(h)
+    table = []
+    for i in range(NN):
+        s = names.raw[name_off[i]:name_off[i + 1]]
+        table.append(json.loads(b'"' + s + b'"') if name_esc[i] else s.decode("utf-8"))
+    arrays = TraceArrays(duration_us=k_dur, kernel_index=k_index, kernel_name_code=k_code, name_table=table,
+                         kernel_stage=k_stage, kernel_layer=k_layer, tensor_id=t_id, size_bytes=t_size,
+                         kind=t_kind, tensor_layer=t_layer, access_ptr=ptr, accesses=acc)
+    return arrays, json.loads(meta.raw[:MB].decode("utf-8"))
+
+
 def parse_trace(data: bytes | str | IO) -> Trace:
-    """Parse + validate a JSONL trace (reference trace.py:217-275)."""
+    """Parse + validate a JSONL trace (reference trace.py:217-275).
+
+    Valid files in the writer's format take the C++ multi-threaded parser
+    (columns directly, no per-record objects); anything else goes through the
+    exact parser below so errors carry the reference's messages and lines."""
+    raw = _as_bytes(data)
+    fast = _fast_parse(raw)
+    if fast is not None:
+        arrays, meta = fast
+        report = validate_arrays(arrays)
+        if not report.ok:
+            raise TraceValidationError(report.violations)
+        return Trace.from_arrays(arrays, meta)
+    return _parse_exact(raw)
+
+
+def _parse_exact(data) -> Trace:
     lines = _as_text(data).splitlines()
     if not lines or not lines[0].strip():
         raise TraceParseError("missing header line", 1)
