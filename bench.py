@@ -319,15 +319,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "planner": {"kernel": "plan_loop_kernel", "bound": "latency (2 grid barriers per round)",
                     "rounds": rounds, "commits": int(info.num_commits),
                     "us_per_round": (loop_ms / K) * 1e3 / max(1, rounds),
-                    "phase_us_per_round_block0": dict(zip(
+                    **({"phase_us_per_round_block0": dict(zip(
                         ["prologue", "evaluate", "block_reduce", "barrier1", "argmax", "channel_merge",
                          "residual", "commit_barrier2"], [round(info.dbg[q] / 1e3 / max(1, rounds), 3)
                                                           for q in range(8)])),
-                    "dirty_tiles_per_round": info.dbg[8] / max(1, rounds),
-                    "refits_per_round": info.dbg[9] / max(1, rounds),
-                    "max_evaluate_us_per_round": info.dbg[10] / 1e3 / max(1, rounds),
-                    "thread_mode_tiles": info.dbg[11], "thread_mode_refits": info.dbg[12],
-                    "max_dirty_tiles_in_a_block_per_round": info.dbg[13] / max(1, rounds),
+                        "dirty_tiles_per_round": info.dbg[8] / max(1, rounds),
+                        "refits_per_round": info.dbg[9] / max(1, rounds),
+                        "max_evaluate_us_per_round": info.dbg[10] / 1e3 / max(1, rounds)}
+                       if any(info.dbg[q] for q in range(14)) else {}),
                     "share_of_step": loop_ms / tot_ms},
         "e2e": {"value": world * E * K / (e2e_ms / 1e3), "unit": "events/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "tio_plan_host (C ABI), pinned host buffers"},

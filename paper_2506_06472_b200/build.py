@@ -41,6 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(LIBDIR, os.path.basename(src).replace(".cu", ".o"))
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-diag-suppress", "177", "-c", src, "-o", obj]
+        if os.environ.get("TIO_PLAN_PROFILE"):
+            cmd.insert(1, "-DTIO_PLAN_PROFILE")      # round-loop phase timers (debug build)
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)

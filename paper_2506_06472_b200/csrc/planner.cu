@@ -398,10 +398,18 @@ plan_loop_kernel(PlanArgs a) {
     }
     grid.sync();
 
+#ifdef TIO_PLAN_PROFILE
+    // phase profile (block 0, %globaltimer): a debug build only, the timer
+    // read is a long-latency operation
     int64_t dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int64_t tprev = gtime();
     const bool tb = (b == 0 && threadIdx.x == 0);
 #define TICK(slot) do { if (tb) { int64_t _t = gtime(); dbg[slot] += _t - tprev; tprev = _t; } } while (0)
+#define PROF(stmt) stmt
+#else
+#define TICK(slot) do { } while (0)
+#define PROF(stmt)
+#endif
     for (int64_t round = 0;; ++round) {
         // ---- round prologue: crit count, last round's flips, chunk prefix
         if (threadIdx.x == 0) {
@@ -434,7 +442,7 @@ plan_loop_kernel(PlanArgs a) {
         __syncthreads();
         if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
         TICK(0);
-        const int64_t te0 = gtime();
+        PROF(const int64_t te0 = gtime());
 
         // ---- phase E: re-evaluate the dirty tiles of this block
         ChanView cv[4];
@@ -469,8 +477,8 @@ plan_loop_kernel(PlanArgs a) {
             __syncthreads();
             const int nd = s_ndirty;
             if (nd) any_dirty = true;
-            if (nd && threadIdx.x == 0) atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 14]), (long long)nd);
-            if (nd && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 8], nd);
+            PROF(if (nd && threadIdx.x == 0) atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 14]), (long long)nd));
+            PROF(if (nd && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 8], nd));
             for (int di = 0; di < nd; ++di) {
                 const int64_t t = s_dirty[di];
                 const int64_t pos = t * TILE + threadIdx.x;
@@ -493,11 +501,11 @@ plan_loop_kernel(PlanArgs a) {
                 __syncthreads();
                 const int nref = s_nrefit;
                 const bool warp_mode = round > 0 && nref <= a.warp_refit_max;
-                if (!warp_mode && nref && threadIdx.x == 0) {
+                PROF(if (!warp_mode && nref && threadIdx.x == 0) {
                     atomic_add_i64(&a.scalars[PS_DBG + 11], 1);
                     atomic_add_i64(&a.scalars[PS_DBG + 12], nref);
-                }
-                if (nref && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 9], nref);
+                })
+                PROF(if (nref && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 9], nref));
                 if (warp_mode) {
                     // one warp per refit: 32-ary searches, 32-wide fit walks
                     for (int k = warp; k < nref; k += nwarps) {
@@ -678,18 +686,17 @@ plan_loop_kernel(PlanArgs a) {
         } else if (round == 0 && threadIdx.x == 0) {
             a.blk_best[b] = none;
         }
-        if (threadIdx.x == 0) {
-            atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 15]), (long long)(gtime() - te0));
-        }
+        PROF(if (threadIdx.x == 0) atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 15]),
+                                             (long long)(gtime() - te0)));
         TICK(2);
         grid.sync();
         TICK(3);
-        if (tb) {
+        PROF(if (tb) {
             a.scalars[PS_DBG + 10] += ld_cg(&a.scalars[PS_DBG + 15]);
             a.scalars[PS_DBG + 15] = 0;
             a.scalars[PS_DBG + 13] += ld_cg(&a.scalars[PS_DBG + 14]);
             a.scalars[PS_DBG + 14] = 0;
-        }
+        })
 
         // ---- phase C: global argmax (redundant per block) and commit
         {
@@ -833,9 +840,9 @@ plan_loop_kernel(PlanArgs a) {
         grid.sync();
         TICK(7);
     }
-    if (tb)
-        for (int q = 0; q < 8; ++q) a.scalars[PS_DBG + q] = dbg[q];
+    PROF(if (tb) for (int q = 0; q < 8; ++q) a.scalars[PS_DBG + q] = dbg[q]);
 #undef TICK
+#undef PROF
 }
 
 int plan_loop_grid(int *blocks) {

@@ -32,7 +32,7 @@ def sass_samples(rep):
 
 def line_map(so, func):
     d = tempfile.mkdtemp()
-    subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=d, capture_output=True)
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=d, capture_output=True)
     cur = None
     out = {}
     for cub in os.listdir(d):
