@@ -44,9 +44,24 @@ struct LastCommit {
     int64_t occ_s, occ_e;         // new host occupancy (CPU commits)
 };
 
+// A channel as the searches see it: the sorted interval arrays in global
+// memory, optionally with a window [w0, w1) of them staged in shared memory
+// (a dirty tile's time span); indices outside the window read global memory.
 struct ChanView {
     const int64_t *s, *e;
     int64_t n;
+    const int64_t *ws = nullptr, *we = nullptr;
+    int64_t w0 = 0, w1 = 0;
+    __device__ __forceinline__ int64_t S(int64_t i) const { return (i >= w0 && i < w1) ? ws[i - w0] : ld_cg(s + i); }
+    __device__ __forceinline__ int64_t E(int64_t i) const { return (i >= w0 && i < w1) ? we[i - w0] : ld_cg(e + i); }
+};
+
+// kernel start times, optionally with a shared-memory window [w0, w1)
+struct StartsView {
+    const int64_t *g;
+    const int64_t *w = nullptr;
+    int64_t w0 = 0, w1 = 0;
+    __device__ __forceinline__ int64_t operator()(int64_t k) const { return (k >= w0 && k < w1) ? w[k - w0] : __ldg(g + k); }
 };
 
 // ---------------------------------------------------------------- searches
@@ -109,12 +124,12 @@ __device__ __forceinline__ int64_t first_true(int64_t lo, int64_t hi, bool cold,
 // stopped: every booking before it ends at or before the fit.
 __device__ int64_t ch_earliest(const ChanView &c, int64_t ready, int64_t d, int64_t lo_idx, int64_t hi_idx,
                                bool cold, int64_t *p) {
-    int64_t i = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return ld_cg(c.e + j) > ready; });
+    int64_t i = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return c.E(j) > ready; });
     int64_t t = ready;
     for (; i < c.n; ++i) {
-        int64_t s = ld_cg(c.s + i);
+        int64_t s = c.S(i);
         if (s >= t + d) break;
-        int64_t e = ld_cg(c.e + i);
+        int64_t e = c.E(i);
         if (e > t) t = e;
     }
     *p = i;
@@ -126,13 +141,13 @@ __device__ int64_t ch_earliest(const ChanView &c, int64_t ready, int64_t d, int6
 __device__ bool ch_latest(const ChanView &c, int64_t deadline, int64_t not_before, int64_t d,
                           int64_t lo_idx, int64_t hi_idx, bool cold, int64_t *out, int64_t *q) {
     int64_t start = deadline - d;
-    const int64_t lo = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return ld_cg(c.s + j) >= deadline; });
+    const int64_t lo = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return c.S(j) >= deadline; });
     int64_t i = lo - 1;
     for (; i >= 0; --i) {
         if (start < not_before) return false;
-        int64_t s = ld_cg(c.s + i);
+        int64_t s = c.S(i);
         if (s >= start + d) continue;
-        int64_t e = ld_cg(c.e + i);
+        int64_t e = c.E(i);
         if (e <= start) break;
         start = s - d;
     }
@@ -194,7 +209,7 @@ __device__ int64_t host_peak(const int64_t *os, const int64_t *oe, const int64_t
 }
 
 // _covered_kernels (planner.py:232-250) as <= 2 kernel ranges
-__device__ void covered_ranges(const int64_t *__restrict__ starts, int64_t N, int64_t iteration,
+__device__ void covered_ranges(const StartsView &starts, int64_t N, int64_t iteration,
                                int wraps, int32_t sk, int32_t ek, int32_t first, int32_t last,
                                int64_t lo_t, int64_t hi_t, int32_t r[4]) {
     r[0] = 1; r[1] = 0; r[2] = 1; r[3] = 0;
@@ -202,13 +217,13 @@ __device__ void covered_ranges(const int64_t *__restrict__ starts, int64_t N, in
         int64_t L = a, H = b + 1;
         while (L < H) {
             int64_t M = (L + H) >> 1;
-            if (__ldg(starts + M) + sh >= lo_t) H = M; else L = M + 1;
+            if (starts(M) + sh >= lo_t) H = M; else L = M + 1;
         }
         int64_t klo = L;
         L = klo; H = b + 1;
         while (L < H) {
             int64_t M = (L + H) >> 1;
-            if (__ldg(starts + M + 1) + sh <= hi_t) L = M + 1; else H = M;
+            if (starts(M + 1) + sh <= hi_t) L = M + 1; else H = M;
         }
         olo = (int32_t)klo;
         ohi = (int32_t)(L - 1);
@@ -224,14 +239,14 @@ __device__ void covered_ranges(const int64_t *__restrict__ starts, int64_t N, in
 // Refit version: the new window [lo_t, hi_t] lies inside the old one, so each
 // new range lies inside the old range r_old (planner.py:232-250 restated);
 // gallop inward from the old endpoints.
-__device__ void covered_ranges_shrunk(const int64_t *__restrict__ starts, int64_t iteration, int wraps,
+__device__ void covered_ranges_shrunk(const StartsView &starts, int64_t iteration, int wraps,
                                       int64_t lo_t, int64_t hi_t, const int32_t r_old[4], int32_t r[4]) {
     for (int q = 0; q < 4; q += 2) {
         const int64_t a = r_old[q], bnd = r_old[q + 1];
         if (a > bnd) { r[q] = r_old[q]; r[q + 1] = r_old[q + 1]; continue; }
         const int64_t sh = (wraps && q == 2) ? iteration : 0;
-        const int64_t klo = gallop_up(a, bnd + 1, [&](int64_t k) { return __ldg(starts + k) + sh >= lo_t; });
-        const int64_t kend = gallop_down(klo, bnd + 1, [&](int64_t k) { return __ldg(starts + k + 1) + sh > hi_t; });
+        const int64_t klo = gallop_up(a, bnd + 1, [&](int64_t k) { return starts(k) + sh >= lo_t; });
+        const int64_t kend = gallop_down(klo, bnd + 1, [&](int64_t k) { return starts(k + 1) + sh > hi_t; });
         r[q] = (int32_t)klo;
         r[q + 1] = (int32_t)(kend - 1);
     }
@@ -329,6 +344,10 @@ struct WinInfo {
     uint64_t blo, bhi;
 };
 
+constexpr int WIN_CH = 1024;     // channel intervals staged per channel
+constexpr int WIN_ST = 2048;     // kernel start times staged
+constexpr size_t PLAN_DYN_SMEM = sizeof(int64_t) * (4 * WIN_CH + WIN_ST);
+
 __global__ void __launch_bounds__(PLAN_THREADS)
 plan_loop_kernel(PlanArgs a) {
     cg::grid_group grid = cg::this_grid();
@@ -346,6 +365,11 @@ plan_loop_kernel(PlanArgs a) {
     __shared__ int32_t s_dirty[PLAN_THREADS];
     __shared__ int32_t s_ndirty;
     __shared__ int16_t s_refit[PLAN_THREADS];
+    __shared__ int64_t s_wnd[6];
+    extern __shared__ __align__(16) int64_t dyn[];          // channel + start-time windows
+    int64_t *s_chs[2] = {dyn, dyn + 2 * WIN_CH};
+    int64_t *s_che[2] = {dyn + WIN_CH, dyn + 3 * WIN_CH};
+    int64_t *s_st = dyn + 4 * WIN_CH;
     __shared__ int32_t s_nrefit;
 
     const int64_t N = a.N, I = a.iteration, cap = a.capacity;
@@ -554,6 +578,40 @@ plan_loop_kernel(PlanArgs a) {
                     __syncthreads();
                     if (need) st = ld_cg(&a.st[c]);
                 }
+                // stage the tile's channel window and kernel start times in shared
+                // memory: the refits' searches then walk shared memory, with
+                // global reads only past the window
+                ChanView wv[2] = {cv[0], cv[1]};
+                StartsView sv{a.starts};
+                if (nref > 0 && !warp_mode) {
+                    const int64_t lo_t = __ldg(&a.t_lo[t]), hi_t = __ldg(&a.t_hi[t]);
+                    if (warp < 2) {
+                        const ChanView &c = cv[warp];
+                        const int64_t w0 = warp_lower_bound(0, c.n, [&](int64_t j) { return ld_cg(c.e + j) > lo_t; });
+                        int64_t w1 = warp_lower_bound(w0, c.n, [&](int64_t j) { return ld_cg(c.s + j) >= hi_t; });
+                        if (w1 - w0 > WIN_CH) w1 = w0 + WIN_CH;
+                        if (lane == 0) { s_wnd[2 * warp] = w0; s_wnd[2 * warp + 1] = w1; }
+                    } else if (warp == 2 && lane == 0) {
+                        int64_t k0 = __ldg(&a.t_ka_lo[t]), k1 = (int64_t)__ldg(&a.t_ka_hi[t]) + 2;   // starts[k0 .. khi+1]
+                        if (k0 > k1 - 2) { k0 = 0; k1 = 0; }
+                        if (k1 > N + 1) k1 = N + 1;
+                        if (k1 - k0 > WIN_ST) k1 = k0 + WIN_ST;
+                        s_wnd[4] = k0; s_wnd[5] = k1;
+                    }
+                    __syncthreads();
+                    for (int q = 0; q < 2; ++q) {
+                        const int64_t w0 = s_wnd[2 * q], w1 = s_wnd[2 * q + 1];
+                        for (int64_t i = w0 + threadIdx.x; i < w1; i += blockDim.x) {
+                            s_chs[q][i - w0] = ld_cg(cv[q].s + i);
+                            s_che[q][i - w0] = ld_cg(cv[q].e + i);
+                        }
+                        wv[q].ws = s_chs[q]; wv[q].we = s_che[q]; wv[q].w0 = w0; wv[q].w1 = w1;
+                    }
+                    for (int64_t k = s_wnd[4] + threadIdx.x; k < s_wnd[5]; k += blockDim.x)
+                        s_st[k - s_wnd[4]] = __ldg(a.starts + k);
+                    sv.w = s_st; sv.w0 = s_wnd[4]; sv.w1 = s_wnd[5];
+                    __syncthreads();
+                }
                 // pass 2: per-candidate evaluation
                 Key mine = none;
                 if (!(st & ST_GONE)) {
@@ -572,14 +630,14 @@ plan_loop_kernel(PlanArgs a) {
                             hp = ld_cg(&a.hidx[2 * c]); hq = ld_cg(&a.hidx[2 * c + 1]); hn = ld_cg(&a.hver[c]);
                         }
                         int64_t os, ps, np, nq;
-                        if (fit_pair(cv[0], cv[1], d0, d1, I, h_off, h_pre, &os, &ps, hp, hq, hn, &np, &nq)) {
+                        if (fit_pair(wv[0], wv[1], d0, d1, I, h_off, h_pre, &os, &ps, hp, hq, hn, &np, &nq)) {
                             int32_t r[4];
                             if (hinted) {
                                 int32_t ro[4];
                                 for (int q = 0; q < 4; ++q) ro[q] = ld_cg(&a.rng[4 * c + q]);
-                                covered_ranges_shrunk(a.starts, I, __ldg(&a.c_wraps[c]), os + d0, ps, ro, r);
+                                covered_ranges_shrunk(sv, I, __ldg(&a.c_wraps[c]), os + d0, ps, ro, r);
                             } else {
-                                covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                                covered_ranges(sv, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
                                                __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
                                                os + d0, ps, r);
                             }
@@ -639,7 +697,7 @@ plan_loop_kernel(PlanArgs a) {
                         if (moved) {
                             const int64_t os = ld_cg(&a.place[4 * c + q0]);
                             const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
-                            covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                            covered_ranges(sv, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
                                            __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
                                            os + doff, ps, r);
                             for (int q = 0; q < 4; ++q) a.rng[4 * c + q] = r[q];
@@ -851,7 +909,8 @@ int plan_loop_grid(int *blocks) {
         int dev = 0, sms = 0, per_sm = 0;
         TIO_CUDA(cudaGetDevice(&dev));
         TIO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        TIO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_loop_kernel, PLAN_THREADS, 0));
+        TIO_CUDA(cudaFuncSetAttribute(plan_loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DYN_SMEM));
+        TIO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_loop_kernel, PLAN_THREADS, PLAN_DYN_SMEM));
         if (per_sm < 1) return fail(TIO_ERR_CUDA, "planner kernel cannot be resident");
         cached = sms * (per_sm < 2 ? per_sm : 2);
         if (cached > MAXG) cached = MAXG;
@@ -863,7 +922,7 @@ int plan_loop_grid(int *blocks) {
 int launch_plan_loop(const PlanArgs &args, int blocks, cudaStream_t stream) {
     void *params[] = {const_cast<PlanArgs *>(&args)};
     TIO_CUDA(cudaLaunchCooperativeKernel((const void *)plan_loop_kernel, dim3(blocks), dim3(PLAN_THREADS),
-                                         params, 0, stream));
+                                         params, PLAN_DYN_SMEM, stream));
     count_launch();
     return TIO_OK;
 }
