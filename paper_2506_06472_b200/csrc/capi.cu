@@ -231,11 +231,11 @@ int tio_lifetime(tio_trace *t, void *stream) {
         TIO_TRY(t->arena.alloc(&t->p_end, t->E));
         TIO_TRY(t->arena.alloc(&t->p_wraps, t->E));
         TIO_TRY(t->arena.alloc(&t->tpp, t->T + 1));
-        TIO_TRY(t->arena.alloc(&t->blk, 3 * (int64_t)t->lgrid));
+        TIO_TRY(t->arena.alloc(&t->blk, lifetime_tiles(t->E) + 2 * (int64_t)t->lgrid));
+        TIO_CUDA(cudaMemsetAsync(t->diff, 0, 8 * (t->N + 1), s));   // the kernel re-zeroes it behind its scan
         TIO_TRY(t->arena.alloc(&t->scalars, SC_COUNT));
     }
     TIO_CUDA(cudaMemsetAsync(t->active, 0, 8 * (t->N > 0 ? t->N : 1), s));
-    TIO_CUDA(cudaMemsetAsync(t->diff, 0, 8 * (t->N + 1), s));
     TIO_CUDA(cudaMemsetAsync(t->scalars, 0, 8 * SC_COUNT, s));
     if (t->T == 0) TIO_CUDA(cudaMemsetAsync(t->tpp, 0, 8, s));
     LifetimeArgs a;
@@ -244,7 +244,8 @@ int tio_lifetime(tio_trace *t, void *stream) {
     a.starts = t->starts; a.timeline = t->timeline; a.active = t->active; a.diff = t->diff;
     a.p_tensor = t->p_tensor; a.p_start = t->p_start; a.p_end = t->p_end; a.p_wraps = t->p_wraps;
     a.tensor_pptr = t->tpp;
-    a.blk_periods = t->blk; a.blk_dur = t->blk + t->lgrid; a.blk_diff = t->blk + 2 * t->lgrid;
+    const int64_t ntiles = lifetime_tiles(t->E);
+    a.blk_periods = t->blk; a.blk_dur = t->blk + ntiles; a.blk_diff = t->blk + ntiles + t->lgrid;
     a.scalars = t->scalars;
     if (t->N == 0) {
         // no kernels: every trace with tensors is invalid (accesses out of range)
@@ -431,17 +432,26 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
         k_build_candidates<<<grid_for(P), 256, 0, s>>>(cb); ::tio::count_launch();
         PCUDA(cudaGetLastError());
     }
-    // ---- tiles: candidates in ready-time order (planner.cu)
+    // ---- tiles: candidates in ready-time order (planner.cu).  The planner's
+    // candidate columns are stored in tile order (position p) so a tile's
+    // data is contiguous; tcand[p] = candidate index (the tie-break key),
+    // cpos[c] = its position.
     const int64_t ntiles = (P + TILE - 1) / TILE;
     uint32_t *tcand;
-    int32_t *ctile, *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;
+    int32_t *cpos, *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;
     int64_t *t_lo, *t_hi;
     Key *tile_best;
-    PTRY(A.alloc(&ctile, P));
+    PTRY(A.alloc(&cpos, P));
     PTRY(A.alloc(&t_lo, ntiles)); PTRY(A.alloc(&t_hi, ntiles));
     PTRY(A.alloc(&t_ka_lo, ntiles)); PTRY(A.alloc(&t_ka_hi, ntiles));
     PTRY(A.alloc(&t_kb_lo, ntiles)); PTRY(A.alloc(&t_kb_hi, ntiles));
     PTRY(A.alloc(&tile_best, ntiles));
+    CandCols src{c_size, c_ready, c_deadline, c_d, c_tid, c_sk, c_ek, c_first, c_last, c_tpos, c_wraps, st};
+    CandCols dst;
+    PTRY(A.alloc(&dst.size, P)); PTRY(A.alloc(&dst.ready, P)); PTRY(A.alloc(&dst.deadline, P));
+    PTRY(A.alloc(&dst.d, 4 * P)); PTRY(A.alloc(&dst.tid, P));
+    PTRY(A.alloc(&dst.sk, P)); PTRY(A.alloc(&dst.ek, P)); PTRY(A.alloc(&dst.first, P)); PTRY(A.alloc(&dst.last, P));
+    PTRY(A.alloc(&dst.tpos, P)); PTRY(A.alloc(&dst.wraps, P)); PTRY(A.alloc(&dst.st, P));
     {
         uint64_t *k0, *k1;
         uint32_t *v0, *v1, *hist;
@@ -454,13 +464,17 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
         }
         tcand = in_tmp ? v1 : v0;
         if (P > 0) {
-            k_tile_spans<<<grid_for(ntiles * 32), 256, 0, s>>>(tcand, P, ntiles, TILE, N, c_ready, c_deadline,
-                                                              c_wraps, c_sk, c_ek, c_first, c_last, ctile, t_lo,
+            k_permute_candidates<<<grid_for(P), 256, 0, s>>>(tcand, P, src, dst, cpos); ::tio::count_launch();
+            k_tile_spans<<<grid_for(ntiles * 32), 256, 0, s>>>(nullptr, P, ntiles, TILE, N, dst.ready, dst.deadline,
+                                                              dst.wraps, dst.sk, dst.ek, dst.first, dst.last, nullptr, t_lo,
                                                               t_hi, t_ka_lo, t_ka_hi, t_kb_lo, t_kb_hi); ::tio::count_launch();
         }
         PCUDA(cudaGetLastError());
     }
-    a.ntiles = ntiles; a.tcand = tcand; a.ctile = ctile; a.t_lo = t_lo; a.t_hi = t_hi;
+    c_size = dst.size; c_ready = dst.ready; c_deadline = dst.deadline; c_d = dst.d; c_tid = dst.tid;
+    c_sk = dst.sk; c_ek = dst.ek; c_first = dst.first; c_last = dst.last; c_tpos = dst.tpos;
+    c_wraps = dst.wraps; st = dst.st;
+    a.ntiles = ntiles; a.tcand = tcand; a.cpos = cpos; a.t_lo = t_lo; a.t_hi = t_hi;
     a.t_ka_lo = t_ka_lo; a.t_ka_hi = t_ka_hi; a.t_kb_lo = t_kb_lo; a.t_kb_hi = t_kb_hi; a.tile_best = tile_best;
     int G = 0;
     PTRY(plan_loop_grid(&G));
@@ -483,6 +497,14 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     PTRY(A.alloc(&occ_s, has_host ? P : 1)); PTRY(A.alloc(&occ_e, has_host ? P : 1)); PTRY(A.alloc(&occ_z, has_host ? P : 1));
     Key *blk_best;
     PTRY(A.alloc(&blk_best, G));
+    int64_t *prof;
+    PTRY(A.alloc(&prof, 8 * (int64_t)G));
+    PCUDA(cudaMemsetAsync(prof, 0, 64 * (size_t)G, s));
+    a.prof = prof;
+    unsigned *bar;
+    PTRY(A.alloc(&bar, 2));
+    PCUDA(cudaMemsetAsync(bar, 0, 8, s));
+    a.bar = bar;
     PTRY(A.alloc(&p->commits, P));
     a.N = N; a.P = P; a.iteration = I; a.capacity = capacity; a.host_cap = host_cap;
     a.has_host = has_host;
@@ -530,6 +552,20 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     pi.num_entries = 2 * nc;
     pi.rounds = hs[PS_ROUNDS];
     for (int q = 0; q < 14; ++q) pi.dbg[q] = hs[PS_DBG + q];
+    if (getenv("TIO_PLAN_PROFILE_DUMP")) {
+        std::vector<int64_t> hp(8 * (size_t)G);
+        cudaMemcpy(hp.data(), prof, 64 * (size_t)G, cudaMemcpyDeviceToHost);
+        int64_t tot[7] = {0, 0, 0, 0, 0, 0, 0};
+        for (int bb = 0; bb < G; ++bb)
+            for (int q = 0; q < 7; ++q) tot[q] += hp[8 * bb + q];
+        fprintf(stderr, "fit walks: %lld steps total, longest %lld\n", (long long)hs[PS_DBG + 11],
+                (long long)hs[PS_DBG + 12]);
+        fprintf(stderr, "slow phase-E rounds (>15us): %lld block-rounds; mean us: dirty %.2f pass1 %.2f window %.2f "
+                "pass2 %.2f tile-reduce %.2f block-reduce %.2f\n", (long long)tot[6],
+                tot[0] / 1e3 / (tot[6] ? tot[6] : 1), tot[1] / 1e3 / (tot[6] ? tot[6] : 1),
+                tot[2] / 1e3 / (tot[6] ? tot[6] : 1), tot[3] / 1e3 / (tot[6] ? tot[6] : 1),
+                tot[4] / 1e3 / (tot[6] ? tot[6] : 1), tot[5] / 1e3 / (tot[6] ? tot[6] : 1));
+    }
 
     // ---- epilogue: over list, peak, planned host, sorted + urgent entries
     p->resid = resid;

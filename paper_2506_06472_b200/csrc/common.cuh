@@ -41,6 +41,35 @@ __device__ __forceinline__ uint64_t ld_cg(const uint64_t *p) { return __ldcg(rei
 __device__ __forceinline__ int8_t ld_cg(const int8_t *p) { return (int8_t)__ldcg(reinterpret_cast<const signed char *>(p)); }
 __device__ __forceinline__ uint8_t ld_cg(const uint8_t *p) { return (uint8_t)__ldcg(reinterpret_cast<const unsigned char *>(p)); }
 
+// Grid-wide barrier for a co-resident (cooperatively launched) grid: one
+// arrival counter and a generation word.  Waiters poll the generation with
+// __nanosleep backoff instead of a tight loop, so a grid of blocks parked at
+// the barrier does not flood the L2 slice that holds the flag while the last
+// blocks are still working.  Release/acquire via __threadfence (gpu scope,
+// which also invalidates L1).  bar[0] = count, bar[1] = generation; zeroed
+// before the launch.
+__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            unsigned ns = 32;
+            while (*gen == g) {
+                __nanosleep(ns);
+                if (ns < 256) ns <<= 1;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ void atomic_add_i64(int64_t *p, int64_t v) {
     atomicAdd(reinterpret_cast<unsigned long long *>(p), (unsigned long long)v);
 }

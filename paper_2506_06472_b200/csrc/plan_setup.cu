@@ -119,8 +119,8 @@ __global__ void k_tile_spans(const uint32_t *tcand, int64_t P, int64_t ntiles, i
         long long lo = LLONG_MAX, hi = LLONG_MIN;
         int alo = INT_MAX, ahi = INT_MIN, blo = INT_MAX, bhi = INT_MIN;
         for (int64_t p = t * tile + lane; p < (t + 1) * tile && p < P; p += 32) {
-            const uint32_t c = tcand[p];
-            ctile[c] = (int32_t)t;
+            const int64_t c = tcand ? (int64_t)tcand[p] : p;      // arrays in tile order: identity
+            if (ctile) ctile[c] = (int32_t)t;
             lo = min(lo, (long long)ready[c]);
             hi = max(hi, (long long)deadline[c]);
             int a0, a1, b0 = 1, b1 = 0;
@@ -142,6 +142,20 @@ __global__ void k_tile_spans(const uint32_t *tcand, int64_t P, int64_t ntiles, i
             ka_lo[t] = alo <= ahi ? alo : 1; ka_hi[t] = alo <= ahi ? ahi : 0;
             kb_lo[t] = blo <= bhi ? blo : 1; kb_hi[t] = blo <= bhi ? bhi : 0;
         }
+    }
+}
+
+// candidate columns from planner order (index c) into tile order (position p)
+__global__ void k_permute_candidates(const uint32_t *tcand, int64_t P, CandCols src, CandCols dst, int32_t *cpos) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = tcand[p];
+        dst.size[p] = src.size[c]; dst.ready[p] = src.ready[c]; dst.deadline[p] = src.deadline[c];
+        for (int q = 0; q < 4; ++q) dst.d[4 * p + q] = src.d[4 * c + q];
+        dst.tid[p] = src.tid[c];
+        dst.sk[p] = src.sk[c]; dst.ek[p] = src.ek[c]; dst.first[p] = src.first[c]; dst.last[p] = src.last[c];
+        dst.tpos[p] = src.tpos[c];
+        dst.wraps[p] = src.wraps[c]; dst.st[p] = src.st[c];
+        cpos[c] = (int32_t)p;
     }
 }
 

@@ -37,6 +37,12 @@ __global__ void k_id_keys(const int64_t *tid, int64_t T, uint64_t *keys, uint32_
 __global__ void k_rank(const uint64_t *skeys, const uint32_t *order, int64_t T, const int64_t *tpp,
                        int32_t *rank, int64_t *cnt_by_rank, int64_t *flags);
 __global__ void k_build_candidates(CandBuild a);
+struct CandCols {
+    int64_t *size, *ready, *deadline, *d, *tid;
+    int32_t *sk, *ek, *first, *last, *tpos;
+    int8_t *wraps, *st;
+};
+__global__ void k_permute_candidates(const uint32_t *tcand, int64_t P, CandCols src, CandCols dst, int32_t *cpos);
 __global__ void k_ready_keys(const int64_t *ready, int64_t P, uint64_t *keys, uint32_t *vals);
 __global__ void k_tile_spans(const uint32_t *tcand, int64_t P, int64_t ntiles, int tile, int64_t N,
                              const int64_t *ready, const int64_t *deadline, const int8_t *wraps,

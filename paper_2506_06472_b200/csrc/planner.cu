@@ -122,16 +122,25 @@ __device__ __forceinline__ int64_t first_true(int64_t lo, int64_t hi, bool cold,
 // (end > ready) lies in [lo_idx, hi_idx] (0..n for a cold search; a window
 // from the candidate's last fit for a refit).  *p = index where the walk
 // stopped: every booking before it ends at or before the fit.
+#ifdef TIO_PLAN_PROFILE
+__device__ unsigned long long g_walk_total, g_walk_max;
+#define WALK_COUNT(n) do { atomicAdd(&g_walk_total, (unsigned long long)(n)); atomicMax(&g_walk_max, (unsigned long long)(n)); } while (0)
+#else
+#define WALK_COUNT(n) do { } while (0)
+#endif
+
 __device__ int64_t ch_earliest(const ChanView &c, int64_t ready, int64_t d, int64_t lo_idx, int64_t hi_idx,
                                bool cold, int64_t *p) {
     int64_t i = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return c.E(j) > ready; });
     int64_t t = ready;
+    const int64_t i0 = i;
     for (; i < c.n; ++i) {
         int64_t s = c.S(i);
         if (s >= t + d) break;
         int64_t e = c.E(i);
         if (e > t) t = e;
     }
+    WALK_COUNT(i - i0);
     *p = i;
     return t;
 }
@@ -144,13 +153,14 @@ __device__ bool ch_latest(const ChanView &c, int64_t deadline, int64_t not_befor
     const int64_t lo = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return c.S(j) >= deadline; });
     int64_t i = lo - 1;
     for (; i >= 0; --i) {
-        if (start < not_before) return false;
+        if (start < not_before) { WALK_COUNT(lo - 1 - i); return false; }
         int64_t s = c.S(i);
         if (s >= start + d) continue;
         int64_t e = c.E(i);
         if (e <= start) break;
         start = s - d;
     }
+    WALK_COUNT(lo - 1 - i);
     if (start < not_before) return false;
     *out = start;
     *q = i + 1;
@@ -350,7 +360,6 @@ constexpr size_t PLAN_DYN_SMEM = sizeof(int64_t) * (4 * WIN_CH + WIN_ST);
 
 __global__ void __launch_bounds__(PLAN_THREADS)
 plan_loop_kernel(PlanArgs a) {
-    cg::grid_group grid = cg::this_grid();
     __shared__ int64_t cp_prefix[MAXG + 1];
     __shared__ Key sm_key[33];
     __shared__ WinInfo s_win;
@@ -418,9 +427,12 @@ plan_loop_kernel(PlanArgs a) {
             for (int q = 0; q < 4; ++q) { ch_n[q] = 0; ch_par[q] = 0; }
             if (b == 0)
                 for (int q = 0; q < 3; ++q) { flip[3 * q] = 0; flip[3 * q + 1] = INT64_MAX; flip[3 * q + 2] = -1; }
+#ifdef TIO_PLAN_PROFILE
+            if (b == 0) { g_walk_total = 0; g_walk_max = 0; }
+#endif
         }
     }
-    grid.sync();
+    grid_barrier(a.bar);
 
 #ifdef TIO_PLAN_PROFILE
     // phase profile (block 0, %globaltimer): a debug build only, the timer
@@ -430,9 +442,16 @@ plan_loop_kernel(PlanArgs a) {
     const bool tb = (b == 0 && threadIdx.x == 0);
 #define TICK(slot) do { if (tb) { int64_t _t = gtime(); dbg[slot] += _t - tprev; tprev = _t; } } while (0)
 #define PROF(stmt) stmt
+    // per-block phase-E split (thread 0 of every block): dirty test, pass 1,
+    // window staging, pass 2, tile reduce, block reduce
+    int64_t sub[6] = {0, 0, 0, 0, 0, 0};      // this round
+    int64_t slow[7] = {0, 0, 0, 0, 0, 0, 0};  // summed over rounds whose phase E took > 15 us; [6] = count
+    int64_t tsub = 0;
+#define SUB(slot) do { if (threadIdx.x == 0) { int64_t _t = gtime(); sub[slot] += _t - tsub; tsub = _t; } } while (0)
 #else
 #define TICK(slot) do { } while (0)
 #define PROF(stmt)
+#define SUB(slot) do { } while (0)
 #endif
     for (int64_t round = 0;; ++round) {
         // ---- round prologue: crit count, last round's flips, chunk prefix
@@ -467,6 +486,7 @@ plan_loop_kernel(PlanArgs a) {
         if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
         TICK(0);
         PROF(const int64_t te0 = gtime());
+        PROF(if (threadIdx.x == 0) { tsub = te0; for (int q = 0; q < 6; ++q) sub[q] = 0; });
 
         // ---- phase E: re-evaluate the dirty tiles of this block
         ChanView cv[4];
@@ -503,10 +523,12 @@ plan_loop_kernel(PlanArgs a) {
             if (nd) any_dirty = true;
             PROF(if (nd && threadIdx.x == 0) atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 14]), (long long)nd));
             PROF(if (nd && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 8], nd));
+            SUB(0);
             for (int di = 0; di < nd; ++di) {
                 const int64_t t = s_dirty[di];
                 const int64_t pos = t * TILE + threadIdx.x;
-                const int32_t c = pos < a.P ? (int32_t)__ldg(&a.tcand[pos]) : -1;
+                const int64_t c = pos < a.P ? pos : -1;                 // column position
+                const int32_t cid = pos < a.P ? (int32_t)__ldg(&a.tcand[pos]) : -1;   // tie-break index
                 int8_t st = c >= 0 ? ld_cg(&a.st[c]) : ST_GONE;
                 // pass 1: which candidates need an SSD re-search (planner.py:147-176)
                 bool need = false;
@@ -525,15 +547,12 @@ plan_loop_kernel(PlanArgs a) {
                 __syncthreads();
                 const int nref = s_nrefit;
                 const bool warp_mode = round > 0 && nref <= a.warp_refit_max;
-                PROF(if (!warp_mode && nref && threadIdx.x == 0) {
-                    atomic_add_i64(&a.scalars[PS_DBG + 11], 1);
-                    atomic_add_i64(&a.scalars[PS_DBG + 12], nref);
-                })
+
                 PROF(if (nref && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 9], nref));
                 if (warp_mode) {
                     // one warp per refit: 32-ary searches, 32-wide fit walks
                     for (int k = warp; k < nref; k += nwarps) {
-                        const int32_t cc = (int32_t)__ldg(&a.tcand[t * TILE + s_refit[k]]);
+                        const int64_t cc = t * TILE + s_refit[k];
                         const int8_t sc = ld_cg(&a.st[cc]);
                         const int64_t d0 = __ldg(&a.c_d[4 * cc]), d1 = __ldg(&a.c_d[4 * cc + 1]);
                         int64_t h_off = __ldg(&a.c_ready[cc]), h_pre = __ldg(&a.c_deadline[cc]);
@@ -578,6 +597,7 @@ plan_loop_kernel(PlanArgs a) {
                     __syncthreads();
                     if (need) st = ld_cg(&a.st[c]);
                 }
+                SUB(1);
                 // stage the tile's channel window and kernel start times in shared
                 // memory: the refits' searches then walk shared memory, with
                 // global reads only past the window
@@ -612,6 +632,7 @@ plan_loop_kernel(PlanArgs a) {
                     sv.w = s_st; sv.w0 = s_wnd[4]; sv.w1 = s_wnd[5];
                     __syncthreads();
                 }
+                SUB(2);
                 // pass 2: per-candidate evaluation
                 Key mine = none;
                 if (!(st & ST_GONE)) {
@@ -721,16 +742,19 @@ plan_loop_kernel(PlanArgs a) {
                             mine.blo = (uint64_t)bf;
                             mine.bhi = (uint64_t)(bf >> 64);
                             mine.cost = doff + dpre;
-                            mine.meta = 4 * (int64_t)c + dest;
+                            mine.meta = 4 * (int64_t)cid + dest;
                         }
                     }
                     if (nst != st) a.st[c] = nst;
                 }
+                SUB(3);
                 const Key tk = block_best(mine, sm_key);
                 if (threadIdx.x == 0) a.tile_best[t] = tk;
+                SUB(4);
             }
             __syncthreads();
         }
+        SUB(0);
         TICK(1);
         // block best over this block's tiles (unchanged when no tile was dirty)
         if (any_dirty) {
@@ -744,10 +768,15 @@ plan_loop_kernel(PlanArgs a) {
         } else if (round == 0 && threadIdx.x == 0) {
             a.blk_best[b] = none;
         }
+        SUB(5);
+        PROF(if (threadIdx.x == 0 && gtime() - te0 > 15000) {
+            for (int q = 0; q < 6; ++q) slow[q] += sub[q];
+            slow[6] += 1;
+        });
         PROF(if (threadIdx.x == 0) atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 15]),
                                              (long long)(gtime() - te0)));
         TICK(2);
-        grid.sync();
+        grid_barrier(a.bar);
         TICK(3);
         PROF(if (tb) {
             a.scalars[PS_DBG + 10] += ld_cg(&a.scalars[PS_DBG + 15]);
@@ -760,14 +789,15 @@ plan_loop_kernel(PlanArgs a) {
         {
             Key w = none;
             for (int j = threadIdx.x; j < G; j += blockDim.x) {
-                const Key o = a.blk_best[j];
+                const uint64_t *q = reinterpret_cast<const uint64_t *>(&a.blk_best[j]);
+                const Key o{ld_cg(q), ld_cg(q + 1), (int64_t)ld_cg(q + 2), (int64_t)ld_cg(q + 3)};
                 if (kbetter(o, w)) w = o;
             }
             w = block_best(w, sm_key);
             if (threadIdx.x == 0) {
                 WinInfo wi;
                 wi.blo = w.blo; wi.bhi = w.bhi; wi.cost = w.cost;
-                wi.idx = w.meta >> 2;
+                wi.idx = (w.blo | w.bhi) != 0 ? __ldg(&a.cpos[w.meta >> 2]) : 0;   // column position
                 wi.dest = w.meta & 3;
                 if ((w.blo | w.bhi) != 0) {
                     const int64_t c = wi.idx;
@@ -893,14 +923,17 @@ plan_loop_kernel(PlanArgs a) {
             if (w.dest == TIO_DEST_CPU) s_nocc += 1;
             ch_n[q0] += nb; ch_n[q0 + 1] += nb;
             ch_par[q0] ^= 1; ch_par[q0 + 1] ^= 1;
-            s_win_tile = __ldg(&a.ctile[w.idx]);
+            s_win_tile = w.idx / TILE;
         }
-        grid.sync();
+        grid_barrier(a.bar);
         TICK(7);
     }
     PROF(if (tb) for (int q = 0; q < 8; ++q) a.scalars[PS_DBG + q] = dbg[q]);
+    PROF(if (tb) { a.scalars[PS_DBG + 11] = (int64_t)g_walk_total; a.scalars[PS_DBG + 12] = (int64_t)g_walk_max; });
+    PROF(if (threadIdx.x == 0 && a.prof) for (int q = 0; q < 7; ++q) a.prof[8 * b + q] = slow[q]);
 #undef TICK
 #undef PROF
+#undef SUB
 }
 
 int plan_loop_grid(int *blocks) {

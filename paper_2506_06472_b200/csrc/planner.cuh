@@ -40,7 +40,7 @@ struct PlanArgs {
     int64_t *resid;                // [N]
     int64_t *local_cp;             // [N+1] prefix of dur*[resid>cap] within each chunk
     int64_t *chunk_sum;            // [grid]
-    // candidates (immutable, planner order)
+    // candidates (immutable), all per-candidate columns in tile order (position)
     const int64_t *c_size;
     const int32_t *c_sk, *c_ek, *c_first, *c_last;
     const int8_t *c_wraps;
@@ -54,8 +54,8 @@ struct PlanArgs {
     int32_t *hver;                 // [P]  SSD channel size at the last fit
     // tiles: candidates in ready-time order, TILE per tile
     int64_t ntiles;
-    const uint32_t *tcand;         // [P] candidate at tile position
-    const int32_t *ctile;          // [P] tile of a candidate
+    const uint32_t *tcand;         // [P] candidate index (planner order) at tile position
+    const int32_t *cpos;           // [P] tile position of a candidate index
     const int64_t *t_lo, *t_hi;    // [ntiles] span [min ready, max deadline)
     const int32_t *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;  // [ntiles] kernel hulls (lo > hi: empty)
     Key *tile_best;                // [ntiles]
@@ -67,6 +67,8 @@ struct PlanArgs {
     int64_t *occ_s, *occ_e, *occ_size;
     // reduction + outputs
     Key *blk_best;                 // [grid]
+    int64_t *prof;                 // [grid * 8] phase-E split per block (debug build)
+    unsigned *bar;                 // [2] grid barrier (count, generation), zeroed
     tio_commit *commits;           // [P]
     int64_t *scalars;              // [PS_COUNT]
     const int64_t *c_tid;          // [P] tensor id per candidate (for commit records)
