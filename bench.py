@@ -335,7 +335,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, rounds, sample_rounds=args.ref_rounds)
-    if not args.no_migration:
+    if not args.no_migration and world == 1:
+        # C4 on one GPU; at N > 1 the per-rank pinned host extents (24-78 GB
+        # each) would exceed the box's host memory, so the leg runs at N = 1 only
         from paper_2506_06472_b200 import engine
         link = engine.measure_link()
         line["migration"] = [migration_bench(args.microbatches, link=link, cap_frac=f) for f in (0.5, 0.9)]

@@ -172,6 +172,17 @@ int tio_lifetime_copy_out(tio_trace *t, void *stream, int64_t *starts, int64_t *
  * a non-positive rate. */
 int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap,
                     void *stream, tio_plan **out, tio_plan_info *info);
+/* Options of tio_plan_create2: max_rounds > 0 stops the greedy loop after
+ * that many commits (the plan is then the reference's first max_rounds
+ * commits; used to check a prefix of huge plans against the oracle);
+ * warp_refit_max: refits per tile served warp-cooperatively (-1: default). */
+typedef struct tio_plan_opts {
+    int64_t max_rounds;
+    int32_t warp_refit_max;
+    int32_t pad;
+} tio_plan_opts;
+int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap,
+                     const tio_plan_opts *opts, void *stream, tio_plan **out, tio_plan_info *info);
 int tio_plan_info_get(tio_plan *p, tio_plan_info *out);
 /* Host copies: commits[num_commits], entries[num_entries], residual[N],
  * over[num_over]; any may be NULL. */

@@ -74,6 +74,10 @@ class PlanInfo(ctypes.Structure):
         ("dbg", _i64 * 14)]
 
 
+class PlanOpts(ctypes.Structure):
+    _fields_ = [("max_rounds", _i64), ("warp_refit_max", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
 class SimReportC(ctypes.Structure):
     _fields_ = [(n, _i64) for n in ("total_time", "ideal_time", "stall_time_total", "peak_resident_bytes",
                                     "emergency_offloads")] + [("channel_busy", _i64 * 4), ("num_transfers", _i64)]
@@ -95,7 +99,7 @@ ENTRY_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("trigger_u
 # every exported symbol of include/tio.h
 EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_device_info", "tio_trace_create",
            "tio_trace_destroy", "tio_lifetime", "tio_lifetime_view_get", "tio_lifetime_copy_out",
-           "tio_plan_create", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
+           "tio_plan_create", "tio_plan_create2", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
            "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate",
            "tio_engine_replay", "tio_pack", "tio_unpack", "tio_schedule", "tio_trace_parse",
            "tio_parsed_sizes", "tio_parsed_copy", "tio_parsed_destroy")
@@ -226,11 +230,12 @@ class DeviceTrace:
         out["iteration"] = v.iteration_us
         return out
 
-    def plan(self, capacity: int, rates: Rates, host_cap: int) -> "DevicePlan":
+    def plan(self, capacity: int, rates: Rates, host_cap: int, max_rounds: int = 0) -> "DevicePlan":
         info = PlanInfo()
         h = ctypes.c_void_p()
-        rc = self._lib.tio_plan_create(self.handle, _i64(capacity), ctypes.byref(rates), _i64(host_cap),
-                                       self.stream, ctypes.byref(h), ctypes.byref(info))
+        opts = PlanOpts(max_rounds, -1, 0)
+        rc = self._lib.tio_plan_create2(self.handle, _i64(capacity), ctypes.byref(rates), _i64(host_cap),
+                                        ctypes.byref(opts), self.stream, ctypes.byref(h), ctypes.byref(info))
         if rc != TIO_OK:
             err = TioError(rc, last_error())
             err.info = info

@@ -327,6 +327,11 @@ static unsigned grid_for(int64_t n, int threads = 256) {
 
 int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap, void *stream,
                     tio_plan **out, tio_plan_info *info) {
+    return tio_plan_create2(t, capacity, rates, host_cap, nullptr, stream, out, info);
+}
+
+int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap,
+                     const tio_plan_opts *opts, void *stream, tio_plan **out, tio_plan_info *info) {
     if (!t || !rates || !out) return fail(TIO_ERR_INVALID, "null argument");
     *out = nullptr;
     cudaStream_t s = (cudaStream_t)stream;
@@ -511,6 +516,8 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
     a.chunk = (int32_t)((N + 1 + G - 1) / G);
     a.warp_refit_max = 0;     // per-thread refits measured faster on C2 (tools/planner_sweep.sh)
     if (const char *e = getenv("TIO_WARP_REFIT_MAX")) a.warp_refit_max = atoi(e);
+    if (opts && opts->warp_refit_max >= 0) a.warp_refit_max = opts->warp_refit_max;
+    a.max_rounds = opts ? opts->max_rounds : 0;
     a.starts = t->starts; a.dur = t->dur; a.resid = resid; a.local_cp = local_cp; a.chunk_sum = chunk_sum;
     a.c_size = c_size; a.c_sk = c_sk; a.c_ek = c_ek; a.c_first = c_first; a.c_last = c_last; a.c_wraps = c_wraps;
     a.c_ready = c_ready; a.c_deadline = c_deadline; a.c_d = c_d;

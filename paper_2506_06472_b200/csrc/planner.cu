@@ -52,6 +52,10 @@ struct ChanView {
     int64_t n;
     const int64_t *ws = nullptr, *we = nullptr;
     int64_t w0 = 0, w1 = 0;
+    // search bounds valid for every placement inside the staged tile span
+    // [t_lo, t_hi): the first booking ending after t_lo .. the first starting
+    // at or after t_hi (a fit's searched index lies between them)
+    int64_t lb = 0, ub = INT64_MAX;
     __device__ __forceinline__ int64_t S(int64_t i) const { return (i >= w0 && i < w1) ? ws[i - w0] : ld_cg(s + i); }
     __device__ __forceinline__ int64_t E(int64_t i) const { return (i >= w0 && i < w1) ? we[i - w0] : ld_cg(e + i); }
 };
@@ -131,7 +135,10 @@ __device__ unsigned long long g_walk_total, g_walk_max;
 
 __device__ int64_t ch_earliest(const ChanView &c, int64_t ready, int64_t d, int64_t lo_idx, int64_t hi_idx,
                                bool cold, int64_t *p) {
-    int64_t i = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return c.E(j) > ready; });
+    if (lo_idx < c.lb) lo_idx = c.lb;
+    if (hi_idx > c.ub) hi_idx = c.ub;
+    if (hi_idx < lo_idx) hi_idx = lo_idx;
+    int64_t i = first_true(lo_idx, hi_idx, cold && hi_idx - lo_idx > 64, [&](int64_t j) { return c.E(j) > ready; });
     int64_t t = ready;
     const int64_t i0 = i;
     for (; i < c.n; ++i) {
@@ -150,7 +157,10 @@ __device__ int64_t ch_earliest(const ChanView &c, int64_t ready, int64_t d, int6
 __device__ bool ch_latest(const ChanView &c, int64_t deadline, int64_t not_before, int64_t d,
                           int64_t lo_idx, int64_t hi_idx, bool cold, int64_t *out, int64_t *q) {
     int64_t start = deadline - d;
-    const int64_t lo = first_true(lo_idx, hi_idx, cold, [&](int64_t j) { return c.S(j) >= deadline; });
+    if (lo_idx < c.lb) lo_idx = c.lb;
+    if (hi_idx > c.ub) hi_idx = c.ub;
+    if (hi_idx < lo_idx) hi_idx = lo_idx;
+    const int64_t lo = first_true(lo_idx, hi_idx, cold && hi_idx - lo_idx > 64, [&](int64_t j) { return c.S(j) >= deadline; });
     int64_t i = lo - 1;
     for (; i >= 0; --i) {
         if (start < not_before) { WALK_COUNT(lo - 1 - i); return false; }
@@ -375,6 +385,7 @@ plan_loop_kernel(PlanArgs a) {
     __shared__ int32_t s_ndirty;
     __shared__ int16_t s_refit[PLAN_THREADS];
     __shared__ int64_t s_wnd[6];
+    __shared__ int64_t s_wub[2];
     extern __shared__ __align__(16) int64_t dyn[];          // channel + start-time windows
     int64_t *s_chs[2] = {dyn, dyn + 2 * WIN_CH};
     int64_t *s_che[2] = {dyn + WIN_CH, dyn + 3 * WIN_CH};
@@ -484,6 +495,7 @@ plan_loop_kernel(PlanArgs a) {
         }
         __syncthreads();
         if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
+        if (a.max_rounds > 0 && round >= a.max_rounds) break;
         TICK(0);
         PROF(const int64_t te0 = gtime());
         PROF(if (threadIdx.x == 0) { tsub = te0; for (int q = 0; q < 6; ++q) sub[q] = 0; });
@@ -608,9 +620,9 @@ plan_loop_kernel(PlanArgs a) {
                     if (warp < 2) {
                         const ChanView &c = cv[warp];
                         const int64_t w0 = warp_lower_bound(0, c.n, [&](int64_t j) { return ld_cg(c.e + j) > lo_t; });
-                        int64_t w1 = warp_lower_bound(w0, c.n, [&](int64_t j) { return ld_cg(c.s + j) >= hi_t; });
-                        if (w1 - w0 > WIN_CH) w1 = w0 + WIN_CH;
-                        if (lane == 0) { s_wnd[2 * warp] = w0; s_wnd[2 * warp + 1] = w1; }
+                        const int64_t wub = warp_lower_bound(w0, c.n, [&](int64_t j) { return ld_cg(c.s + j) >= hi_t; });
+                        const int64_t w1 = wub - w0 > WIN_CH ? w0 + WIN_CH : wub;
+                        if (lane == 0) { s_wnd[2 * warp] = w0; s_wnd[2 * warp + 1] = w1; s_wub[warp] = wub; }
                     } else if (warp == 2 && lane == 0) {
                         int64_t k0 = __ldg(&a.t_ka_lo[t]), k1 = (int64_t)__ldg(&a.t_ka_hi[t]) + 2;   // starts[k0 .. khi+1]
                         if (k0 > k1 - 2) { k0 = 0; k1 = 0; }
@@ -626,6 +638,7 @@ plan_loop_kernel(PlanArgs a) {
                             s_che[q][i - w0] = ld_cg(cv[q].e + i);
                         }
                         wv[q].ws = s_chs[q]; wv[q].we = s_che[q]; wv[q].w0 = w0; wv[q].w1 = w1;
+                        wv[q].lb = w0; wv[q].ub = s_wub[q];
                     }
                     for (int64_t k = s_wnd[4] + threadIdx.x; k < s_wnd[5]; k += blockDim.x)
                         s_st[k - s_wnd[4]] = __ldg(a.starts + k);

@@ -264,12 +264,13 @@ def _raise_for(err: _native.TioError, capacity: int, rates: ChannelRates) -> Non
     raise err
 
 
-def plan_device(trace: Trace, capacity: int, rates: ChannelRates, host_cap: int = 0) -> dict:
+def plan_device(trace: Trace, capacity: int, rates: ChannelRates, host_cap: int = 0, max_rounds: int = 0) -> dict:
     """Run the device planner; return its raw columns (commits, entries,
-    residual, over) plus the info struct — no per-entry Python objects."""
+    residual, over) plus the info struct — no per-entry Python objects.
+    max_rounds > 0 stops after that many commits (a prefix of the plan)."""
     dt = _device_trace(trace)
     try:
-        p = dt.plan(capacity, _rates_struct(rates), host_cap)
+        p = dt.plan(capacity, _rates_struct(rates), host_cap, max_rounds)
     except _native.TioError as err:
         _raise_for(err, capacity, rates)
     try:

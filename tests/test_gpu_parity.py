@@ -249,3 +249,26 @@ def test_native_library_is_the_code_that_ran():
     assert "sm_100a" in info
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert _native.lib_path() in maps
+
+
+def test_c3_lifetime_and_plan_prefix_vs_oracle():
+    """Config C3 (Llama-3-70B shape, E=9,935,960): lifetime bit-exact against
+    the oracle; the planner's first 24 commits (max_rounds) against the
+    oracle's first 24 — a prefix of the same greedy sequence."""
+    from paper_2506_06472_b200 import LLAMA3_70B, gen_llama_trace
+    from paper_2506_06472_b200.tracegen import llama_peak_bytes
+    tr = gen_llama_trace(LLAMA3_70B)
+    a = tr.arrays()
+    assert a.num_events == 9_935_960
+    per, tl, act = O.lifetime(a)
+    la = lifetime_arrays(tr)
+    assert np.array_equal(la.timeline, tl) and np.array_equal(la.active, act)
+    assert np.array_equal(la.period_tensor, per["tensor"]) and np.array_equal(la.period_start, per["start"])
+    assert np.array_equal(la.period_end, per["end"])
+    cap = llama_peak_bytes(tr) // 2
+    R = 24
+    o = O.plan(a, cap, 16000.0, 16000.0, lifetime_out=(per, tl, act), max_rounds=R)
+    g = plan_device(tr, cap, ChannelRates.symmetric(16_000), 0, max_rounds=R)
+    assert int(g["info"].num_commits) == len(o["committed"]) == R
+    assert g["plan_bytes"] == o["plan_bytes"]
+    assert np.array_equal(g["residual"], o["residual"])
