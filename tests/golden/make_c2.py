@@ -1,10 +1,12 @@
-"""Fingerprint of the C2 plan computed by the CPU oracle (slow: tens of
-minutes on 8 cores; run once in the build container).
+"""Fingerprints of the C2 / C3 plans computed by the CPU oracle (slow: tens
+of minutes on 8 cores each; run once in the build container).
+
+    python tests/golden/make_c2.py [c2|c3]
 
 The reference planner cannot run at C2 (~8 h per round), so the
-C2 checker is the oracle (oracle/tio_oracle.c), whose bit-exactness against
+C2/C3 checker is the oracle (oracle/tio_oracle.c), whose bit-exactness against
 the reference is pinned by tests/test_oracle_golden.py on the fuzz corpora,
-C1 and the 1-microbatch Llama trace.  Output: tests/golden/c2.json.gz.
+C1 and the 1-microbatch Llama trace.  Output: tests/golden/<config>.json.gz.
 """
 
 from __future__ import annotations
@@ -21,11 +23,11 @@ ROOT = os.path.abspath(os.path.join(HERE, "..", ".."))
 sys.path.insert(0, ROOT)
 
 
-def main():
+def main(config: str = "c2"):
     from oracle import oracle as O
-    from paper_2506_06472_b200 import LLAMA3_8B, gen_llama_trace, write_trace
+    from paper_2506_06472_b200 import LLAMA3_8B, LLAMA3_70B, gen_llama_trace, write_trace
     from paper_2506_06472_b200.tracegen import llama_peak_bytes
-    tr = gen_llama_trace(LLAMA3_8B)
+    tr = gen_llama_trace({"c2": LLAMA3_8B, "c3": LLAMA3_70B}[config])
     a = tr.arrays()
     cap = llama_peak_bytes(tr) // 2
     t0 = time.time()
@@ -39,10 +41,10 @@ def main():
         "over_capacity_kernels": len(p["over_capacity_kernels"]),
         "oracle_seconds": round(time.time() - t0, 1), "oracle_threads": int(O.lib().tio_oracle_threads()),
     }
-    with gzip.open(os.path.join(HERE, "c2.json.gz"), "wt") as f:
+    with gzip.open(os.path.join(HERE, f"{config}.json.gz"), "wt") as f:
         json.dump(rec, f)
     print(rec)
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1] if len(sys.argv) > 1 else "c2")

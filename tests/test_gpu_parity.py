@@ -251,6 +251,23 @@ def test_native_library_is_the_code_that_ran():
     assert _native.lib_path() in maps
 
 
+def test_c3_full_plan_bit_exact_vs_oracle():
+    """Config C3 (Llama-3-70B shape, E=9,935,960), the north star's 10M-event
+    trace: the whole plan (1,347 commits) against the oracle's fingerprint
+    (tests/golden/c3.json.gz, tests/golden/make_c2.py c3: 493 s on 8 cores)."""
+    from paper_2506_06472_b200 import LLAMA3_70B, gen_llama_trace
+    from paper_2506_06472_b200.tracegen import llama_peak_bytes
+    rec = load_golden("c3")
+    tr = gen_llama_trace(LLAMA3_70B)
+    assert tr.arrays().num_events == rec["num_events"]
+    cap = llama_peak_bytes(tr) // 2
+    assert cap == rec["capacity"]
+    raw = plan_device(tr, cap, ChannelRates.symmetric(16_000), 0)
+    assert hashlib.sha256(raw["plan_bytes"]).hexdigest() == rec["plan_sha256"]
+    assert int(raw["info"].num_commits) == rec["num_commits"]
+    assert hashlib.sha256(raw["residual"].tobytes()).hexdigest() == rec["residual_sha256"]
+
+
 def test_c3_lifetime_and_plan_prefix_vs_oracle():
     """Config C3 (Llama-3-70B shape, E=9,935,960): lifetime bit-exact against
     the oracle; the planner's first 24 commits (max_rounds) against the
