@@ -108,7 +108,6 @@ struct tio_trace {
     int64_t *p_tensor = nullptr, *tpp = nullptr, *blk = nullptr, *scalars = nullptr;
     int32_t *p_start = nullptr, *p_end = nullptr;
     int8_t *p_wraps = nullptr;
-    int lgrid = 0;
     // host copies after sync
     int64_t num_periods = 0, iteration = 0, flags = 0, ids_unsorted = 0;
 };
@@ -221,7 +220,6 @@ int tio_lifetime(tio_trace *t, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     t->arena.stream = s;
     if (!t->starts) {
-        TIO_TRY(lifetime_grid(&t->lgrid));
         TIO_TRY(t->arena.alloc(&t->starts, t->N + 1));
         TIO_TRY(t->arena.alloc(&t->timeline, t->N));
         TIO_TRY(t->arena.alloc(&t->active, t->N));
@@ -231,7 +229,7 @@ int tio_lifetime(tio_trace *t, void *stream) {
         TIO_TRY(t->arena.alloc(&t->p_end, t->E));
         TIO_TRY(t->arena.alloc(&t->p_wraps, t->E));
         TIO_TRY(t->arena.alloc(&t->tpp, t->T + 1));
-        TIO_TRY(t->arena.alloc(&t->blk, lifetime_tiles(t->E) + 2 * (int64_t)t->lgrid));
+        TIO_TRY(t->arena.alloc(&t->blk, lifetime_workspace_elems(t->N, t->E)));
         TIO_CUDA(cudaMemsetAsync(t->diff, 0, 8 * (t->N + 1), s));   // the kernel re-zeroes it behind its scan
         TIO_TRY(t->arena.alloc(&t->scalars, SC_COUNT));
     }
@@ -244,8 +242,7 @@ int tio_lifetime(tio_trace *t, void *stream) {
     a.starts = t->starts; a.timeline = t->timeline; a.active = t->active; a.diff = t->diff;
     a.p_tensor = t->p_tensor; a.p_start = t->p_start; a.p_end = t->p_end; a.p_wraps = t->p_wraps;
     a.tensor_pptr = t->tpp;
-    const int64_t ntiles = lifetime_tiles(t->E);
-    a.blk_periods = t->blk; a.blk_dur = t->blk + ntiles; a.blk_diff = t->blk + ntiles + t->lgrid;
+    a.work = t->blk;
     a.scalars = t->scalars;
     if (t->N == 0) {
         // no kernels: every trace with tensors is invalid (accesses out of range)
@@ -256,7 +253,7 @@ int tio_lifetime(tio_trace *t, void *stream) {
             TIO_CUDA(cudaStreamSynchronize(s));
         }
     } else {
-        TIO_TRY(launch_lifetime(a, t->lgrid, s));
+        TIO_TRY(launch_lifetime(a, s));
     }
     t->lifetime_enqueued = true;
     t->synced = false;
@@ -394,7 +391,8 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     if (T > 0) {
         if (t->ids_unsorted) {
             uint64_t *k0, *k1;
-            uint32_t *v0, *v1, *hist;
+            uint32_t *v0, *v1;
+        int64_t *hist;
             PTRY(A.alloc(&k0, T)); PTRY(A.alloc(&k1, T));
             PTRY(A.alloc(&v0, T)); PTRY(A.alloc(&v1, T));
             PTRY(A.alloc(&hist, radix_hist_elems(T)));
@@ -459,7 +457,8 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     PTRY(A.alloc(&dst.tpos, P)); PTRY(A.alloc(&dst.wraps, P)); PTRY(A.alloc(&dst.st, P));
     {
         uint64_t *k0, *k1;
-        uint32_t *v0, *v1, *hist;
+        uint32_t *v0, *v1;
+        int64_t *hist;
         PTRY(A.alloc(&k0, P)); PTRY(A.alloc(&k1, P)); PTRY(A.alloc(&v0, P)); PTRY(A.alloc(&v1, P));
         PTRY(A.alloc(&hist, radix_hist_elems(P)));
         bool in_tmp = false;
@@ -594,7 +593,8 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     if (nc > 0) {
         const int64_t ne = 2 * nc;
         uint64_t *k0, *k1;
-        uint32_t *v0, *v1, *hist;
+        uint32_t *v0, *v1;
+        int64_t *hist;
         PTRY(A.alloc(&k0, ne)); PTRY(A.alloc(&k1, ne)); PTRY(A.alloc(&v0, ne)); PTRY(A.alloc(&v1, ne));
         PTRY(A.alloc(&hist, radix_hist_elems(ne)));
         const int rbits = bitlen((uint64_t)(T > 0 ? T - 1 : 0));

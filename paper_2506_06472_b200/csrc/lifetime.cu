@@ -1,25 +1,24 @@
-// lifetime.cu — the lifetime stage on sm_100a.
+// lifetime.cu — the lifetime stage on sm_100a (reference analysis.py:58-117,
+// trace.py:97-107) as three streaming kernels, each a single pass over its
+// input with decoupled look-back scans between tiles (no grid barrier, no
+// second read of the events):
 //
-// One cooperative (persistent) kernel, three phases separated by two grid
-// barriers, replacing reference analysis.py:58-117 and trace.py:97-107:
-//
-//   phase A  event tiles (TILE_E consecutive access events of the
-//            tensor-major CSR): the tile's accesses, CSR offsets and tensor
-//            sizes/kinds are staged in shared memory with coalesced loads;
-//            each thread walks a contiguous run of events and
-//              active[k] += size                (per_kernel_active_bytes, :111-117)
-//              diff[first] += size, diff[last+1] -= size for intermediates
-//                                               (compute_memory_timeline, :97-108)
-//              counts inactive periods: gaps b-a>1, and the wrap of a global
-//              when (n-1-last)+first > 0        (compute_inactive_periods, :58-83)
-//              and validates the CSR invariants the kernels rely on;
-//            tensor chunks: sizes/kinds/ids checks, global bytes;
-//            kernel chunks: duration sums (start-time scan).
-//   phase B  period records written at their scanned offsets in reference
-//            order (tensor order, gaps ascending, wrap last) with per-tensor
-//            period offsets; kernel start times; per-chunk diff sums.
-//   phase C  timeline = global bytes + inclusive scan of diff (diff is
-//            re-zeroed behind the scan for the next call).
+//   k_tile_owners  owner tensor of every event-tile boundary (32-ary warp
+//                  searches over the CSR offsets).
+//   k_events       one tile of LT_EPT consecutive events per thread (LT_TILE
+//                  per block, tiles claimed in order from an atomic counter):
+//                    active[k] += size                (per_kernel_active_bytes, :111-117)
+//                    diff[first] += size, diff[last+1] -= size for intermediates
+//                                                     (compute_memory_timeline, :97-108)
+//                    inactive periods: gaps b-a>1, and the wrap of a global
+//                    when (n-1-last)+first > 0, written at their scanned
+//                    offsets in reference order (compute_inactive_periods, :58-83)
+//                    with the per-tensor period offsets;
+//                  plus a slice of the tensor table: CSR / size / kind / id
+//                  order checks and the bytes of the globals.
+//   k_kernels      per kernel tile: start times = exclusive scan of the
+//                  durations, timeline = global bytes + inclusive scan of diff
+//                  (diff re-zeroed behind the scan for the next call).
 //
 // Invalid input never faults (every index is range-checked); it raises a flag
 // the host turns into TIO_ERR_INVALID.
@@ -30,8 +29,6 @@
 #include "lifetime.cuh"
 #include "warp_search.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace tio {
 
 enum : unsigned long long {
@@ -39,329 +36,372 @@ enum : unsigned long long {
     LF_NOT_INCREASING = 16, LF_BAD_KIND = 32
 };
 
-constexpr int EV_PER_THREAD = 8;
-constexpr int TILE_E = LIFETIME_THREADS * EV_PER_THREAD;    // events per tile
+constexpr int LT_EPT = 16;                          // events per thread
+constexpr int LT_TILE = LIFETIME_THREADS * LT_EPT;  // events per tile
+constexpr int LT_MAXO = LT_TILE + 2;                // staged tensors per tile
+constexpr int KT_EPT = 16;                          // kernels per thread
+constexpr int KT_TILE = LIFETIME_THREADS * KT_EPT;
 
-// largest i in [0, T) with ptr[i] <= e (ptr non-decreasing for valid traces)
-__device__ __forceinline__ int64_t owner_global(const int64_t *ptr, int64_t T, int64_t e) {
-    int64_t lo = 0, hi = T;
-    while (hi - lo > 1) {
-        int64_t mid = (lo + hi) >> 1;
-        if (ptr[mid] <= e) lo = mid; else hi = mid;
-    }
-    return lo;
+__host__ __device__ int64_t lifetime_event_tiles(int64_t E) { return (E + LT_TILE - 1) / LT_TILE; }
+__host__ __device__ int64_t lifetime_kernel_tiles(int64_t N) { return (N + KT_TILE - 1) / KT_TILE; }
+
+// workspace layout (int64 words): [0,2) tile counters | owners [NTe+1],
+// padded to an even length | event look-back status [2 NTe] | dur / diff
+// look-back status [2 NTk] each (status words 16-byte aligned)
+__host__ __device__ __forceinline__ int64_t owners_len(int64_t nte) { return (nte + 3) & ~(int64_t)1; }
+int64_t lifetime_workspace_elems(int64_t N, int64_t E) {
+    const int64_t nte = lifetime_event_tiles(E), ntk = lifetime_kernel_tiles(N);
+    return 2 + owners_len(nte) + 2 * nte + 4 * ntk + 8;
 }
 
-// A staged tile: events [e0, e1), tensors [o0, o0 + no) with their CSR
-// offsets ptr[o0 .. o0 + no], sizes and kinds; accesses acc[e0 .. e1] (+1
-// for the next-access look-ahead).  Reads outside the staged ranges fall
-// back to global memory (only reachable with invalid input).
-struct Tile {
-    int64_t e0, e1, o0, no;
-    int64_t *ptr;      // [TILE_E + 2]
-    int64_t *size;     // [TILE_E + 1]
-    int8_t *kind;      // [TILE_E + 1]
-    int32_t *acc;      // [TILE_E + 1]
+// ---------------------------------------------------------------- look-back
+// Tile status {value, flag} as one 16-byte word: flag 1 = the tile's own
+// aggregate, 2 = its inclusive prefix.  Published with a single vector store,
+// polled with relaxed gpu-scope vector loads.
+__device__ __forceinline__ void status_store(int64_t *st, int64_t tile, int64_t value, int64_t flag) {
+    int64_t *p = st + 2 * tile;
+    asm volatile("st.relaxed.gpu.global.v2.s64 [%0], {%1, %2};" ::"l"(p), "l"(value), "l"(flag) : "memory");
+}
+
+__device__ __forceinline__ void status_load(const int64_t *st, int64_t tile, int64_t *value, int64_t *flag) {
+    const int64_t *p = st + 2 * tile;
+    long long v, f;
+    asm volatile("ld.relaxed.gpu.global.v2.s64 {%0, %1}, [%2];" : "=l"(v), "=l"(f) : "l"(p) : "memory");
+    *value = v;
+    *flag = f;
+}
+
+// Exclusive prefix of tile `tile` given its aggregate (warp 0, all lanes;
+// returns the prefix in every lane).  Publishes the aggregate first and the
+// inclusive prefix after.
+__device__ int64_t lookback(int64_t *st, int64_t tile, int64_t agg) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) status_store(st, 0, agg, 2);
+        return 0;
+    }
+    if (lane == 0) status_store(st, tile, agg, 1);
+    int64_t prefix = 0;
+    int64_t base = tile - 1;                 // lanes read base - lane
+    while (true) {
+        const int64_t idx = base - lane;
+        int64_t v = 0, f = 2;                // before tile 0: an inclusive 0
+        if (idx >= 0) {
+            do { status_load(st, idx, &v, &f); } while (f == 0);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 32;      // nearest inclusive prefix
+        int64_t part = lane <= stop ? v : 0;
+        part = warp_sum<int64_t>(part);
+        prefix += part;
+        if (inc) break;
+        base -= 32;
+    }
+    if (lane == 0) status_store(st, tile, prefix + agg, 2);
+    return prefix;
+}
+
+// ---------------------------------------------------------------- owners
+// owner[t] = largest i in [0, T) with ptr[i] <= e_t, e_t = min(t * LT_TILE, E - 1)
+__global__ void k_tile_owners(const int64_t *ptr, int64_t T, int64_t E, int64_t ntiles, int64_t *owner) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (warp > ntiles) return;
+    int64_t e = warp * LT_TILE;
+    if (e > E - 1) e = E - 1;
+    int64_t o = warp_lower_bound(0, T, [&](int64_t j) { return __ldg(ptr + j) > e; }) - 1;
+    if (o < 0) o = 0;
+    if ((threadIdx.x & 31) == 0) owner[warp] = o;
+}
+
+// ---------------------------------------------------------------- events
+struct EvSmem {
+    int32_t ptr[LT_MAXO + 1];   // staged CSR offsets relative to the tile's first event
+    int64_t size[LT_MAXO];
+    int8_t kind[LT_MAXO];
+    int64_t scan[40];
+    int64_t prefix;
+    int64_t tile;
 };
-
-struct TileSmem {
-    int64_t ptr[TILE_E + 2];
-    int64_t size[TILE_E + 1];
-    int32_t acc[TILE_E + 1];
-    int8_t kind[TILE_E + 1];
-    int64_t o[2];
-};
-
-__device__ void stage_tile(const LifetimeArgs &a, int64_t tile, TileSmem &sm, Tile &t) {
-    const int64_t E = a.E, T = a.T;
-    const int64_t e0 = tile * TILE_E, e1 = (e0 + TILE_E < E) ? e0 + TILE_E : E;
-    const int warp = threadIdx.x >> 5;
-    // owners of the first and last event: 32-ary warp searches (largest i with ptr[i] <= e)
-    if (warp < 2) {
-        const int64_t e = warp == 0 ? e0 : e1 - 1;
-        int64_t o = warp_lower_bound(0, T, [&](int64_t j) { return __ldg(a.ptr + j) > e; }) - 1;
-        if (o < 0) o = 0;
-        if ((threadIdx.x & 31) == 0) sm.o[warp] = o;
-    }
-    __syncthreads();
-    int64_t o0 = sm.o[0], o1 = sm.o[1];
-    if (o1 < o0) o1 = o0;
-    int64_t no = o1 - o0 + 1;
-    if (no > TILE_E + 1) no = TILE_E + 1;
-    for (int64_t i = threadIdx.x; i <= no; i += blockDim.x) sm.ptr[i] = (o0 + i <= T) ? a.ptr[o0 + i] : E;
-    for (int64_t i = threadIdx.x; i < no; i += blockDim.x) {
-        sm.size[i] = a.size[o0 + i];
-        sm.kind[i] = a.kind[o0 + i];
-    }
-    for (int64_t i = threadIdx.x; i <= e1 - e0; i += blockDim.x)
-        sm.acc[i] = (e0 + i < E) ? a.acc[e0 + i] : 0;
-    __syncthreads();
-    t.e0 = e0; t.e1 = e1; t.o0 = o0; t.no = no;
-    t.ptr = sm.ptr; t.size = sm.size; t.kind = sm.kind; t.acc = sm.acc;
-}
-
-// staged accessors with global fallback
-__device__ __forceinline__ int64_t t_ptr(const LifetimeArgs &a, const Tile &t, int64_t i) {
-    return (i >= t.o0 && i <= t.o0 + t.no) ? t.ptr[i - t.o0] : (i <= a.T ? a.ptr[i] : a.E);
-}
-__device__ __forceinline__ int64_t t_size(const LifetimeArgs &a, const Tile &t, int64_t i) {
-    return (i >= t.o0 && i < t.o0 + t.no) ? t.size[i - t.o0] : a.size[i];
-}
-__device__ __forceinline__ int8_t t_kind(const LifetimeArgs &a, const Tile &t, int64_t i) {
-    return (i >= t.o0 && i < t.o0 + t.no) ? t.kind[i - t.o0] : a.kind[i];
-}
-__device__ __forceinline__ int64_t t_acc(const LifetimeArgs &a, const Tile &t, int64_t e) {
-    return (e >= t.e0 && e <= t.e1) ? t.acc[e - t.e0] : (e < a.E ? a.acc[e] : 0);
-}
-
-// owner of event e inside the staged tensor range: largest i with ptr[i] <= e
-__device__ __forceinline__ int64_t t_owner(const LifetimeArgs &a, const Tile &t, int64_t e) {
-    int64_t lo = 0, hi = t.no;           // staged ptr[0 .. no]
-    if (t.no <= 0 || t.ptr[0] > e) return owner_global(a.ptr, a.T, e);
-    while (hi - lo > 1) {
-        int64_t mid = (lo + hi) >> 1;
-        if (t.ptr[mid] <= e) lo = mid; else hi = mid;
-    }
-    int64_t own = t.o0 + lo;
-    if (own >= a.T) own = a.T - 1;
-    return own;
-}
 
 __global__ void __launch_bounds__(LIFETIME_THREADS)
-lifetime_kernel(LifetimeArgs a) {
-    cg::grid_group grid = cg::this_grid();
+k_events(LifetimeArgs a) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    TileSmem &tsm = *reinterpret_cast<TileSmem *>(smraw);
-    __shared__ int64_t sm[40];
-    __shared__ int64_t s_pre[64];            // prefixes of this block's tiles / chunks
-
+    EvSmem &sm = *reinterpret_cast<EvSmem *>(smraw);
     const int64_t N = a.N, T = a.T, E = a.E;
-    const int G = gridDim.x, b = blockIdx.x;
-    const int64_t NT = (E + TILE_E - 1) / TILE_E;                 // event tiles
-    const int64_t gtid = (int64_t)b * blockDim.x + threadIdx.x;
-    const int64_t nthreads = (int64_t)G * blockDim.x;
-    const int64_t kchunk = (N + G - 1) / G;                       // kernel chunk per block
-    const int64_t k0 = (int64_t)b * kchunk < N ? (int64_t)b * kchunk : N;
-    const int64_t k1 = k0 + kchunk < N ? k0 + kchunk : N;
+    const int64_t NTe = lifetime_event_tiles(E);
+    int64_t *counter = a.work;
+    const int64_t *owner = a.work + 2;
+    int64_t *est = a.work + 2 + owners_len(NTe);
     unsigned long long flags = 0;
 
-    // ------------------------------------------------------------ phase A
-    // tensor-level checks and global bytes
-    int64_t glob = 0;
-    for (int64_t i = gtid; i < T; i += nthreads) {
-        const int64_t p0 = a.ptr[i], p1 = a.ptr[i + 1];
-        if (p1 <= p0) flags |= LF_BAD_PTR;
-        if (a.size[i] <= 0) flags |= LF_BAD_SIZE;
-        const int8_t kd = a.kind[i];
-        if (kd != 0 && kd != 1) flags |= LF_BAD_KIND;
-        if (kd == 1) glob += a.size[i];
-        if (i + 1 < T && !(a.tid[i] < a.tid[i + 1])) a.scalars[SC_IDS_UNSORTED] = 1;
+    if (threadIdx.x == 0) sm.tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+    __syncthreads();
+    const int64_t tile = sm.tile;
+
+    // ---- tensor-table slice: CSR / size / kind / id order, global bytes
+    {
+        const int64_t per = (T + gridDim.x - 1) / gridDim.x;
+        const int64_t i0 = tile * per, i1 = i0 + per < T ? i0 + per : T;
+        int64_t glob = 0;
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+            if (__ldg(a.ptr + i + 1) <= __ldg(a.ptr + i)) flags |= LF_BAD_PTR;
+            const int64_t sz = __ldg(a.size + i);
+            if (sz <= 0) flags |= LF_BAD_SIZE;
+            const int8_t kd = __ldg(a.kind + i);
+            if (kd != 0 && kd != 1) flags |= LF_BAD_KIND;
+            if (kd == 1) glob += sz;
+            if (i + 1 < T && !(__ldg(a.tid + i) < __ldg(a.tid + i + 1))) a.scalars[SC_IDS_UNSORTED] = 1;
+        }
+        if (tile == 0 && threadIdx.x == 0 && (__ldg(a.ptr) != 0 || __ldg(a.ptr + T) != E)) flags |= LF_BAD_PTR;
+        const int64_t g = block_sum<int64_t>(glob, sm.scan);
+        if (threadIdx.x == 0 && g) atomic_add_i64(&a.scalars[SC_GLOBAL_BYTES], g);
     }
-    if (gtid == 0 && (a.ptr[0] != 0 || a.ptr[T] != E)) flags |= LF_BAD_PTR;
-    // event tiles: atomics and period counts
-    const bool single_tile = NT > b && NT - b <= G;    // this block owns exactly one tile
-    Tile kept{};
-    for (int64_t tile = b; tile < NT; tile += G) {
-        Tile t;
-        stage_tile(a, tile, tsm, t);
-        kept = t;
-        const int64_t r0 = t.e0 + (int64_t)threadIdx.x * EV_PER_THREAD;
-        const int64_t r1 = r0 + EV_PER_THREAD < t.e1 ? r0 + EV_PER_THREAD : t.e1;
-        int64_t cnt = 0;
-        if (r0 < r1) {
-            int64_t own = t_owner(a, t, r0);
-            int64_t beg = t_ptr(a, t, own), nxt = t_ptr(a, t, own + 1);
-            for (int64_t e = r0; e < r1; ++e) {
-                while (e >= nxt && own + 1 < T) { ++own; beg = nxt; nxt = t_ptr(a, t, own + 1); }
-                const int64_t k = t_acc(a, t, e);
-                if (k < 0 || k >= N) { flags |= LF_ACCESS_RANGE; continue; }
-                const int64_t size = t_size(a, t, own);
-                const int8_t kd = t_kind(a, t, own);
-                atomic_add_i64(&a.active[k], size);
-                const bool last = (e == nxt - 1);
-                if (!last) {
-                    const int64_t k2 = t_acc(a, t, e + 1);
-                    if (k2 <= k) flags |= LF_NOT_INCREASING;
-                    else if (k2 - k > 1) ++cnt;
-                } else if (kd == 1) {
-                    const int64_t first = t_acc(a, t, beg);
-                    if ((N - 1 - k) + first > 0) ++cnt;
-                }
-                if (kd == 0) {
-                    if (e == beg) atomic_add_i64(&a.diff[k], size);
-                    if (last) atomic_add_i64(&a.diff[k + 1], -size);
-                }
+    if (tile >= NTe) {
+        if (flags) atomicOr(reinterpret_cast<unsigned long long *>(&a.scalars[SC_FLAGS]), flags);
+        return;
+    }
+
+    // ---- stage the tile: its tensors' offsets, sizes, kinds
+    const int64_t e0 = tile * LT_TILE, e1 = (e0 + LT_TILE < E) ? e0 + LT_TILE : E;
+    const int64_t o0 = __ldcg(reinterpret_cast<const long long *>(owner + tile));
+    int64_t o1 = __ldcg(reinterpret_cast<const long long *>(owner + tile + 1));
+    if (o1 < o0) o1 = o0;
+    int64_t no = o1 - o0 + 1;
+    if (no > LT_MAXO) no = LT_MAXO;        // only with empty tensors (invalid; global fallback)
+    for (int64_t i = threadIdx.x; i <= no; i += blockDim.x) {
+        const int64_t p = (o0 + i <= T) ? __ldg(a.ptr + o0 + i) : E;
+        sm.ptr[i] = (int32_t)(p - e0 < INT32_MIN ? INT32_MIN : (p - e0 > INT32_MAX ? INT32_MAX : p - e0));
+    }
+    for (int64_t i = threadIdx.x; i < no; i += blockDim.x) {
+        sm.size[i] = __ldg(a.size + o0 + i);
+        sm.kind[i] = __ldg(a.kind + o0 + i);
+    }
+    // ---- this thread's events (vector loads; the tile start is 64-byte aligned)
+    const int64_t f = e0 + (int64_t)threadIdx.x * LT_EPT;
+    int32_t k[LT_EPT + 1];
+    if (f + LT_EPT <= E && ((uintptr_t)a.acc & 15) == 0) {
+        const int4 *q = reinterpret_cast<const int4 *>(a.acc + f);
+#pragma unroll
+        for (int j = 0; j < LT_EPT / 4; ++j) {
+            const int4 v = __ldg(q + j);
+            k[4 * j] = v.x; k[4 * j + 1] = v.y; k[4 * j + 2] = v.z; k[4 * j + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) k[j] = f + j < E ? __ldg(a.acc + f + j) : 0;
+    }
+    k[LT_EPT] = f + LT_EPT < E ? __ldg(a.acc + f + LT_EPT) : 0;
+    __syncthreads();
+
+    auto ptr_of = [&](int64_t i) -> int64_t {     // CSR offset of tensor i
+        const int64_t r = i - o0;
+        if (r >= 0 && r <= no) return e0 + sm.ptr[r];
+        return i <= T ? __ldg(a.ptr + i) : E;
+    };
+    auto size_of = [&](int64_t i) -> int64_t {
+        const int64_t r = i - o0;
+        return (r >= 0 && r < no) ? sm.size[r] : __ldg(a.size + i);
+    };
+    auto kind_of = [&](int64_t i) -> int8_t {
+        const int64_t r = i - o0;
+        return (r >= 0 && r < no) ? sm.kind[r] : __ldg(a.kind + i);
+    };
+    // owner of the first event: largest staged i with ptr <= f
+    int64_t own0 = o0;
+    const int64_t nev = f < e1 ? (e1 - f < LT_EPT ? e1 - f : LT_EPT) : 0;
+    if (nev > 0) {
+        int lo = 0, hi = (int)no;                   // staged ptr[0 .. no]
+        const int32_t rel = (int32_t)(f - e0);
+        if (sm.ptr[0] <= rel) {
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (sm.ptr[mid] <= rel) lo = mid; else hi = mid;
+            }
+            own0 = o0 + lo;
+        }
+        if (own0 >= T) own0 = T - 1;
+    }
+
+    // ---- pass 1: atomics, validation, period count
+    int64_t cnt = 0;
+    {
+        int64_t own = own0, beg = ptr_of(own0), nxt = ptr_of(own0 + 1);
+        int64_t firstk = 0;                       // first access of `own` if seen in this run
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) {
+            if (j >= nev) break;
+            const int64_t e = f + j;
+            while (e >= nxt && own + 1 < T) { ++own; beg = nxt; nxt = ptr_of(own + 1); }
+            const int64_t kk = k[j];
+            if (e == beg) firstk = kk;
+            if (kk < 0 || kk >= N) { flags |= LF_ACCESS_RANGE; continue; }
+            const int64_t sz = size_of(own);
+            const int8_t kd = kind_of(own);
+            atomic_add_i64(&a.active[kk], sz);
+            const bool last = e == nxt - 1;
+            if (!last) {
+                const int64_t k2 = k[j + 1];
+                if (k2 <= kk) flags |= LF_NOT_INCREASING;
+                else if (k2 - kk > 1) ++cnt;
+            } else if (kd == 1) {
+                const int64_t first = beg >= f ? firstk : __ldg(a.acc + beg);
+                if ((N - 1 - kk) + first > 0) ++cnt;
+            }
+            if (kd == 0) {
+                if (e == beg) atomic_add_i64(&a.diff[kk], sz);
+                if (last) atomic_add_i64(&a.diff[kk + 1], -sz);
             }
         }
-        const int64_t tot = block_sum<int64_t>(cnt, sm);
-        if (threadIdx.x == 0) a.blk_periods[tile] = tot;
-    }
-    // kernel chunk: duration sum + validation
-    {
-        int64_t dsum = 0;
-        for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-            const int64_t d = a.dur[k];
-            if (d <= 0) flags |= LF_BAD_DURATION;
-            dsum += d;
-        }
-        const int64_t dtot = block_sum<int64_t>(dsum, sm);
-        if (threadIdx.x == 0) a.blk_dur[b] = dtot;
-        const int64_t gtot = block_sum<int64_t>(glob, sm);
-        if (threadIdx.x == 0 && gtot) atomic_add_i64(&a.scalars[SC_GLOBAL_BYTES], gtot);
     }
     if (flags) atomicOr(reinterpret_cast<unsigned long long *>(&a.scalars[SC_FLAGS]), flags);
-    grid.sync();
 
-    // ------------------------------------------------------------ phase B
-    // exclusive prefixes of the tile period counts for this block's tiles
-    // (scanned redundantly per block; tiles b, b + G, ... take slots 0, 1, ...)
-    auto prefix_for_mine = [&](const int64_t *vals, int64_t n, int64_t *out_slots, int64_t *grand) {
-        int64_t run = 0;
-        for (int64_t base = 0; base < n; base += blockDim.x) {
-            const int64_t j = base + threadIdx.x;
-            const int64_t v = j < n ? __ldcg(reinterpret_cast<const long long *>(vals + j)) : 0;
-            int64_t tot;
-            const int64_t ex = block_exclusive_sum<int64_t>(v, sm, &tot);
-            if (j < n && j % G == b && j / G < 64) out_slots[j / G] = run + ex;
-            run += tot;
-        }
-        if (grand) *grand = run;
-    };
-    const bool valid = __ldcg(reinterpret_cast<const long long *>(&a.scalars[SC_FLAGS])) == 0;
-    int64_t total_periods = 0;
-    prefix_for_mine(a.blk_periods, NT, s_pre, &total_periods);
+    // ---- tile offset: block scan + decoupled look-back over tiles
+    int64_t tot;
+    int64_t out = block_exclusive_sum<int64_t>(cnt, sm.scan, &tot);
+    if (threadIdx.x < 32) {
+        const int64_t pre = lookback(est, tile, tot);
+        if (threadIdx.x == 0) sm.prefix = pre;
+    }
     __syncthreads();
-    int64_t slot = 0;
-    for (int64_t tile = b; tile < NT; tile += G, ++slot) {
-        // more than 64 tiles per block: recompute the prefix directly
-        int64_t base_off;
-        if (slot < 64) base_off = s_pre[slot];
-        else {
-            int64_t v = 0;
-            for (int64_t j = threadIdx.x; j < tile; j += blockDim.x)
-                v += __ldcg(reinterpret_cast<const long long *>(a.blk_periods + j));
-            base_off = block_sum<int64_t>(v, sm);
-        }
-        Tile t;
-        if (single_tile) t = kept;              // still staged in shared memory
-        else stage_tile(a, tile, tsm, t);
-        const int64_t r0 = t.e0 + (int64_t)threadIdx.x * EV_PER_THREAD;
-        const int64_t r1 = r0 + EV_PER_THREAD < t.e1 ? r0 + EV_PER_THREAD : t.e1;
-        // count again (cheap, staged) to place this thread's periods
-        int64_t cnt = 0;
-        int64_t own = 0, beg = 0, nxt = 0;
-        if (valid && r0 < r1) {
-            own = t_owner(a, t, r0);
-            beg = t_ptr(a, t, own); nxt = t_ptr(a, t, own + 1);
-            int64_t o = own, bg = beg, nx = nxt;
-            for (int64_t e = r0; e < r1; ++e) {
-                while (e >= nx && o + 1 < T) { ++o; bg = nx; nx = t_ptr(a, t, o + 1); }
-                const int64_t k = t_acc(a, t, e);
-                if (e != nx - 1) { if (t_acc(a, t, e + 1) - k > 1) ++cnt; }
-                else if (t_kind(a, t, o) == 1 && (N - 1 - k) + t_acc(a, t, bg) > 0) ++cnt;
-            }
-        }
-        int64_t tot;
-        int64_t out = block_exclusive_sum<int64_t>(cnt, sm, &tot) + base_off;
-        if (valid && r0 < r1) {
-            for (int64_t e = r0; e < r1; ++e) {
-                while (e >= nxt && own + 1 < T) { ++own; beg = nxt; nxt = t_ptr(a, t, own + 1); }
-                if (e == beg) a.tensor_pptr[own] = out;
-                const int64_t k = t_acc(a, t, e);
-                if (e != nxt - 1) {
-                    const int64_t k2 = t_acc(a, t, e + 1);
-                    if (k2 - k > 1) {
-                        a.p_tensor[out] = own; a.p_start[out] = (int32_t)(k + 1);
-                        a.p_end[out] = (int32_t)(k2 - 1); a.p_wraps[out] = 0; ++out;
-                    }
-                } else if (t_kind(a, t, own) == 1) {
-                    const int64_t first = t_acc(a, t, beg);
-                    if ((N - 1 - k) + first > 0) {
-                        a.p_tensor[out] = own; a.p_start[out] = (int32_t)((k + 1) % N);
-                        a.p_end[out] = (int32_t)(((first - 1) % N + N) % N);
-                        a.p_wraps[out] = 1; ++out;
-                    }
+    out += sm.prefix;
+    if (tile == NTe - 1 && threadIdx.x == 0) {
+        a.tensor_pptr[T] = sm.prefix + tot;
+        a.scalars[SC_NUM_PERIODS] = sm.prefix + tot;
+    }
+
+    // ---- pass 2: period records in reference order + per-tensor offsets
+    // (analysis.py:68-82: tensor order, gaps ascending, wrap last)
+    if (nev > 0 && flags == 0) {
+        int64_t own = own0, beg = ptr_of(own0), nxt = ptr_of(own0 + 1);
+        int64_t firstk = 0;
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) {
+            if (j >= nev) break;
+            const int64_t e = f + j;
+            while (e >= nxt && own + 1 < T) { ++own; beg = nxt; nxt = ptr_of(own + 1); }
+            const int64_t kk = k[j];
+            if (e == beg) { a.tensor_pptr[own] = out; firstk = kk; }
+            if (e != nxt - 1) {
+                const int64_t k2 = k[j + 1];
+                if (k2 - kk > 1) {
+                    a.p_tensor[out] = own; a.p_start[out] = (int32_t)(kk + 1);
+                    a.p_end[out] = (int32_t)(k2 - 1); a.p_wraps[out] = 0; ++out;
+                }
+            } else if (kind_of(own) == 1) {
+                const int64_t first = beg >= f ? firstk : __ldg(a.acc + beg);
+                if ((N - 1 - kk) + first > 0) {
+                    a.p_tensor[out] = own; a.p_start[out] = (int32_t)((kk + 1) % N);
+                    a.p_end[out] = (int32_t)(((first - 1) % N + N) % N);
+                    a.p_wraps[out] = 1; ++out;
                 }
             }
         }
     }
-    if (b == 0 && threadIdx.x == 0) {
-        a.tensor_pptr[T] = total_periods;
-        a.scalars[SC_NUM_PERIODS] = total_periods;
-    }
-    // kernel start times for this block's chunk
-    {
-        int64_t v = 0;
-        for (int j = threadIdx.x; j < b; j += blockDim.x)
-            v += __ldcg(reinterpret_cast<const long long *>(&a.blk_dur[j]));
-        int64_t run = block_sum<int64_t>(v, sm);
-        for (int64_t base = k0; base < k1; base += blockDim.x) {
-            const int64_t k = base + threadIdx.x;
-            const int64_t d = k < k1 ? a.dur[k] : 0;
-            int64_t tot;
-            const int64_t ex = block_exclusive_sum<int64_t>(d, sm, &tot);
-            if (k < k1) a.starts[k] = run + ex;
-            run += tot;
-        }
-        if (b == G - 1 && threadIdx.x == 0) a.starts[N] = run;
-    }
-    // diff chunk sums (the atomics of phase A are complete)
-    {
-        int64_t v = 0;
-        for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
-            v += __ldcg(reinterpret_cast<const long long *>(&a.diff[k]));
-        const int64_t tot = block_sum<int64_t>(v, sm);
-        if (threadIdx.x == 0) a.blk_diff[b] = tot;
-    }
-    grid.sync();
+}
 
-    // ------------------------------------------------------------ phase C
-    {
-        int64_t v = 0;
-        for (int j = threadIdx.x; j < b; j += blockDim.x)
-            v += __ldcg(reinterpret_cast<const long long *>(&a.blk_diff[j]));
-        const int64_t pv = block_sum<int64_t>(v, sm);
-        int64_t run = pv + __ldcg(reinterpret_cast<const long long *>(&a.scalars[SC_GLOBAL_BYTES]));
-        for (int64_t base = k0; base < k1; base += blockDim.x) {
-            const int64_t k = base + threadIdx.x;
-            const int64_t d = k < k1 ? __ldcg(reinterpret_cast<const long long *>(&a.diff[k])) : 0;
-            int64_t tot;
-            const int64_t ex = block_exclusive_sum<int64_t>(d, sm, &tot);
-            if (k < k1) {
-                a.timeline[k] = run + ex + d;
-                a.diff[k] = 0;                        // ready for the next call
-            }
-            run += tot;
+// ---------------------------------------------------------------- kernels
+__global__ void __launch_bounds__(LIFETIME_THREADS)
+k_kernels(LifetimeArgs a) {
+    __shared__ int64_t scan[40];
+    __shared__ int64_t s_pre[2];
+    __shared__ int64_t s_tile;
+    const int64_t N = a.N, E = a.E;
+    const int64_t NTe = lifetime_event_tiles(E), NTk = lifetime_kernel_tiles(N);
+    int64_t *counter = a.work + 1;
+    int64_t *dst = a.work + 2 + owners_len(NTe) + 2 * NTe;
+    int64_t *fst = dst + 2 * NTk;
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= NTk) return;
+    const int64_t k0 = tile * KT_TILE + (int64_t)threadIdx.x * KT_EPT;
+    int64_t d[KT_EPT], df[KT_EPT];
+    const bool vec = (((uintptr_t)a.dur | (uintptr_t)a.diff | (uintptr_t)a.starts | (uintptr_t)a.timeline) & 15) == 0;
+    if (k0 + KT_EPT <= N && vec) {
+        const longlong2 *qd = reinterpret_cast<const longlong2 *>(a.dur + k0);
+        const longlong2 *qf = reinterpret_cast<const longlong2 *>(a.diff + k0);
+#pragma unroll
+        for (int j = 0; j < KT_EPT / 2; ++j) {
+            const longlong2 x = __ldg(qd + j), y = __ldcg(qf + j);
+            d[2 * j] = x.x; d[2 * j + 1] = x.y; df[2 * j] = y.x; df[2 * j + 1] = y.y;
         }
-        if (b == G - 1 && threadIdx.x == 0) a.diff[N] = 0;
+    } else {
+#pragma unroll
+        for (int j = 0; j < KT_EPT; ++j) {
+            d[j] = k0 + j < N ? __ldg(a.dur + k0 + j) : 0;
+            df[j] = k0 + j < N ? __ldcg(reinterpret_cast<const long long *>(a.diff + k0 + j)) : 0;
+        }
+    }
+    unsigned long long flags = 0;
+    int64_t sd = 0, sf = 0;
+#pragma unroll
+    for (int j = 0; j < KT_EPT; ++j) {
+        if (k0 + j < N && d[j] <= 0) flags |= LF_BAD_DURATION;
+        sd += d[j];
+        sf += df[j];
+    }
+    if (flags) atomicOr(reinterpret_cast<unsigned long long *>(&a.scalars[SC_FLAGS]), flags);
+    int64_t td, tf;
+    int64_t xd = block_exclusive_sum<int64_t>(sd, scan, &td);
+    int64_t xf = block_exclusive_sum<int64_t>(sf, scan, &tf);
+    if (threadIdx.x < 32) {
+        const int64_t pd = lookback(dst, tile, td);
+        const int64_t pf = lookback(fst, tile, tf);
+        if (threadIdx.x == 0) { s_pre[0] = pd; s_pre[1] = pf; }
+    }
+    __syncthreads();
+    xd += s_pre[0];
+    xf += s_pre[1] + __ldcg(reinterpret_cast<const long long *>(&a.scalars[SC_GLOBAL_BYTES]));
+    int64_t so[KT_EPT], to[KT_EPT];
+#pragma unroll
+    for (int j = 0; j < KT_EPT; ++j) {
+        so[j] = xd; xd += d[j];
+        xf += df[j]; to[j] = xf;
+    }
+    if (k0 + KT_EPT <= N && vec) {
+        longlong2 *ps = reinterpret_cast<longlong2 *>(a.starts + k0);
+        longlong2 *pt = reinterpret_cast<longlong2 *>(a.timeline + k0);
+        longlong2 *pz = reinterpret_cast<longlong2 *>(a.diff + k0);
+#pragma unroll
+        for (int j = 0; j < KT_EPT / 2; ++j) {
+            ps[j] = make_longlong2(so[2 * j], so[2 * j + 1]);
+            pt[j] = make_longlong2(to[2 * j], to[2 * j + 1]);
+            pz[j] = make_longlong2(0, 0);                      // ready for the next call
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < KT_EPT; ++j)
+            if (k0 + j < N) { a.starts[k0 + j] = so[j]; a.timeline[k0 + j] = to[j]; a.diff[k0 + j] = 0; }
+    }
+    if (tile == NTk - 1 && threadIdx.x == blockDim.x - 1) {
+        a.starts[N] = s_pre[0] + td;
+        a.diff[N] = 0;
     }
 }
 
-int lifetime_grid(int *blocks) {
-    static int cached = 0;
-    if (!cached) {
-        int dev = 0, sms = 0, per_sm = 0;
-        TIO_CUDA(cudaGetDevice(&dev));
-        TIO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        TIO_CUDA(cudaFuncSetAttribute(lifetime_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sizeof(TileSmem)));
-        TIO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lifetime_kernel, LIFETIME_THREADS,
-                                                               sizeof(TileSmem)));
-        if (per_sm < 1) return fail(TIO_ERR_CUDA, "lifetime kernel cannot be resident");
-        cached = sms * (per_sm < 4 ? per_sm : 4);
-        if (cached > 1024) cached = 1024;
+int launch_lifetime(const LifetimeArgs &args, cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        TIO_CUDA(cudaFuncSetAttribute(k_events, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EvSmem)));
+        attr = true;
     }
-    *blocks = cached;
-    return TIO_OK;
-}
-
-int64_t lifetime_tiles(int64_t E) { return (E + TILE_E - 1) / TILE_E; }
-
-int launch_lifetime(const LifetimeArgs &args, int blocks, cudaStream_t stream) {
-    void *params[] = {const_cast<LifetimeArgs *>(&args)};
-    TIO_CUDA(cudaLaunchCooperativeKernel((const void *)lifetime_kernel, dim3(blocks),
-                                         dim3(LIFETIME_THREADS), params, sizeof(TileSmem), stream));
+    const int64_t NTe = lifetime_event_tiles(args.E), NTk = lifetime_kernel_tiles(args.N);
+    // counters + event / kernel look-back status
+    TIO_CUDA(cudaMemsetAsync(args.work, 0, sizeof(int64_t) * 2, stream));
+    TIO_CUDA(cudaMemsetAsync(args.work + 2 + owners_len(NTe), 0, sizeof(int64_t) * (2 * NTe + 4 * NTk), stream));
+    if (NTe > 0) {
+        const int64_t thr = 32 * (NTe + 1);
+        k_tile_owners<<<(unsigned)((thr + 255) / 256), 256, 0, stream>>>(args.ptr, args.T, args.E, NTe, args.work + 2);
+        count_launch();
+    }
+    const int64_t nb = NTe > 0 ? NTe : 1;            // >= 1 block: the tensor-table checks
+    k_events<<<(unsigned)nb, LIFETIME_THREADS, sizeof(EvSmem), stream>>>(args);
     count_launch();
+    if (NTk > 0) {
+        k_kernels<<<(unsigned)NTk, LIFETIME_THREADS, 0, stream>>>(args);
+        count_launch();
+    }
+    TIO_CUDA(cudaGetLastError());
     return TIO_OK;
 }
 

@@ -27,14 +27,14 @@ struct LifetimeArgs {
     int32_t *p_end;
     int8_t *p_wraps;
     int64_t *tensor_pptr;  // [T+1]
-    int64_t *blk_periods;  // [event tiles]
-    int64_t *blk_dur;      // [grid]
-    int64_t *blk_diff;     // [grid]
+    int64_t *work;         // [lifetime_workspace_elems(N, E)] tile counters, owners, look-back status
     int64_t *scalars;      // [SC_COUNT] zeroed by the caller
 };
 
-int lifetime_grid(int *blocks);
-int64_t lifetime_tiles(int64_t E);   // event tiles (blk_periods entries)
-int launch_lifetime(const LifetimeArgs &args, int blocks, cudaStream_t stream);
+__host__ __device__ int64_t lifetime_event_tiles(int64_t E);
+__host__ __device__ int64_t lifetime_kernel_tiles(int64_t N);
+int64_t lifetime_workspace_elems(int64_t N, int64_t E);
+// enqueues the lifetime stage (memsets of its look-back state + 3 kernels)
+int launch_lifetime(const LifetimeArgs &args, cudaStream_t stream);
 
 }  // namespace tio

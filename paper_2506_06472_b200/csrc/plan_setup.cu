@@ -167,7 +167,8 @@ __global__ void k_over_flags(const int64_t *resid, int64_t N, int64_t cap, int64
         flag[k] = r > cap;
         if (r > m) m = r;
     }
-    if (m != LLONG_MIN) atomicMax(peak, m);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m != LLONG_MIN) atomicMax(peak, m);   // one atomic per warp
 }
 
 __global__ void k_over_write(const int64_t *flag, const int64_t *pos, int64_t N, int64_t *over) {

@@ -1,12 +1,14 @@
 // radix_sort.cu — hand-written stable LSD radix sort of (u64 key, u32 value)
 // pairs on sm_100a.  8-bit digits; per pass: tile histograms (digit-major),
-// one-block exclusive scan of the histogram, and a scatter in which each tile
-// ranks its keys stably with eight 1-bit block splits in shared memory.
+// a device-wide exclusive scan of the histogram (scan.cu, reduce-then-scan),
+// and a scatter in which each tile ranks its keys stably with eight 1-bit
+// block splits in shared memory.
 // Used for tensor-id ordering of candidates (planner.py:283-284) and the
 // plan-entry order (planner.py:360-361); only the bits that vary are sorted.
 #include "common.cuh"
 #include "block_scan.cuh"
 #include "radix_sort.cuh"
+#include "scan.cuh"
 
 namespace tio {
 
@@ -15,7 +17,7 @@ constexpr int RS_ITEMS = 4;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 
 __global__ void __launch_bounds__(RS_THREADS)
-rs_hist(const uint64_t *keys, int64_t n, int shift, uint32_t *hist, int64_t ntiles) {
+rs_hist(const uint64_t *keys, int64_t n, int shift, int64_t *hist, int64_t ntiles) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
@@ -28,27 +30,9 @@ rs_hist(const uint64_t *keys, int64_t n, int shift, uint32_t *hist, int64_t ntil
     hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
-// exclusive scan of m uint32 counts in place, one block of 1024 threads
-__global__ void __launch_bounds__(1024)
-rs_scan(uint32_t *hist, int64_t m) {
-    __shared__ int64_t sm[40];
-    const int64_t per = (m + blockDim.x - 1) / blockDim.x;
-    const int64_t b0 = threadIdx.x * per;
-    const int64_t b1 = b0 + per < m ? b0 + per : m;
-    int64_t s = 0;
-    for (int64_t i = b0; i < b1; ++i) s += hist[i];
-    int64_t tot;
-    int64_t run = block_exclusive_sum<int64_t>(s, sm, &tot);
-    for (int64_t i = b0; i < b1; ++i) {
-        uint32_t v = hist[i];
-        hist[i] = (uint32_t)run;
-        run += v;
-    }
-}
-
 __global__ void __launch_bounds__(RS_THREADS)
 rs_scatter(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout, int64_t n,
-           int shift, const uint32_t *offs, int64_t ntiles) {
+           int shift, const int64_t *offs, int64_t ntiles) {
     __shared__ uint64_t sk[2][RS_TILE];
     __shared__ uint32_t sv[2][RS_TILE];
     __shared__ uint32_t dstart[256];
@@ -108,7 +92,7 @@ rs_scatter(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *v
 }
 
 int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_t *vals_tmp,
-                     uint32_t *hist, int64_t n, int bits, cudaStream_t stream, bool *result_in_tmp) {
+                     int64_t *hist, int64_t n, int bits, cudaStream_t stream, bool *result_in_tmp) {
     *result_in_tmp = false;
     if (n <= 1 || bits <= 0) return TIO_OK;
     const int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
@@ -116,7 +100,7 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_
     uint32_t *va = vals, *vb = vals_tmp;
     for (int shift = 0; shift < bits; shift += 8) {
         rs_hist<<<(unsigned)ntiles, RS_THREADS, 0, stream>>>(ka, n, shift, hist, ntiles); ::tio::count_launch();
-        rs_scan<<<1, 1024, 0, stream>>>(hist, 256 * ntiles); ::tio::count_launch();
+        TIO_TRY(exclusive_scan(hist, hist, 256 * ntiles, hist + 256 * ntiles, nullptr, stream));
         rs_scatter<<<(unsigned)ntiles, RS_THREADS, 0, stream>>>(ka, va, kb, vb, n, shift, hist, ntiles); ::tio::count_launch();
         TIO_CUDA(cudaGetLastError());
         uint64_t *tk = ka; ka = kb; kb = tk;
@@ -126,6 +110,10 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_
     return TIO_OK;
 }
 
-int64_t radix_hist_elems(int64_t n) { return 256 * ((n + RS_TILE - 1) / RS_TILE) + 1; }
+// histogram + the scan's tile totals
+int64_t radix_hist_elems(int64_t n) {
+    const int64_t m = 256 * ((n + RS_TILE - 1) / RS_TILE);
+    return m + scan_tmp_elems(m) + 1;
+}
 
 }  // namespace tio
