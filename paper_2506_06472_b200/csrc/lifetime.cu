@@ -39,7 +39,7 @@ enum : unsigned long long {
 constexpr int LT_EPT = 16;                          // events per thread
 constexpr int LT_TILE = LIFETIME_THREADS * LT_EPT;  // events per tile
 constexpr int LT_MAXO = LT_TILE + 2;                // staged tensors per tile
-constexpr int KT_EPT = 16;                          // kernels per thread
+constexpr int KT_EPT = 8;                           // kernels per thread
 constexpr int KT_TILE = LIFETIME_THREADS * KT_EPT;
 
 __host__ __device__ int64_t lifetime_event_tiles(int64_t E) { return (E + LT_TILE - 1) / LT_TILE; }
@@ -71,34 +71,44 @@ __device__ __forceinline__ void status_load(const int64_t *st, int64_t tile, int
     *flag = f;
 }
 
-// Exclusive prefix of tile `tile` given its aggregate (warp 0, all lanes;
-// returns the prefix in every lane).  Publishes the aggregate first and the
-// inclusive prefix after.
-__device__ int64_t lookback(int64_t *st, int64_t tile, int64_t agg) {
+// Decoupled look-back, split so a tile can publish its aggregate as soon as
+// it is known and do independent work before it needs its prefix.
+__device__ __forceinline__ void lookback_publish(int64_t *st, int64_t tile, int64_t agg) {
+    if ((threadIdx.x & 31) == 0) status_store(st, tile, agg, tile == 0 ? 2 : 1);
+}
+
+// Exclusive prefix of tile `tile` (one warp, all lanes; the result in every
+// lane); publishes the inclusive prefix.  nch independent chains (stride
+// cstride words) resolved in the same loop.
+template <int NCH>
+__device__ void lookback_resolve(int64_t *st, int64_t cstride, int64_t tile, const int64_t *agg, int64_t *prefix) {
     const int lane = threadIdx.x & 31;
-    if (tile == 0) {
-        if (lane == 0) status_store(st, 0, agg, 2);
-        return 0;
-    }
-    if (lane == 0) status_store(st, tile, agg, 1);
-    int64_t prefix = 0;
+    for (int c = 0; c < NCH; ++c) prefix[c] = 0;
+    if (tile == 0) return;
+    bool done[NCH];
+    for (int c = 0; c < NCH; ++c) done[c] = false;
     int64_t base = tile - 1;                 // lanes read base - lane
     while (true) {
         const int64_t idx = base - lane;
-        int64_t v = 0, f = 2;                // before tile 0: an inclusive 0
-        if (idx >= 0) {
-            do { status_load(st, idx, &v, &f); } while (f == 0);
+        bool all = true;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            if (done[c]) continue;
+            int64_t v = 0, f = 2;            // before tile 0: an inclusive 0
+            if (idx >= 0) {
+                do { status_load(st + c * cstride, idx, &v, &f); } while (f == 0);
+            }
+            const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
+            const int stop = inc ? __ffs(inc) - 1 : 32;      // nearest inclusive prefix
+            prefix[c] += warp_sum<int64_t>(lane <= stop ? v : 0);
+            done[c] = inc != 0;
+            all = all && done[c];
         }
-        const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
-        const int stop = inc ? __ffs(inc) - 1 : 32;      // nearest inclusive prefix
-        int64_t part = lane <= stop ? v : 0;
-        part = warp_sum<int64_t>(part);
-        prefix += part;
-        if (inc) break;
+        if (all) break;
         base -= 32;
     }
-    if (lane == 0) status_store(st, tile, prefix + agg, 2);
-    return prefix;
+    if (lane == 0)
+        for (int c = 0; c < NCH; ++c) status_store(st + c * cstride, tile, prefix[c] + agg[c], 2);
 }
 
 // ---------------------------------------------------------------- owners
@@ -114,31 +124,250 @@ __global__ void k_tile_owners(const int64_t *ptr, int64_t T, int64_t E, int64_t 
 }
 
 // ---------------------------------------------------------------- events
+constexpr int LT_REC = 2816;            // period records staged per tile (else direct stores)
 struct EvSmem {
     int32_t ptr[LT_MAXO + 1];   // staged CSR offsets relative to the tile's first event
-    int64_t size[LT_MAXO];
-    int8_t kind[LT_MAXO];
+    union {
+        struct {                // during the walks
+            int64_t size[LT_MAXO];
+            int8_t kind[LT_MAXO];
+        };
+        struct {                // afterwards: the tile's period records, tile-local order
+            int32_t tensor[LT_REC];
+            int32_t start[LT_REC];
+            int32_t end[LT_REC];
+            int8_t wraps[LT_REC];
+        } rec;
+    };
     int64_t scan[40];
     int64_t prefix;
     int64_t tile;
 };
 
+// One event tile: stage the tile's tensors, one walk over each thread's
+// events (validation, atomics, period count and a bitmask of the events that
+// open a period), tile prefix by decoupled look-back, then the period records.
+__device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, EvSmem &sm, int64_t tile,
+                                                         int64_t NTe, int64_t *est, const int64_t *owner) {
+    const int64_t T = a.T, E = a.E;
+    const int32_t N = (int32_t)a.N;
+    unsigned long long flags = 0;
+    const int64_t e0 = tile * LT_TILE, e1 = (e0 + LT_TILE < E) ? e0 + LT_TILE : E;
+    const int64_t o0 = __ldcg(reinterpret_cast<const long long *>(owner + tile));
+    int64_t o1 = __ldcg(reinterpret_cast<const long long *>(owner + tile + 1));
+    if (o1 < o0) o1 = o0;
+    const int64_t no = o1 - o0 + 1;
+    // more staged tensors than events can only come from empty tensors (an
+    // invalid trace, flagged by the tensor-table checks): skip the tile
+    const bool staged = no <= LT_MAXO;
+    if (staged) {
+        for (int64_t i = threadIdx.x; i <= no; i += blockDim.x) {
+            const int64_t p = (o0 + i <= T) ? __ldg(a.ptr + o0 + i) : E;
+            sm.ptr[i] = (int32_t)(p - e0 < INT32_MIN ? INT32_MIN : (p - e0 > INT32_MAX ? INT32_MAX : p - e0));
+        }
+        for (int64_t i = threadIdx.x; i < no; i += blockDim.x) {
+            sm.size[i] = __ldg(a.size + o0 + i);
+            sm.kind[i] = __ldg(a.kind + o0 + i);
+        }
+    }
+    // this thread's events (vector loads; the tile start is 64-byte aligned)
+    const int32_t frel = (int32_t)threadIdx.x * LT_EPT;        // tile-relative first event
+    const int64_t f = e0 + frel;
+    int32_t k[LT_EPT + 1];
+    if (f + LT_EPT <= E && ((uintptr_t)a.acc & 15) == 0) {
+        const int4 *q = reinterpret_cast<const int4 *>(a.acc + f);
+#pragma unroll
+        for (int j = 0; j < LT_EPT / 4; ++j) {
+            const int4 v = __ldg(q + j);
+            k[4 * j] = v.x; k[4 * j + 1] = v.y; k[4 * j + 2] = v.z; k[4 * j + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) k[j] = f + j < E ? __ldg(a.acc + f + j) : 0;
+    }
+    k[LT_EPT] = f + LT_EPT < E ? __ldg(a.acc + f + LT_EPT) : 0;
+    __syncthreads();
+
+    const int nev = (!staged || f >= e1) ? 0 : (int)(e1 - f < LT_EPT ? e1 - f : LT_EPT);
+    // owner of the first event: largest staged i with ptr <= frel
+    int32_t own0 = 0;
+    if (nev > 0) {
+        if (sm.ptr[0] > frel) { flags |= LF_BAD_PTR; }
+        int lo = 0, hi = (int)no;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (sm.ptr[mid] <= frel) lo = mid; else hi = mid;
+        }
+        own0 = lo;
+    }
+    const int nv = (flags & LF_BAD_PTR) ? 0 : nev;
+
+    // ---- walk 1: validation, period count, masks
+    int64_t cnt = 0;
+    uint32_t pmask = 0;                      // bit j: event j opens a period
+    uint32_t fmask = 0;                      // bit j: event j is its tensor's first access
+    {
+        int32_t own = own0, beg = sm.ptr[own0], nxt = sm.ptr[own0 + 1];
+        int8_t kd = sm.kind[own0];
+        int32_t firstk = 0;                  // first access of `own` if it lies in this run
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) {
+            if (j >= nv) break;
+            const int32_t e = frel + j;
+            while (e >= nxt && own + 1 < no) { ++own; beg = nxt; nxt = sm.ptr[own + 1]; kd = sm.kind[own]; }
+            const int32_t kk = k[j];
+            if (e == beg) { fmask |= 1u << j; firstk = kk; }
+            if ((uint32_t)kk >= (uint32_t)N) { flags |= LF_ACCESS_RANGE; continue; }
+            if (e != nxt - 1) {
+                const int32_t k2 = k[j + 1];
+                if (k2 <= kk) flags |= LF_NOT_INCREASING;
+                else if (k2 - kk > 1) { pmask |= 1u << j; ++cnt; }
+            } else if (kd == 1) {
+                const int32_t fk = beg >= frel ? firstk : __ldg(a.acc + e0 + beg);
+                if ((N - 1 - kk) + fk > 0) { pmask |= 1u << j; ++cnt; }
+            }
+        }
+    }
+    // tile-local offsets; the aggregate goes out before the atomics so the
+    // successors' look-backs only wait for this counting walk
+    int64_t tot;
+    const int64_t loc = block_exclusive_sum<int64_t>(cnt, sm.scan, &tot);
+#ifndef LT_EXP_NOLB
+    if (threadIdx.x < 32) lookback_publish(est, tile, tot);
+#endif
+
+    // ---- walk 2: per-kernel active bytes and the timeline difference array
+#ifndef LT_EXP_NORED
+    if (!(flags & LF_ACCESS_RANGE)) {
+        int32_t own = own0, beg = sm.ptr[own0], nxt = sm.ptr[own0 + 1];
+        int64_t sz = sm.size[own0];
+        int8_t kd = sm.kind[own0];
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) {
+            if (j >= nv) break;
+            const int32_t e = frel + j;
+            while (e >= nxt && own + 1 < no) { ++own; beg = nxt; nxt = sm.ptr[own + 1]; sz = sm.size[own]; kd = sm.kind[own]; }
+            const int32_t kk = k[j];
+            atomic_add_i64(&a.active[kk], sz);                     // per_kernel_active_bytes (:111-117)
+            if (kd == 0) {                                         // compute_memory_timeline (:97-108)
+                if (e == beg) atomic_add_i64(&a.diff[kk], sz);
+                if (e == nxt - 1) atomic_add_i64(&a.diff[kk + 1], -sz);
+            }
+        }
+    }
+#endif
+    __syncthreads();                         // sizes / kinds no longer needed: records reuse them
+
+    // ---- walk 3: period records in reference order (analysis.py:68-82:
+    // tensor order, gaps ascending, wrap last), staged at tile-local offsets
+    const bool staged_rec = tot <= LT_REC;
+#ifdef LT_EXP_NOREC
+    pmask = 0;
+#endif
+    if (staged_rec && pmask && flags == 0) {
+        int32_t own = own0, beg = sm.ptr[own0], nxt = sm.ptr[own0 + 1];
+        int32_t firstk = 0;
+        int32_t o = (int32_t)loc;
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) {
+            if (j >= nv) break;
+            const int32_t e = frel + j;
+            while (e >= nxt && own + 1 < no) { ++own; beg = nxt; nxt = sm.ptr[own + 1]; }
+            const int32_t kk = k[j];
+            if (e == beg) firstk = kk;
+            if (pmask & (1u << j)) {
+                if (e != nxt - 1) {
+                    sm.rec.start[o] = kk + 1; sm.rec.end[o] = k[j + 1] - 1; sm.rec.wraps[o] = 0;
+                } else {
+                    const int32_t fk = beg >= frel ? firstk : __ldg(a.acc + e0 + beg);
+                    sm.rec.start[o] = (kk + 1) % N; sm.rec.end[o] = ((fk - 1) % N + N) % N; sm.rec.wraps[o] = 1;
+                }
+                sm.rec.tensor[o] = own;
+                ++o;
+            }
+        }
+    }
+
+    // ---- tile prefix
+    if (threadIdx.x < 32) {
+#ifndef LT_EXP_NOLB
+        int64_t pre;
+        lookback_resolve<1>(est, 0, tile, &tot, &pre);
+#else
+        int64_t pre = tile * (LT_TILE / 2);
+#endif
+        if (threadIdx.x == 0) sm.prefix = pre;
+    }
+    __syncthreads();
+    const int64_t prefix = sm.prefix;
+    if (tile == NTe - 1 && threadIdx.x == 0) {
+        a.tensor_pptr[T] = prefix + tot;
+        a.scalars[SC_NUM_PERIODS] = prefix + tot;
+    }
+    if (flags != 0) return flags;
+    // per-tensor period offsets
+    if (fmask) {
+        int32_t own = own0, nxt = sm.ptr[own0 + 1];
+        int64_t o = prefix + loc;
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) {
+            if (j >= nv) break;
+            const int32_t e = frel + j;
+            while (e >= nxt && own + 1 < no) { ++own; nxt = sm.ptr[own + 1]; }
+            if (fmask & (1u << j)) a.tensor_pptr[o0 + own] = o;
+            if (pmask & (1u << j)) ++o;
+        }
+    }
+    if (staged_rec) {
+        // coalesced copy of the staged records
+        for (int64_t i = threadIdx.x; i < tot; i += blockDim.x) {
+            const int64_t g = prefix + i;
+            a.p_tensor[g] = o0 + sm.rec.tensor[i];
+            a.p_start[g] = sm.rec.start[i];
+            a.p_end[g] = sm.rec.end[i];
+            a.p_wraps[g] = sm.rec.wraps[i];
+        }
+    } else if (pmask) {
+        // more periods than the staging area: direct stores
+        int32_t own = own0, beg = sm.ptr[own0], nxt = sm.ptr[own0 + 1];
+        int32_t firstk = 0;
+        int64_t o = prefix + loc;
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) {
+            if (j >= nv) break;
+            const int32_t e = frel + j;
+            while (e >= nxt && own + 1 < no) { ++own; beg = nxt; nxt = sm.ptr[own + 1]; }
+            const int32_t kk = k[j];
+            if (e == beg) firstk = kk;
+            if (pmask & (1u << j)) {
+                int32_t ps, pe;
+                int8_t w;
+                if (e != nxt - 1) { ps = kk + 1; pe = k[j + 1] - 1; w = 0; }
+                else {
+                    const int32_t fk = beg >= frel ? firstk : __ldg(a.acc + e0 + beg);
+                    ps = (kk + 1) % N; pe = ((fk - 1) % N + N) % N; w = 1;
+                }
+                a.p_tensor[o] = o0 + own; a.p_start[o] = ps; a.p_end[o] = pe; a.p_wraps[o] = w;
+                ++o;
+            }
+        }
+    }
+    return flags;
+}
+
 __global__ void __launch_bounds__(LIFETIME_THREADS)
 k_events(LifetimeArgs a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     EvSmem &sm = *reinterpret_cast<EvSmem *>(smraw);
-    const int64_t N = a.N, T = a.T, E = a.E;
+    const int64_t T = a.T, E = a.E;
     const int64_t NTe = lifetime_event_tiles(E);
-    int64_t *counter = a.work;
-    const int64_t *owner = a.work + 2;
-    int64_t *est = a.work + 2 + owners_len(NTe);
-    unsigned long long flags = 0;
-
-    if (threadIdx.x == 0) sm.tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+    if (threadIdx.x == 0) sm.tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(a.work), 1ull);
     __syncthreads();
     const int64_t tile = sm.tile;
+    unsigned long long flags = 0;
+    if (tile < NTe) flags = event_tile(a, sm, tile, NTe, a.work + 2 + owners_len(NTe), a.work + 2);
 
-    // ---- tensor-table slice: CSR / size / kind / id order, global bytes
+    // ---- a slice of the tensor table: CSR / size / kind / id order, global bytes
     {
         const int64_t per = (T + gridDim.x - 1) / gridDim.x;
         const int64_t i0 = tile * per, i1 = i0 + per < T ? i0 + per : T;
@@ -156,167 +385,25 @@ k_events(LifetimeArgs a) {
         const int64_t g = block_sum<int64_t>(glob, sm.scan);
         if (threadIdx.x == 0 && g) atomic_add_i64(&a.scalars[SC_GLOBAL_BYTES], g);
     }
-    if (tile >= NTe) {
-        if (flags) atomicOr(reinterpret_cast<unsigned long long *>(&a.scalars[SC_FLAGS]), flags);
-        return;
-    }
-
-    // ---- stage the tile: its tensors' offsets, sizes, kinds
-    const int64_t e0 = tile * LT_TILE, e1 = (e0 + LT_TILE < E) ? e0 + LT_TILE : E;
-    const int64_t o0 = __ldcg(reinterpret_cast<const long long *>(owner + tile));
-    int64_t o1 = __ldcg(reinterpret_cast<const long long *>(owner + tile + 1));
-    if (o1 < o0) o1 = o0;
-    int64_t no = o1 - o0 + 1;
-    if (no > LT_MAXO) no = LT_MAXO;        // only with empty tensors (invalid; global fallback)
-    for (int64_t i = threadIdx.x; i <= no; i += blockDim.x) {
-        const int64_t p = (o0 + i <= T) ? __ldg(a.ptr + o0 + i) : E;
-        sm.ptr[i] = (int32_t)(p - e0 < INT32_MIN ? INT32_MIN : (p - e0 > INT32_MAX ? INT32_MAX : p - e0));
-    }
-    for (int64_t i = threadIdx.x; i < no; i += blockDim.x) {
-        sm.size[i] = __ldg(a.size + o0 + i);
-        sm.kind[i] = __ldg(a.kind + o0 + i);
-    }
-    // ---- this thread's events (vector loads; the tile start is 64-byte aligned)
-    const int64_t f = e0 + (int64_t)threadIdx.x * LT_EPT;
-    int32_t k[LT_EPT + 1];
-    if (f + LT_EPT <= E && ((uintptr_t)a.acc & 15) == 0) {
-        const int4 *q = reinterpret_cast<const int4 *>(a.acc + f);
-#pragma unroll
-        for (int j = 0; j < LT_EPT / 4; ++j) {
-            const int4 v = __ldg(q + j);
-            k[4 * j] = v.x; k[4 * j + 1] = v.y; k[4 * j + 2] = v.z; k[4 * j + 3] = v.w;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) k[j] = f + j < E ? __ldg(a.acc + f + j) : 0;
-    }
-    k[LT_EPT] = f + LT_EPT < E ? __ldg(a.acc + f + LT_EPT) : 0;
-    __syncthreads();
-
-    auto ptr_of = [&](int64_t i) -> int64_t {     // CSR offset of tensor i
-        const int64_t r = i - o0;
-        if (r >= 0 && r <= no) return e0 + sm.ptr[r];
-        return i <= T ? __ldg(a.ptr + i) : E;
-    };
-    auto size_of = [&](int64_t i) -> int64_t {
-        const int64_t r = i - o0;
-        return (r >= 0 && r < no) ? sm.size[r] : __ldg(a.size + i);
-    };
-    auto kind_of = [&](int64_t i) -> int8_t {
-        const int64_t r = i - o0;
-        return (r >= 0 && r < no) ? sm.kind[r] : __ldg(a.kind + i);
-    };
-    // owner of the first event: largest staged i with ptr <= f
-    int64_t own0 = o0;
-    const int64_t nev = f < e1 ? (e1 - f < LT_EPT ? e1 - f : LT_EPT) : 0;
-    if (nev > 0) {
-        int lo = 0, hi = (int)no;                   // staged ptr[0 .. no]
-        const int32_t rel = (int32_t)(f - e0);
-        if (sm.ptr[0] <= rel) {
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (sm.ptr[mid] <= rel) lo = mid; else hi = mid;
-            }
-            own0 = o0 + lo;
-        }
-        if (own0 >= T) own0 = T - 1;
-    }
-
-    // ---- pass 1: atomics, validation, period count
-    int64_t cnt = 0;
-    {
-        int64_t own = own0, beg = ptr_of(own0), nxt = ptr_of(own0 + 1);
-        int64_t firstk = 0;                       // first access of `own` if seen in this run
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) {
-            if (j >= nev) break;
-            const int64_t e = f + j;
-            while (e >= nxt && own + 1 < T) { ++own; beg = nxt; nxt = ptr_of(own + 1); }
-            const int64_t kk = k[j];
-            if (e == beg) firstk = kk;
-            if (kk < 0 || kk >= N) { flags |= LF_ACCESS_RANGE; continue; }
-            const int64_t sz = size_of(own);
-            const int8_t kd = kind_of(own);
-            atomic_add_i64(&a.active[kk], sz);
-            const bool last = e == nxt - 1;
-            if (!last) {
-                const int64_t k2 = k[j + 1];
-                if (k2 <= kk) flags |= LF_NOT_INCREASING;
-                else if (k2 - kk > 1) ++cnt;
-            } else if (kd == 1) {
-                const int64_t first = beg >= f ? firstk : __ldg(a.acc + beg);
-                if ((N - 1 - kk) + first > 0) ++cnt;
-            }
-            if (kd == 0) {
-                if (e == beg) atomic_add_i64(&a.diff[kk], sz);
-                if (last) atomic_add_i64(&a.diff[kk + 1], -sz);
-            }
-        }
-    }
     if (flags) atomicOr(reinterpret_cast<unsigned long long *>(&a.scalars[SC_FLAGS]), flags);
-
-    // ---- tile offset: block scan + decoupled look-back over tiles
-    int64_t tot;
-    int64_t out = block_exclusive_sum<int64_t>(cnt, sm.scan, &tot);
-    if (threadIdx.x < 32) {
-        const int64_t pre = lookback(est, tile, tot);
-        if (threadIdx.x == 0) sm.prefix = pre;
-    }
-    __syncthreads();
-    out += sm.prefix;
-    if (tile == NTe - 1 && threadIdx.x == 0) {
-        a.tensor_pptr[T] = sm.prefix + tot;
-        a.scalars[SC_NUM_PERIODS] = sm.prefix + tot;
-    }
-
-    // ---- pass 2: period records in reference order + per-tensor offsets
-    // (analysis.py:68-82: tensor order, gaps ascending, wrap last)
-    if (nev > 0 && flags == 0) {
-        int64_t own = own0, beg = ptr_of(own0), nxt = ptr_of(own0 + 1);
-        int64_t firstk = 0;
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) {
-            if (j >= nev) break;
-            const int64_t e = f + j;
-            while (e >= nxt && own + 1 < T) { ++own; beg = nxt; nxt = ptr_of(own + 1); }
-            const int64_t kk = k[j];
-            if (e == beg) { a.tensor_pptr[own] = out; firstk = kk; }
-            if (e != nxt - 1) {
-                const int64_t k2 = k[j + 1];
-                if (k2 - kk > 1) {
-                    a.p_tensor[out] = own; a.p_start[out] = (int32_t)(kk + 1);
-                    a.p_end[out] = (int32_t)(k2 - 1); a.p_wraps[out] = 0; ++out;
-                }
-            } else if (kind_of(own) == 1) {
-                const int64_t first = beg >= f ? firstk : __ldg(a.acc + beg);
-                if ((N - 1 - kk) + first > 0) {
-                    a.p_tensor[out] = own; a.p_start[out] = (int32_t)((kk + 1) % N);
-                    a.p_end[out] = (int32_t)(((first - 1) % N + N) % N);
-                    a.p_wraps[out] = 1; ++out;
-                }
-            }
-        }
-    }
 }
 
 // ---------------------------------------------------------------- kernels
-__global__ void __launch_bounds__(LIFETIME_THREADS)
+__global__ void __launch_bounds__(LIFETIME_THREADS, 4)
 k_kernels(LifetimeArgs a) {
     __shared__ int64_t scan[40];
     __shared__ int64_t s_pre[2];
     __shared__ int64_t s_tile;
     const int64_t N = a.N, E = a.E;
     const int64_t NTe = lifetime_event_tiles(E), NTk = lifetime_kernel_tiles(N);
-    int64_t *counter = a.work + 1;
-    int64_t *dst = a.work + 2 + owners_len(NTe) + 2 * NTe;
-    int64_t *fst = dst + 2 * NTk;
-    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(counter), 1ull);
+    int64_t *dst = a.work + 2 + owners_len(NTe) + 2 * NTe;     // dur chain, then diff chain (+2 NTk)
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(a.work + 1), 1ull);
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= NTk) return;
     const int64_t k0 = tile * KT_TILE + (int64_t)threadIdx.x * KT_EPT;
-    int64_t d[KT_EPT], df[KT_EPT];
     const bool vec = (((uintptr_t)a.dur | (uintptr_t)a.diff | (uintptr_t)a.starts | (uintptr_t)a.timeline) & 15) == 0;
+    int64_t d[KT_EPT], df[KT_EPT];
     if (k0 + KT_EPT <= N && vec) {
         const longlong2 *qd = reinterpret_cast<const longlong2 *>(a.dur + k0);
         const longlong2 *qf = reinterpret_cast<const longlong2 *>(a.diff + k0);
@@ -341,40 +428,44 @@ k_kernels(LifetimeArgs a) {
         sf += df[j];
     }
     if (flags) atomicOr(reinterpret_cast<unsigned long long *>(&a.scalars[SC_FLAGS]), flags);
-    int64_t td, tf;
-    int64_t xd = block_exclusive_sum<int64_t>(sd, scan, &td);
-    int64_t xf = block_exclusive_sum<int64_t>(sf, scan, &tf);
+    int64_t agg[2];
+    int64_t xd = block_exclusive_sum<int64_t>(sd, scan, &agg[0]);
+    int64_t xf = block_exclusive_sum<int64_t>(sf, scan, &agg[1]);
     if (threadIdx.x < 32) {
-        const int64_t pd = lookback(dst, tile, td);
-        const int64_t pf = lookback(fst, tile, tf);
-        if (threadIdx.x == 0) { s_pre[0] = pd; s_pre[1] = pf; }
+        lookback_publish(dst, tile, agg[0]);
+        lookback_publish(dst + 2 * NTk, tile, agg[1]);
+        int64_t pre[2];
+        lookback_resolve<2>(dst, 2 * NTk, tile, agg, pre);
+        if (threadIdx.x == 0) { s_pre[0] = pre[0]; s_pre[1] = pre[1]; }
     }
     __syncthreads();
     xd += s_pre[0];
     xf += s_pre[1] + __ldcg(reinterpret_cast<const long long *>(&a.scalars[SC_GLOBAL_BYTES]));
-    int64_t so[KT_EPT], to[KT_EPT];
-#pragma unroll
-    for (int j = 0; j < KT_EPT; ++j) {
-        so[j] = xd; xd += d[j];
-        xf += df[j]; to[j] = xf;
-    }
     if (k0 + KT_EPT <= N && vec) {
         longlong2 *ps = reinterpret_cast<longlong2 *>(a.starts + k0);
         longlong2 *pt = reinterpret_cast<longlong2 *>(a.timeline + k0);
         longlong2 *pz = reinterpret_cast<longlong2 *>(a.diff + k0);
 #pragma unroll
         for (int j = 0; j < KT_EPT / 2; ++j) {
-            ps[j] = make_longlong2(so[2 * j], so[2 * j + 1]);
-            pt[j] = make_longlong2(to[2 * j], to[2 * j + 1]);
+            const int64_t s0 = xd, s1 = xd + d[2 * j];
+            xd = s1 + d[2 * j + 1];
+            const int64_t t0 = xf + df[2 * j], t1 = t0 + df[2 * j + 1];
+            xf = t1;
+            ps[j] = make_longlong2(s0, s1);
+            pt[j] = make_longlong2(t0, t1);
             pz[j] = make_longlong2(0, 0);                      // ready for the next call
         }
     } else {
 #pragma unroll
         for (int j = 0; j < KT_EPT; ++j)
-            if (k0 + j < N) { a.starts[k0 + j] = so[j]; a.timeline[k0 + j] = to[j]; a.diff[k0 + j] = 0; }
+            if (k0 + j < N) {
+                a.starts[k0 + j] = xd; xd += d[j];
+                xf += df[j]; a.timeline[k0 + j] = xf;
+                a.diff[k0 + j] = 0;
+            }
     }
     if (tile == NTk - 1 && threadIdx.x == blockDim.x - 1) {
-        a.starts[N] = s_pre[0] + td;
+        a.starts[N] = s_pre[0] + agg[0];
         a.diff[N] = 0;
     }
 }

@@ -1,6 +1,6 @@
 """Attribute ncu warp-stall samples of a kernel to CUDA source lines.
 
-    python tools/ncu_lines.py <report.ncu-rep> <libtio.so> <mangled kernel> [top]
+    python tools/ncu_lines.py <report.ncu-rep> <libtio.so> <mangled kernel> [top] [kernel regex]
 
 ncu's SASS source page gives per-instruction stall samples with absolute
 addresses; nvdisasm -g on the cubin extracted from libtio.so (compiled with
@@ -18,9 +18,11 @@ import sys
 import tempfile
 
 
-def sass_samples(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
-                         capture_output=True, text=True).stdout
+def sass_samples(rep, kernel=None):
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"]
+    if kernel:
+        cmd += ["-k", f"regex:{kernel}"]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
     h = rows[hdr]
@@ -55,7 +57,7 @@ def line_map(so, func):
 def main():
     rep, so, func = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    samples = sass_samples(rep)
+    samples = sass_samples(rep, sys.argv[5] if len(sys.argv) > 5 else None)
     lm = line_map(so, func)
     agg = collections.Counter()
     for off, n in samples:
