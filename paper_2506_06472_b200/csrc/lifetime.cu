@@ -36,7 +36,7 @@ enum : unsigned long long {
     LF_NOT_INCREASING = 16, LF_BAD_KIND = 32
 };
 
-constexpr int LT_EPT = 16;                          // events per thread
+constexpr int LT_EPT = 8;                           // events per thread
 constexpr int LT_TILE = LIFETIME_THREADS * LT_EPT;  // events per tile
 constexpr int LT_MAXO = LT_TILE + 2;                // staged tensors per tile
 constexpr int KT_EPT = 8;                           // kernels per thread
@@ -124,35 +124,71 @@ __global__ void k_tile_owners(const int64_t *ptr, int64_t T, int64_t E, int64_t 
 }
 
 // ---------------------------------------------------------------- events
-constexpr int LT_REC = 2816;            // period records staged per tile (else direct stores)
 struct EvSmem {
+    alignas(16) int32_t acc[LT_TILE + 4];   // the tile's accesses (+ the next tile's first); first: 16-byte aligned
     int32_t ptr[LT_MAXO + 1];   // staged CSR offsets relative to the tile's first event
+    int16_t own[LT_TILE];       // staged owner index of every event of the tile
     union {
         struct {                // during the walks
             int64_t size[LT_MAXO];
             int8_t kind[LT_MAXO];
         };
         struct {                // afterwards: the tile's period records, tile-local order
-            int32_t tensor[LT_REC];
-            int32_t start[LT_REC];
-            int32_t end[LT_REC];
-            int8_t wraps[LT_REC];
+            int32_t start[LT_TILE];
+            int32_t end[LT_TILE];
+            int16_t tensor[LT_TILE];
+            int8_t wraps[LT_TILE];
         } rec;
     };
+    int32_t scan32[40];
     int64_t scan[40];
     int64_t prefix;
     int64_t tile;
 };
 
-// One event tile: stage the tile's tensors, one walk over each thread's
-// events (validation, atomics, period count and a bitmask of the events that
-// open a period), tile prefix by decoupled look-back, then the period records.
+// exclusive block max-scan of int32 (-1 identity), all threads
+__device__ __forceinline__ int32_t block_exclusive_max(int32_t v, int32_t *sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t n = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o && n > inc) inc = n;
+    }
+    if (lane == 31) sm[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t w = lane < nw ? sm[lane] : -1;
+        int32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t n = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o && n > wi) wi = n;
+        }
+        const int32_t ex = __shfl_up_sync(0xffffffffu, wi, 1);
+        if (lane < nw) sm[lane] = lane == 0 ? -1 : ex;
+    }
+    __syncthreads();
+    int32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) ex = -1;
+    const int32_t r = sm[warp] > ex ? sm[warp] : ex;
+    __syncthreads();
+    return r;
+}
+
+// One event tile.  Staging: the tile's tensors (CSR offsets, sizes, kinds)
+// and accesses in shared memory, and an owner map (tensor heads, then a
+// block max-scan).  Walks over each thread's LT_EPT consecutive events:
+// (1) validation, period count, masks; (2) the atomics; (3) period records
+// in shared memory at tile-local offsets.  The tile prefix comes from a
+// decoupled look-back; records are then stored coalesced.
 __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, EvSmem &sm, int64_t tile,
                                                          int64_t NTe, int64_t *est, const int64_t *owner) {
     const int64_t T = a.T, E = a.E;
     const int32_t N = (int32_t)a.N;
     unsigned long long flags = 0;
     const int64_t e0 = tile * LT_TILE, e1 = (e0 + LT_TILE < E) ? e0 + LT_TILE : E;
+    const int32_t ne = (int32_t)(e1 - e0);
     const int64_t o0 = __ldcg(reinterpret_cast<const long long *>(owner + tile));
     int64_t o1 = __ldcg(reinterpret_cast<const long long *>(owner + tile + 1));
     if (o1 < o0) o1 = o0;
@@ -160,6 +196,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     // more staged tensors than events can only come from empty tensors (an
     // invalid trace, flagged by the tensor-table checks): skip the tile
     const bool staged = no <= LT_MAXO;
+    for (int i = threadIdx.x; i < LT_TILE; i += blockDim.x) sm.own[i] = i == 0 ? 0 : -1;   // o0 starts at or before the tile
     if (staged) {
         for (int64_t i = threadIdx.x; i <= no; i += blockDim.x) {
             const int64_t p = (o0 + i <= T) ? __ldg(a.ptr + o0 + i) : E;
@@ -170,62 +207,61 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
             sm.kind[i] = __ldg(a.kind + o0 + i);
         }
     }
-    // this thread's events (vector loads; the tile start is 64-byte aligned)
-    const int32_t frel = (int32_t)threadIdx.x * LT_EPT;        // tile-relative first event
-    const int64_t f = e0 + frel;
-    int32_t k[LT_EPT + 1];
-    if (f + LT_EPT <= E && ((uintptr_t)a.acc & 15) == 0) {
-        const int4 *q = reinterpret_cast<const int4 *>(a.acc + f);
-#pragma unroll
-        for (int j = 0; j < LT_EPT / 4; ++j) {
-            const int4 v = __ldg(q + j);
-            k[4 * j] = v.x; k[4 * j + 1] = v.y; k[4 * j + 2] = v.z; k[4 * j + 3] = v.w;
-        }
+    if (((uintptr_t)a.acc & 15) == 0 && ne == LT_TILE) {
+        const int4 *q = reinterpret_cast<const int4 *>(a.acc + e0);
+        for (int i = threadIdx.x; i < LT_TILE / 4; i += blockDim.x)
+            reinterpret_cast<int4 *>(sm.acc)[i] = __ldg(q + i);
     } else {
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) k[j] = f + j < E ? __ldg(a.acc + f + j) : 0;
+        for (int i = threadIdx.x; i < ne; i += blockDim.x) sm.acc[i] = __ldg(a.acc + e0 + i);
     }
-    k[LT_EPT] = f + LT_EPT < E ? __ldg(a.acc + f + LT_EPT) : 0;
+    if (threadIdx.x == 0) sm.acc[ne] = e1 < E ? __ldg(a.acc + e1) : 0;
     __syncthreads();
-
-    const int nev = (!staged || f >= e1) ? 0 : (int)(e1 - f < LT_EPT ? e1 - f : LT_EPT);
-    // owner of the first event: largest staged i with ptr <= frel
-    int32_t own0 = 0;
-    if (nev > 0) {
-        if (sm.ptr[0] > frel) { flags |= LF_BAD_PTR; }
-        int lo = 0, hi = (int)no;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (sm.ptr[mid] <= frel) lo = mid; else hi = mid;
+    // owner map: tensor heads inside the tile, then a running max
+    if (staged)
+        for (int64_t i = threadIdx.x; i < no; i += blockDim.x) {
+            const int32_t r = sm.ptr[i];
+            if (r >= 0 && r < ne) sm.own[r] = (int16_t)i;
         }
-        own0 = lo;
+    __syncthreads();
+    const int32_t frel = (int32_t)threadIdx.x * LT_EPT;           // tile-relative first event
+    const int nv = (!staged || frel >= ne) ? 0 : (ne - frel < LT_EPT ? ne - frel : LT_EPT);
+    int32_t own[LT_EPT];
+    {
+        int32_t run = -1;
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) {
+            const int32_t v = frel + j < LT_TILE ? sm.own[frel + j] : -1;
+            run = v > run ? v : run;
+            own[j] = run;
+        }
+        const int32_t ex = block_exclusive_max(run, sm.scan32);
+#pragma unroll
+        for (int j = 0; j < LT_EPT; ++j) own[j] = own[j] > ex ? own[j] : ex;
     }
-    const int nv = (flags & LF_BAD_PTR) ? 0 : nev;
+    int32_t k[LT_EPT + 1];
+#pragma unroll
+    for (int j = 0; j <= LT_EPT; ++j) k[j] = frel + j <= ne ? sm.acc[frel + j] : 0;
 
     // ---- walk 1: validation, period count, masks
     int64_t cnt = 0;
     uint32_t pmask = 0;                      // bit j: event j opens a period
     uint32_t fmask = 0;                      // bit j: event j is its tensor's first access
-    {
-        int32_t own = own0, beg = sm.ptr[own0], nxt = sm.ptr[own0 + 1];
-        int8_t kd = sm.kind[own0];
-        int32_t firstk = 0;                  // first access of `own` if it lies in this run
 #pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) {
-            if (j >= nv) break;
-            const int32_t e = frel + j;
-            while (e >= nxt && own + 1 < no) { ++own; beg = nxt; nxt = sm.ptr[own + 1]; kd = sm.kind[own]; }
-            const int32_t kk = k[j];
-            if (e == beg) { fmask |= 1u << j; firstk = kk; }
-            if ((uint32_t)kk >= (uint32_t)N) { flags |= LF_ACCESS_RANGE; continue; }
-            if (e != nxt - 1) {
-                const int32_t k2 = k[j + 1];
-                if (k2 <= kk) flags |= LF_NOT_INCREASING;
-                else if (k2 - kk > 1) { pmask |= 1u << j; ++cnt; }
-            } else if (kd == 1) {
-                const int32_t fk = beg >= frel ? firstk : __ldg(a.acc + e0 + beg);
-                if ((N - 1 - kk) + fk > 0) { pmask |= 1u << j; ++cnt; }
-            }
+    for (int j = 0; j < LT_EPT; ++j) {
+        if (j >= nv) break;
+        const int32_t e = frel + j, o = own[j];
+        const int32_t beg = sm.ptr[o], nxt = sm.ptr[o + 1];
+        const int32_t kk = k[j];
+        if (e == beg) fmask |= 1u << j;
+        if (e < beg || e >= nxt) { flags |= LF_BAD_PTR; continue; }
+        if ((uint32_t)kk >= (uint32_t)N) { flags |= LF_ACCESS_RANGE; continue; }
+        if (e != nxt - 1) {
+            const int32_t k2 = k[j + 1];
+            if (k2 <= kk) flags |= LF_NOT_INCREASING;
+            else if (k2 - kk > 1) { pmask |= 1u << j; ++cnt; }
+        } else if (sm.kind[o] == 1) {
+            const int32_t fk = beg >= 0 ? sm.acc[beg] : __ldg(a.acc + e0 + beg);
+            if ((N - 1 - kk) + fk > 0) { pmask |= 1u << j; ++cnt; }
         }
     }
     // tile-local offsets; the aggregate goes out before the atomics so the
@@ -238,20 +274,17 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
 
     // ---- walk 2: per-kernel active bytes and the timeline difference array
 #ifndef LT_EXP_NORED
-    if (!(flags & LF_ACCESS_RANGE)) {
-        int32_t own = own0, beg = sm.ptr[own0], nxt = sm.ptr[own0 + 1];
-        int64_t sz = sm.size[own0];
-        int8_t kd = sm.kind[own0];
+    if (!(flags & (LF_ACCESS_RANGE | LF_BAD_PTR))) {
 #pragma unroll
         for (int j = 0; j < LT_EPT; ++j) {
             if (j >= nv) break;
-            const int32_t e = frel + j;
-            while (e >= nxt && own + 1 < no) { ++own; beg = nxt; nxt = sm.ptr[own + 1]; sz = sm.size[own]; kd = sm.kind[own]; }
+            const int32_t e = frel + j, o = own[j];
             const int32_t kk = k[j];
+            const int64_t sz = sm.size[o];
             atomic_add_i64(&a.active[kk], sz);                     // per_kernel_active_bytes (:111-117)
-            if (kd == 0) {                                         // compute_memory_timeline (:97-108)
-                if (e == beg) atomic_add_i64(&a.diff[kk], sz);
-                if (e == nxt - 1) atomic_add_i64(&a.diff[kk + 1], -sz);
+            if (sm.kind[o] == 0) {                                 // compute_memory_timeline (:97-108)
+                if (e == sm.ptr[o]) atomic_add_i64(&a.diff[kk], sz);
+                if (e == sm.ptr[o + 1] - 1) atomic_add_i64(&a.diff[kk + 1], -sz);
             }
         }
     }
@@ -259,32 +292,26 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     __syncthreads();                         // sizes / kinds no longer needed: records reuse them
 
     // ---- walk 3: period records in reference order (analysis.py:68-82:
-    // tensor order, gaps ascending, wrap last), staged at tile-local offsets
-    const bool staged_rec = tot <= LT_REC;
+    // tensor order, gaps ascending, wrap last) at tile-local offsets
 #ifdef LT_EXP_NOREC
     pmask = 0;
 #endif
-    if (staged_rec && pmask && flags == 0) {
-        int32_t own = own0, beg = sm.ptr[own0], nxt = sm.ptr[own0 + 1];
-        int32_t firstk = 0;
-        int32_t o = (int32_t)loc;
+    if (pmask && flags == 0) {
+        int32_t q = (int32_t)loc;
 #pragma unroll
         for (int j = 0; j < LT_EPT; ++j) {
-            if (j >= nv) break;
-            const int32_t e = frel + j;
-            while (e >= nxt && own + 1 < no) { ++own; beg = nxt; nxt = sm.ptr[own + 1]; }
+            if (!(pmask & (1u << j))) continue;
+            const int32_t e = frel + j, o = own[j];
             const int32_t kk = k[j];
-            if (e == beg) firstk = kk;
-            if (pmask & (1u << j)) {
-                if (e != nxt - 1) {
-                    sm.rec.start[o] = kk + 1; sm.rec.end[o] = k[j + 1] - 1; sm.rec.wraps[o] = 0;
-                } else {
-                    const int32_t fk = beg >= frel ? firstk : __ldg(a.acc + e0 + beg);
-                    sm.rec.start[o] = (kk + 1) % N; sm.rec.end[o] = ((fk - 1) % N + N) % N; sm.rec.wraps[o] = 1;
-                }
-                sm.rec.tensor[o] = own;
-                ++o;
+            if (e != sm.ptr[o + 1] - 1) {
+                sm.rec.start[q] = kk + 1; sm.rec.end[q] = k[j + 1] - 1; sm.rec.wraps[q] = 0;
+            } else {
+                const int32_t beg = sm.ptr[o];
+                const int32_t fk = beg >= 0 ? sm.acc[beg] : __ldg(a.acc + e0 + beg);
+                sm.rec.start[q] = (kk + 1) % N; sm.rec.end[q] = ((fk - 1) % N + N) % N; sm.rec.wraps[q] = 1;
             }
+            sm.rec.tensor[q] = (int16_t)o;
+            ++q;
         }
     }
 
@@ -304,53 +331,24 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
         a.tensor_pptr[T] = prefix + tot;
         a.scalars[SC_NUM_PERIODS] = prefix + tot;
     }
-    if (flags != 0) return flags;
+    const bool ok = __syncthreads_or(flags != 0) == 0;
+    if (!ok) return flags;
     // per-tensor period offsets
     if (fmask) {
-        int32_t own = own0, nxt = sm.ptr[own0 + 1];
-        int64_t o = prefix + loc;
+        int64_t q = prefix + loc;
 #pragma unroll
         for (int j = 0; j < LT_EPT; ++j) {
-            if (j >= nv) break;
-            const int32_t e = frel + j;
-            while (e >= nxt && own + 1 < no) { ++own; nxt = sm.ptr[own + 1]; }
-            if (fmask & (1u << j)) a.tensor_pptr[o0 + own] = o;
-            if (pmask & (1u << j)) ++o;
+            if (fmask & (1u << j)) a.tensor_pptr[o0 + own[j]] = q;
+            if (pmask & (1u << j)) ++q;
         }
     }
-    if (staged_rec) {
-        // coalesced copy of the staged records
-        for (int64_t i = threadIdx.x; i < tot; i += blockDim.x) {
-            const int64_t g = prefix + i;
-            a.p_tensor[g] = o0 + sm.rec.tensor[i];
-            a.p_start[g] = sm.rec.start[i];
-            a.p_end[g] = sm.rec.end[i];
-            a.p_wraps[g] = sm.rec.wraps[i];
-        }
-    } else if (pmask) {
-        // more periods than the staging area: direct stores
-        int32_t own = own0, beg = sm.ptr[own0], nxt = sm.ptr[own0 + 1];
-        int32_t firstk = 0;
-        int64_t o = prefix + loc;
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) {
-            if (j >= nv) break;
-            const int32_t e = frel + j;
-            while (e >= nxt && own + 1 < no) { ++own; beg = nxt; nxt = sm.ptr[own + 1]; }
-            const int32_t kk = k[j];
-            if (e == beg) firstk = kk;
-            if (pmask & (1u << j)) {
-                int32_t ps, pe;
-                int8_t w;
-                if (e != nxt - 1) { ps = kk + 1; pe = k[j + 1] - 1; w = 0; }
-                else {
-                    const int32_t fk = beg >= frel ? firstk : __ldg(a.acc + e0 + beg);
-                    ps = (kk + 1) % N; pe = ((fk - 1) % N + N) % N; w = 1;
-                }
-                a.p_tensor[o] = o0 + own; a.p_start[o] = ps; a.p_end[o] = pe; a.p_wraps[o] = w;
-                ++o;
-            }
-        }
+    // coalesced copy of the staged records
+    for (int64_t i = threadIdx.x; i < tot; i += blockDim.x) {
+        const int64_t g = prefix + i;
+        a.p_tensor[g] = o0 + sm.rec.tensor[i];
+        a.p_start[g] = sm.rec.start[i];
+        a.p_end[g] = sm.rec.end[i];
+        a.p_wraps[g] = sm.rec.wraps[i];
     }
     return flags;
 }
