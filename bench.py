@@ -1,10 +1,16 @@
 """Benchmark of the lifetime + plan hot path (BASELINE.json metric 1).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1|llama1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c2|c1|llama1] [--secondary c2|...|""]
 
 One step = one pass of the hot path over the trace: the lifetime stage
 (reference analysis.py:58-117) and the Algorithm-1 planner with entry sort
 and mark_urgent (planner.py:267-397) on a device-resident trace.
+
+Workloads: the headline line is config C3 (BASELINE.json configs[2]: the
+north star's 10M-event Llama-3-70B-shaped trace, which fits one B200); the
+same measurement on C2 (configs[1], 1M events) is reported under the "c2"
+key.  Both plans are bit-exact with the oracle fingerprints in tests/golden.
 
   value  = trace events / s = E / (device time of lifetime + plan), CUDA
            events on the libtio stream, L2 flushed (256 MiB write) before every
@@ -168,11 +174,13 @@ def run_reference(args, rank: int, world: int):
     rounds_total = args.ref_rounds_total
     vals = []
     for _ in range(args.warmup):
-        cpu_baseline(args.config, rounds_total, sample_rounds=args.ref_rounds)
+        cpu_baseline(args.config, rounds_total, sample_rounds=args.ref_rounds_c3
+                     if args.config == "c3" else args.ref_rounds)
     t0 = time.perf_counter()
     last = None
     for _ in range(args.steps):
-        last = cpu_baseline(args.config, rounds_total, sample_rounds=args.ref_rounds)
+        last = cpu_baseline(args.config, rounds_total, sample_rounds=args.ref_rounds_c3
+                            if args.config == "c3" else args.ref_rounds)
         vals.append(last["value"])
     wall = time.perf_counter() - t0
     v = statistics.mean(vals)
@@ -188,14 +196,13 @@ def run_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, rank: int, world: int, local_rank: int):
+def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) -> dict:
+    """Device-timed lifetime + plan on one config (see module docstring)."""
     import torch
     from paper_2506_06472_b200 import _native
     from paper_2506_06472_b200.planner import _rates_struct
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    tr, cap, rates, hc, desc = _trace(args.config)
+    tr, cap, rates, hc, desc = _trace(config)
     a = tr.arrays()
     N, T, E = a.num_kernels, a.num_tensors, a.num_events
     stream = torch.cuda.Stream(device=dev)
@@ -217,7 +224,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         return p
 
     with torch.cuda.stream(stream):
-        for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+        for _ in range(warmup):
             step().close()
         torch.cuda.synchronize()
         if world > 1:
@@ -225,8 +232,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         launches0 = _native.kernel_launches()
         tot_ms, life_ms, plan_ms, loop_ms = 0.0, 0.0, 0.0, 0.0
         info = None
-        with Clocks(local_rank) as clk:
-            for _ in range(args.steps):
+        plan_bytes = b""
+        with Clocks(dev.index) as clk:
+            for i in range(steps):
                 flush.fill_(1)          # L2 flush, outside the timed region
                 evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 p = step(evs)
@@ -236,11 +244,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 tot_ms += evs[0].elapsed_time(evs[2])
                 info = p.info
                 loop_ms += info.loop_ns / 1e6
-                plan_bytes = p.write() if _ == 0 else plan_bytes
+                if i == 0:
+                    plan_bytes = p.write()
                 p.close()
         launches = _native.kernel_launches() - launches0
         torch.cuda.synchronize()
-    # max over ranks
     t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -261,20 +269,21 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     pinfo = _native.PlanInfo()
     h2d = sum(int(v.numel() * v.element_size()) for v in pinned.values())
     d2h = ne * _native.ENTRY_DTYPE.itemsize
-    for _ in range(2):
+
+    def one_shot():
         _native.check(lib.tio_plan_host(ctypes.byref(desc_c), ctypes.c_int64(cap), ctypes.byref(r),
                                         ctypes.c_int64(hc), ctypes.c_void_p(sh), ctypes.byref(pinfo),
                                         ctypes.c_void_p(ent.data_ptr()), ctypes.c_int64(ne)))
+    for _ in range(2):
+        one_shot()
     e2e_ms = 0.0
-    for _ in range(args.steps):
+    for _ in range(steps):
         flush.fill_(1)
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        _native.check(lib.tio_plan_host(ctypes.byref(desc_c), ctypes.c_int64(cap), ctypes.byref(r),
-                                        ctypes.c_int64(hc), ctypes.c_void_p(sh), ctypes.byref(pinfo),
-                                        ctypes.c_void_p(ent.data_ptr()), ctypes.c_int64(ne)))
+        one_shot()
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms += e0.elapsed_time(e1)
@@ -283,11 +292,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     e2e_ms = float(t.item())
 
-    if rank != 0:
-        return
     import hashlib
-    K = args.steps
-    value = world * E * K / (tot_ms_max / 1e3)
+    K = steps
     P = int(info.num_candidates)
     B_L = _lifetime_bytes(N, T, E, P)
     life_s = life_ms / K / 1e3
@@ -298,14 +304,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if os.path.exists(tp):
         try:
             with open(tp) as f:
-                traffic = json.load(f).get(args.config)
+                traffic = json.load(f).get(config)
         except Exception:
             traffic = None
     rounds = int(info.rounds)
-    line = {
-        "metric": "trace events/s (lifetime+plan)", "value": value, "unit": "events/s", "n_gpus": world,
-        "steps": K, "warmup": args.warmup, "ms_per_step": tot_ms_max / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+    return {
+        "value": world * E * K / (tot_ms_max / 1e3), "ms_per_step": tot_ms_max / K,
         "config": {"workload": desc, "events": E, "kernels": N, "tensors": T, "periods": P,
                    "capacity": cap, "rates": "ssd 16000 B/us symmetric", "host_cap": hc,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
@@ -313,28 +317,56 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "plan_sha256": hashlib.sha256(plan_bytes).hexdigest()},
         "breakdown_ms": {"lifetime": life_ms / K, "plan": plan_ms / K, "plan_round_loop": loop_ms / K,
                          "plan_setup_epilogue_host": (plan_ms - loop_ms) / K},
-        "roofline": {"kernel": "lifetime_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "algorithmic_bytes": B_L, "share_of_step": life_ms / tot_ms},
+        "roofline": {"kernel": "lifetime (k_tile_owners + k_events + k_kernels)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": B_L,
+                     "share_of_step": life_ms / tot_ms},
         "planner": {"kernel": "plan_loop_kernel", "bound": "latency (2 grid barriers per round)",
                     "rounds": rounds, "commits": int(info.num_commits),
                     "us_per_round": (loop_ms / K) * 1e3 / max(1, rounds),
-                    **({"phase_us_per_round_block0": dict(zip(
-                        ["prologue", "evaluate", "block_reduce", "barrier1", "argmax", "channel_merge",
-                         "residual", "commit_barrier2"], [round(info.dbg[q] / 1e3 / max(1, rounds), 3)
-                                                          for q in range(8)])),
+                    "share_of_step": loop_ms / tot_ms,
+                    **({"debug_build": {
+                        "phase_us_per_round_block0": dict(zip(
+                            ["prologue", "evaluate", "block_reduce", "barrier1", "argmax", "channel_merge",
+                             "residual", "commit_barrier2"],
+                            [round(info.dbg[q] / 1e3 / max(1, rounds), 3) for q in range(8)])),
                         "dirty_tiles_per_round": info.dbg[8] / max(1, rounds),
-                        "refits_per_round": info.dbg[9] / max(1, rounds),
-                        "max_evaluate_us_per_round": info.dbg[10] / 1e3 / max(1, rounds)}
-                       if any(info.dbg[q] for q in range(14)) else {}),
-                    "share_of_step": loop_ms / tot_ms},
+                        "refits_per_round": info.dbg[9] / max(1, rounds)}}
+                       if any(info.dbg[q] for q in range(12)) else {})},
         "e2e": {"value": world * E * K / (e2e_ms / 1e3), "unit": "events/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "tio_plan_host (C ABI), pinned host buffers"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "rounds": rounds,
     }
+
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    warm = max(args.warmup, 3) if args.warmup >= 3 else args.warmup
+    m = measure(args.config, args.steps, warm, dev, rank, world)
+    extra = None
+    if args.secondary and args.secondary != args.config:
+        extra = measure(args.secondary, args.steps, warm, dev, rank, world)
+    if rank != 0:
+        return
+    rounds = m.pop("rounds")
+    line = {
+        "metric": "trace events/s (lifetime+plan)", "value": m.pop("value"), "unit": "events/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": m.pop("ms_per_step"), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic", **m,
+    }
+    if extra is not None:
+        extra.pop("clocks", None)
+        rx = extra.pop("rounds")
+        if not args.no_cpu_baseline:
+            extra["cpu_baseline"] = cpu_baseline(args.secondary, rx, sample_rounds=args.ref_rounds)
+        line[args.secondary] = extra
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.config, rounds, sample_rounds=args.ref_rounds)
+        line["cpu_baseline"] = cpu_baseline(args.config, rounds, sample_rounds=args.ref_rounds_c3
+                                            if args.config == "c3" else args.ref_rounds)
     if not args.no_migration and world == 1:
         # C4 on one GPU; at N > 1 the per-rank pinned host extents (24-78 GB
         # each) would exceed the box's host memory, so the leg runs at N = 1 only
@@ -389,11 +421,15 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "llama1"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "llama1"],
+                    help="headline workload (default C3: the north star's 10M-event trace)")
+    ap.add_argument("--secondary", default="c2", choices=["", "c1", "c2", "c3", "llama1"],
+                    help="second workload reported under its own key (default C2, BASELINE configs[1])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-migration", action="store_true", help="skip the C4 engine replay leg")
     ap.add_argument("--microbatches", type=int, default=4, help="C4 replay microbatches")
-    ap.add_argument("--ref-rounds", type=int, default=40, help="planner rounds in the CPU sample")
+    ap.add_argument("--ref-rounds", type=int, default=40, help="planner rounds in the CPU sample (C2)")
+    ap.add_argument("--ref-rounds-c3", type=int, default=12, help="planner rounds in the CPU sample (C3)")
     ap.add_argument("--ref-rounds-total", type=int, default=None,
                     help="total rounds of the full plan (for the reference arm's extrapolation)")
     args = ap.parse_args(argv)

@@ -449,6 +449,10 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     PTRY(A.alloc(&t_ka_lo, ntiles)); PTRY(A.alloc(&t_ka_hi, ntiles));
     PTRY(A.alloc(&t_kb_lo, ntiles)); PTRY(A.alloc(&t_kb_hi, ntiles));
     PTRY(A.alloc(&tile_best, ntiles));
+    PTRY(A.alloc(&a.vkey, P));
+    PTRY(A.alloc(&a.rq[0], P)); PTRY(A.alloc(&a.rq[1], P));
+    PTRY(A.alloc(&a.t_refit, ntiles));
+    PCUDA(cudaMemsetAsync(a.t_refit, 0xff, 4 * (size_t)(ntiles > 0 ? ntiles : 1), s));
     CandCols src{c_size, c_ready, c_deadline, c_d, c_tid, c_sk, c_ek, c_first, c_last, c_tpos, c_wraps, st};
     CandCols dst;
     PTRY(A.alloc(&dst.size, P)); PTRY(A.alloc(&dst.ready, P)); PTRY(A.alloc(&dst.deadline, P));

@@ -327,6 +327,18 @@ __device__ Key block_best(Key mine, Key *sm) {
     return r;
 }
 
+__device__ __forceinline__ Key kload(const Key *p) {
+    const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(p);
+    const ulonglong2 x = __ldcg(q), y = __ldcg(q + 1);
+    return Key{x.x, x.y, (int64_t)y.x, (int64_t)y.y};
+}
+
+__device__ __forceinline__ void kstore(Key *p, const Key &k) {
+    ulonglong2 *q = reinterpret_cast<ulonglong2 *>(p);
+    q[0] = make_ulonglong2(k.blo, k.bhi);
+    q[1] = make_ulonglong2((unsigned long long)k.cost, (unsigned long long)k.meta);
+}
+
 // ---------------------------------------------------------------- the kernel
 //
 // Tiles.  Candidates are grouped into tiles of TILE consecutive candidates in
@@ -383,7 +395,7 @@ plan_loop_kernel(PlanArgs a) {
     __shared__ int64_t s_win_tile;
     __shared__ int32_t s_dirty[PLAN_THREADS];
     __shared__ int32_t s_ndirty;
-    __shared__ int16_t s_refit[PLAN_THREADS];
+    __shared__ int16_t s_refit[PLAN_THREADS];   // round 0: first fits of a tile
     __shared__ int64_t s_wnd[6];
     __shared__ int64_t s_wub[2];
     extern __shared__ __align__(16) int64_t dyn[];          // channel + start-time windows
@@ -496,6 +508,47 @@ plan_loop_kernel(PlanArgs a) {
         __syncthreads();
         if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
         if (a.max_rounds > 0 && round >= a.max_rounds) break;
+        // ---- phase R: the SSD refits the last commit queued (candidates whose
+        // cached placement its bookings overlap), spread over every warp of
+        // the grid: 32-ary searches and 32-wide fit walks (bandwidth.py:88-120)
+        if (round > 0) {
+            const int q = (int)((round - 1) & 1);
+            const int64_t nq = ld_cg(&a.scalars[PS_RQ + q]);
+            const int64_t gw = ((int64_t)b * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)G * blockDim.x) >> 5;
+            ChanView cr[2];
+            for (int k = 0; k < 2; ++k) { cr[k].s = a.ch_s[k][ch_par[k]]; cr[k].e = a.ch_e[k][ch_par[k]]; cr[k].n = ch_n[k]; }
+            for (int64_t k = gw; k < nq; k += nw) {
+                const int64_t cc = ld_cg(&a.rq[q][k]);
+                const int8_t sc = ld_cg(&a.st[cc]);
+                const int64_t d0 = __ldg(&a.c_d[4 * cc]), d1 = __ldg(&a.c_d[4 * cc + 1]);
+                const int64_t h_off = ld_cg(&a.place[4 * cc]), h_pre = ld_cg(&a.place[4 * cc + 1]) + d1;
+                const int64_t delta = cr[0].n - ld_cg(&a.hver[cc]);
+                const int64_t plo = ld_cg(&a.hidx[2 * cc]), qlo = ld_cg(&a.hidx[2 * cc + 1]);
+                const int64_t phi = plo + delta < cr[0].n ? plo + delta : cr[0].n;
+                const int64_t qhi = qlo + delta < cr[1].n ? qlo + delta : cr[1].n;
+                int32_t ro[4];
+                for (int qq = 0; qq < 4; ++qq) ro[qq] = ld_cg(&a.rng[4 * cc + qq]);
+                int64_t os = 0, ps = 0, np = 0, nq2 = 0;
+                const bool ok = warp_fit_pair(cr[0].s, cr[0].e, cr[0].n, cr[1].s, cr[1].e, cr[1].n, d0, d1, I,
+                                              h_off, h_pre, plo, phi, qlo, qhi, &os, &ps, &np, &nq2);
+                int32_t r[4] = {1, 0, 1, 0};
+                if (ok) warp_covered_ranges_shrunk(a.starts, I, __ldg(&a.c_wraps[cc]), os + d0, ps, ro, r);
+                if (lane == 0) {
+                    if (ok) {
+                        a.place[4 * cc] = os;
+                        a.place[4 * cc + 1] = ps;
+                        for (int qq = 0; qq < 4; ++qq) a.rng[4 * cc + qq] = r[qq];
+                        a.hidx[2 * cc] = (int32_t)np;
+                        a.hidx[2 * cc + 1] = (int32_t)nq2;
+                        a.hver[cc] = (int32_t)cr[0].n;
+                    }
+                    a.st[cc] = (int8_t)((sc & ~3) | (ok ? S_OK : S_DEAD) | ST_REFIT);
+                }
+                __syncwarp();
+            }
+            PROF(if (b == 0 && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 9], nq));
+            grid_barrier(a.bar);
+        }
         TICK(0);
         PROF(const int64_t te0 = gtime());
         PROF(if (threadIdx.x == 0) { tsub = te0; for (int q = 0; q < 6; ++q) sub[q] = 0; });
@@ -516,7 +569,10 @@ plan_loop_kernel(PlanArgs a) {
             if (j < my_tiles) {
                 const int64_t t = b + j * G;
                 bool d = round == 0 || t == s_win_tile;
-                if (!d && last.dest) {
+                if (!d && last.dest == TIO_DEST_SSD) {
+                    // an SSD commit changes this tile only through the refits it queued
+                    d = ld_cg(&a.t_refit[t]) == (int32_t)(round - 1);
+                } else if (!d && last.dest) {
                     const int64_t lo = __ldg(&a.t_lo[t]), hi = __ldg(&a.t_hi[t]);
                     d = spans_hit(lo, hi, last.off_s, last.off_e, last.nb) ||
                         spans_hit(lo, hi, last.pre_s, last.pre_e, last.nb) ||
@@ -543,72 +599,17 @@ plan_loop_kernel(PlanArgs a) {
                 const int32_t cid = pos < a.P ? (int32_t)__ldg(&a.tcand[pos]) : -1;   // tie-break index
                 int8_t st = c >= 0 ? ld_cg(&a.st[c]) : ST_GONE;
                 // pass 1: which candidates need an SSD re-search (planner.py:147-176)
+                // (round 0: first fits inline; later rounds: phase R refitted the
+                // SSD placements the last commit overlapped and flagged them)
                 bool need = false;
-                if (!(st & ST_GONE)) {
-                    const int ssd = st & 3;
-                    if (ssd == S_UNK) need = true;
-                    else if (ssd == S_OK && last.dest == TIO_DEST_SSD) {
-                        const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
-                        need = overlaps(ld_cg(&a.place[4 * c]), d0, last.off_s, last.off_e, last.nb) ||
-                               overlaps(ld_cg(&a.place[4 * c + 1]), d1, last.pre_s, last.pre_e, last.nb);
-                    }
-                }
+                if (!(st & ST_GONE)) need = (st & 3) == S_UNK || (st & ST_REFIT);
                 if (threadIdx.x == 0) s_nrefit = 0;
                 __syncthreads();
                 if (need) s_refit[atomicAdd(&s_nrefit, 1)] = (int16_t)threadIdx.x;
                 __syncthreads();
                 const int nref = s_nrefit;
-                const bool warp_mode = round > 0 && nref <= a.warp_refit_max;
+                const bool warp_mode = round > 0;          // refits already done in phase R
 
-                PROF(if (nref && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 9], nref));
-                if (warp_mode) {
-                    // one warp per refit: 32-ary searches, 32-wide fit walks
-                    for (int k = warp; k < nref; k += nwarps) {
-                        const int64_t cc = t * TILE + s_refit[k];
-                        const int8_t sc = ld_cg(&a.st[cc]);
-                        const int64_t d0 = __ldg(&a.c_d[4 * cc]), d1 = __ldg(&a.c_d[4 * cc + 1]);
-                        int64_t h_off = __ldg(&a.c_ready[cc]), h_pre = __ldg(&a.c_deadline[cc]);
-                        const bool hinted = (sc & 3) == S_OK;
-                        int64_t plo = 0, phi = cv[0].n, qlo = 0, qhi = cv[1].n;
-                        int32_t ro[4] = {1, 0, 1, 0};
-                        if (hinted) {
-                            h_off = ld_cg(&a.place[4 * cc]);
-                            h_pre = ld_cg(&a.place[4 * cc + 1]) + d1;
-                            const int64_t delta = cv[0].n - ld_cg(&a.hver[cc]);
-                            plo = ld_cg(&a.hidx[2 * cc]);
-                            qlo = ld_cg(&a.hidx[2 * cc + 1]);
-                            phi = plo + delta < phi ? plo + delta : phi;
-                            qhi = qlo + delta < qhi ? qlo + delta : qhi;
-                            for (int q = 0; q < 4; ++q) ro[q] = ld_cg(&a.rng[4 * cc + q]);
-                        }
-                        int64_t os = 0, ps = 0, np = 0, nq = 0;
-                        const bool ok = warp_fit_pair(cv[0].s, cv[0].e, cv[0].n, cv[1].s, cv[1].e, cv[1].n, d0, d1, I,
-                                                      h_off, h_pre, plo, phi, qlo, qhi, &os, &ps, &np, &nq);
-                        int32_t r[4] = {1, 0, 1, 0};
-                        if (ok) {
-                            if (hinted)
-                                warp_covered_ranges_shrunk(a.starts, I, __ldg(&a.c_wraps[cc]), os + d0, ps, ro, r);
-                            else
-                                warp_covered_ranges(a.starts, N, I, __ldg(&a.c_wraps[cc]), __ldg(&a.c_sk[cc]),
-                                                    __ldg(&a.c_ek[cc]), __ldg(&a.c_first[cc]), __ldg(&a.c_last[cc]),
-                                                    os + d0, ps, r);
-                        }
-                        if (lane == 0) {
-                            if (ok) {
-                                a.place[4 * cc] = os;
-                                a.place[4 * cc + 1] = ps;
-                                for (int q = 0; q < 4; ++q) a.rng[4 * cc + q] = r[q];
-                                a.hidx[2 * cc] = (int32_t)np;
-                                a.hidx[2 * cc + 1] = (int32_t)nq;
-                                a.hver[cc] = (int32_t)cv[0].n;
-                            }
-                            a.st[cc] = (int8_t)((sc & ~3) | (ok ? S_OK : S_DEAD));
-                        }
-                        __syncwarp();
-                    }
-                    __syncthreads();
-                    if (need) st = ld_cg(&a.st[c]);
-                }
                 SUB(1);
                 // stage the tile's channel window and kernel start times in shared
                 // memory: the refits' searches then walk shared memory, with
@@ -727,8 +728,25 @@ plan_loop_kernel(PlanArgs a) {
                     } else if (dest) {
                         const int q0 = dest == TIO_DEST_SSD ? 0 : 2;
                         const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
+                        // unchanged since its last evaluation: same window on the same
+                        // path and no kernel of its covered ranges flipped -> same key
+                        bool cached = false;
+                        if (round > 0 && !moved && !need) {
+                            const Key ck = kload(&a.vkey[c]);
+                            if ((ck.meta & 3) == dest && (ck.meta >> 2) == cid) {
+                                cached = true;
+                                if (s_flip[0] > 0) {
+                                    const int4 rr = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c]));
+                                    const int64_t fl = s_flip[1], fh = s_flip[2];
+                                    cached = !((rr.x <= rr.y && rr.x <= fh && fl <= rr.y) ||
+                                               (rr.z <= rr.w && rr.z <= fh && fl <= rr.w));
+                                }
+                                if (cached) mine = ck;
+                            }
+                        }
                         int32_t r[4];
-                        if (moved) {
+                        if (cached) {
+                        } else if (moved) {
                             const int64_t os = ld_cg(&a.place[4 * c + q0]);
                             const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
                             covered_ranges(sv, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
@@ -738,24 +756,28 @@ plan_loop_kernel(PlanArgs a) {
                         } else {
                             for (int q = 0; q < 4; ++q) r[q] = ld_cg(&a.rng[4 * c + q]);
                         }
-                        int64_t ct = 0;
-                        for (int q = 0; q < 4; q += 2) {
-                            if (r[q] <= r[q + 1]) {
-                                int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
-                                ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
-                                      (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
+                        if (!cached) {
+                            int64_t ct = 0;
+                            for (int q = 0; q < 4; q += 2) {
+                                if (r[q] <= r[q + 1]) {
+                                    int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
+                                    ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
+                                          (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
+                                }
                             }
-                        }
-                        if (ct == 0) {
-                            // benefit only ever shrinks on a host window or on an SSD
-                            // window without a host path to fall back to
-                            if (dest == TIO_DEST_CPU || !a.has_host) nst |= ST_GONE;
-                        } else {
-                            const u128 bf = (u128)(uint64_t)size * (uint64_t)ct;
-                            mine.blo = (uint64_t)bf;
-                            mine.bhi = (uint64_t)(bf >> 64);
-                            mine.cost = doff + dpre;
-                            mine.meta = 4 * (int64_t)cid + dest;
+                            if (ct == 0) {
+                                // benefit only ever shrinks on a host window or on an SSD
+                                // window without a host path to fall back to
+                                if (dest == TIO_DEST_CPU || !a.has_host) nst |= ST_GONE;
+                            } else {
+                                const u128 bf = (u128)(uint64_t)size * (uint64_t)ct;
+                                mine.blo = (uint64_t)bf;
+                                mine.bhi = (uint64_t)(bf >> 64);
+                                mine.cost = doff + dpre;
+                                mine.meta = 4 * (int64_t)cid + dest;
+                            }
+                            // the key (zero benefit included) for later rounds
+                            kstore(&a.vkey[c], Key{mine.blo, mine.bhi, doff + dpre, 4 * (int64_t)cid + dest});
                         }
                     }
                     if (nst != st) a.st[c] = nst;
@@ -843,6 +865,58 @@ plan_loop_kernel(PlanArgs a) {
                 ++k;
             }
         }
+        // queue the SSD refits this commit causes: own tiles whose span meets
+        // the new bookings, candidates whose cached placement overlaps them
+        if (w.dest == TIO_DEST_SSD) {
+            const int qn = (int)(round & 1);
+            if (threadIdx.x == 0) s_ndirty = 0;
+            __syncthreads();
+            for (int64_t j = threadIdx.x; j < my_tiles; j += blockDim.x) {
+                const int64_t t = b + j * G;
+                const int64_t lo = __ldg(&a.t_lo[t]), hi = __ldg(&a.t_hi[t]);
+                if (spans_hit(lo, hi, ns[0], ne[0], nb) || spans_hit(lo, hi, ns[1], ne[1], nb)) {
+                    const int k = atomicAdd(&s_ndirty, 1);
+                    if (k < PLAN_THREADS) s_dirty[k] = (int32_t)t;
+                }
+            }
+            __syncthreads();
+            const int nd = s_ndirty < PLAN_THREADS ? s_ndirty : PLAN_THREADS;
+            for (int64_t i = threadIdx.x; i < (int64_t)nd * TILE; i += blockDim.x) {
+                const int64_t c = (int64_t)s_dirty[i / TILE] * TILE + (i % TILE);
+                if (c >= a.P || c == w.idx) continue;
+                const int8_t sc = ld_cg(&a.st[c]);
+                if ((sc & ST_GONE) || (sc & 3) != S_OK) continue;
+                if (overlaps(ld_cg(&a.place[4 * c]), __ldg(&a.c_d[4 * c]), ns[0], ne[0], nb) ||
+                    overlaps(ld_cg(&a.place[4 * c + 1]), __ldg(&a.c_d[4 * c + 1]), ns[1], ne[1], nb)) {
+                    const unsigned long long k =
+                        atomicAdd(reinterpret_cast<unsigned long long *>(&a.scalars[PS_RQ + qn]), 1ull);
+                    a.rq[qn][k] = c;
+                    a.t_refit[c / TILE] = (int32_t)round;
+                }
+            }
+            // more dirty tiles than the list holds: the rest, tile by tile
+            for (int64_t j = 0; s_ndirty > PLAN_THREADS && j < my_tiles; ++j) {
+                const int64_t t = b + j * G;
+                const int64_t lo = __ldg(&a.t_lo[t]), hi = __ldg(&a.t_hi[t]);
+                if (!(spans_hit(lo, hi, ns[0], ne[0], nb) || spans_hit(lo, hi, ns[1], ne[1], nb))) continue;
+                bool listed = false;
+                for (int k = 0; k < PLAN_THREADS; ++k) listed |= s_dirty[k] == t;
+                if (listed) continue;
+                const int64_t c = t * TILE + threadIdx.x;
+                if (c >= a.P || c == w.idx) continue;
+                const int8_t sc = ld_cg(&a.st[c]);
+                if ((sc & ST_GONE) || (sc & 3) != S_OK) continue;
+                if (overlaps(ld_cg(&a.place[4 * c]), __ldg(&a.c_d[4 * c]), ns[0], ne[0], nb) ||
+                    overlaps(ld_cg(&a.place[4 * c + 1]), __ldg(&a.c_d[4 * c + 1]), ns[1], ne[1], nb)) {
+                    const unsigned long long k =
+                        atomicAdd(reinterpret_cast<unsigned long long *>(&a.scalars[PS_RQ + qn]), 1ull);
+                    a.rq[qn][k] = c;
+                    a.t_refit[t] = (int32_t)round;
+                }
+            }
+        }
+        // the queue phase R consumed this round is free again
+        if (b == 0 && threadIdx.x == 0 && round > 0) a.scalars[PS_RQ + (int)((round - 1) & 1)] = 0;
         // merge the bookings into the other buffer of both channels (all blocks)
         for (int side = 0; side < 2; ++side) {
             const int q = q0 + side;

@@ -13,12 +13,13 @@ constexpr int TILE = PLAN_THREADS;   // candidates per tile (one block pass)
 enum : int { S_UNK = 0, S_OK = 1, S_DEAD = 2 };                   // SSD path
 enum : int { H_UNK = 0, H_OK = 1, H_CAPFAIL = 2, H_DEAD = 3 };    // host path
 constexpr int8_t ST_GONE = (int8_t)0x40;  // committed or permanently useless
+constexpr int8_t ST_REFIT = (int8_t)0x20; // placement refitted by phase R this round
 
 // planner scalars[] slots
 enum {
     PS_COMMITS = 0, PS_ROUNDS = 1, PS_CRIT = 2, PS_STATUS = 3, PS_OCC = 4,
     PS_UNSAT_K = 5, PS_UNSAT_B = 6, PS_INVARIANT = 7, PS_FLIP = 8 /* 3 slots x (cnt, lo, hi) */,
-    PS_DBG = 17 /* 16 debug counters */, PS_COUNT = 33
+    PS_DBG = 17 /* 16 debug counters */, PS_RQ = 33 /* 2 refit-queue counts */, PS_COUNT = 35
 };
 
 // argmax key of a candidate (benefit 0 = none); meta = 4 * index + destination
@@ -60,6 +61,9 @@ struct PlanArgs {
     const int64_t *t_lo, *t_hi;    // [ntiles] span [min ready, max deadline)
     const int32_t *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;  // [ntiles] kernel hulls (lo > hi: empty)
     Key *tile_best;                // [ntiles]
+    int64_t *rq[2];                // [P] each: queued SSD refits (positions), alternating by round
+    int32_t *t_refit;              // [ntiles] last round whose commit queued a refit in the tile
+    Key *vkey;                     // [P] key at the last evaluation (reused while unchanged)
     // channels: 4 channels (ssd.off, ssd.pre, host.off, host.pre) x 2 buffers
     int64_t *ch_s[4][2];
     int64_t *ch_e[4][2];
