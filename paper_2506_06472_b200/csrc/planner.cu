@@ -376,9 +376,8 @@ struct WinInfo {
     uint64_t blo, bhi;
 };
 
-constexpr int WIN_CH = 1024;     // channel intervals staged per channel
-constexpr int WIN_ST = 2048;     // kernel start times staged
-constexpr size_t PLAN_DYN_SMEM = sizeof(int64_t) * (4 * WIN_CH + WIN_ST);
+constexpr int DIRTY_MAX = 2048;  // own tiles tested / listed per pass
+constexpr size_t PLAN_DYN_SMEM = 0;
 
 __global__ void __launch_bounds__(PLAN_THREADS)
 plan_loop_kernel(PlanArgs a) {
@@ -393,16 +392,8 @@ plan_loop_kernel(PlanArgs a) {
     __shared__ int64_t s_crit;
     __shared__ int64_t s_flip[3];          // previous round: flipped count, lo, hi
     __shared__ int64_t s_win_tile;
-    __shared__ int32_t s_dirty[PLAN_THREADS];
+    __shared__ int32_t s_dirty[DIRTY_MAX];
     __shared__ int32_t s_ndirty;
-    __shared__ int16_t s_refit[PLAN_THREADS];   // round 0: first fits of a tile
-    __shared__ int64_t s_wnd[6];
-    __shared__ int64_t s_wub[2];
-    extern __shared__ __align__(16) int64_t dyn[];          // channel + start-time windows
-    int64_t *s_chs[2] = {dyn, dyn + 2 * WIN_CH};
-    int64_t *s_che[2] = {dyn + WIN_CH, dyn + 3 * WIN_CH};
-    int64_t *s_st = dyn + 4 * WIN_CH;
-    __shared__ int32_t s_nrefit;
 
     const int64_t N = a.N, I = a.iteration, cap = a.capacity;
     const int G = gridDim.x;
@@ -561,12 +552,11 @@ plan_loop_kernel(PlanArgs a) {
             cv[q].n = ch_n[q];
         }
         bool any_dirty = false;
-        for (int64_t j0 = 0; j0 < my_tiles; j0 += blockDim.x) {
-            // dirty test, one tile per thread
+        for (int64_t j0 = 0; j0 < my_tiles; j0 += DIRTY_MAX) {
+            // dirty test of up to DIRTY_MAX own tiles, compacted into s_dirty
             if (threadIdx.x == 0) s_ndirty = 0;
             __syncthreads();
-            const int64_t j = j0 + threadIdx.x;
-            if (j < my_tiles) {
+            for (int64_t j = j0 + threadIdx.x; j < my_tiles && j < j0 + DIRTY_MAX; j += blockDim.x) {
                 const int64_t t = b + j * G;
                 bool d = round == 0 || t == s_win_tile;
                 if (!d && last.dest == TIO_DEST_SSD) {
@@ -589,94 +579,32 @@ plan_loop_kernel(PlanArgs a) {
             __syncthreads();
             const int nd = s_ndirty;
             if (nd) any_dirty = true;
-            PROF(if (nd && threadIdx.x == 0) atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 14]), (long long)nd));
             PROF(if (nd && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 8], nd));
-            SUB(0);
-            for (int di = 0; di < nd; ++di) {
+            // one warp per dirty tile, one lane per candidate
+            for (int di = warp; di < nd; di += nwarps) {
                 const int64_t t = s_dirty[di];
-                const int64_t pos = t * TILE + threadIdx.x;
+                const int64_t pos = t * TILE + lane;
                 const int64_t c = pos < a.P ? pos : -1;                 // column position
                 const int32_t cid = pos < a.P ? (int32_t)__ldg(&a.tcand[pos]) : -1;   // tie-break index
-                int8_t st = c >= 0 ? ld_cg(&a.st[c]) : ST_GONE;
-                // pass 1: which candidates need an SSD re-search (planner.py:147-176)
-                // (round 0: first fits inline; later rounds: phase R refitted the
-                // SSD placements the last commit overlapped and flagged them)
-                bool need = false;
-                if (!(st & ST_GONE)) need = (st & 3) == S_UNK || (st & ST_REFIT);
-                if (threadIdx.x == 0) s_nrefit = 0;
-                __syncthreads();
-                if (need) s_refit[atomicAdd(&s_nrefit, 1)] = (int16_t)threadIdx.x;
-                __syncthreads();
-                const int nref = s_nrefit;
-                const bool warp_mode = round > 0;          // refits already done in phase R
-
-                SUB(1);
-                // stage the tile's channel window and kernel start times in shared
-                // memory: the refits' searches then walk shared memory, with
-                // global reads only past the window
-                ChanView wv[2] = {cv[0], cv[1]};
-                StartsView sv{a.starts};
-                if (nref > 0 && !warp_mode) {
-                    const int64_t lo_t = __ldg(&a.t_lo[t]), hi_t = __ldg(&a.t_hi[t]);
-                    if (warp < 2) {
-                        const ChanView &c = cv[warp];
-                        const int64_t w0 = warp_lower_bound(0, c.n, [&](int64_t j) { return ld_cg(c.e + j) > lo_t; });
-                        const int64_t wub = warp_lower_bound(w0, c.n, [&](int64_t j) { return ld_cg(c.s + j) >= hi_t; });
-                        const int64_t w1 = wub - w0 > WIN_CH ? w0 + WIN_CH : wub;
-                        if (lane == 0) { s_wnd[2 * warp] = w0; s_wnd[2 * warp + 1] = w1; s_wub[warp] = wub; }
-                    } else if (warp == 2 && lane == 0) {
-                        int64_t k0 = __ldg(&a.t_ka_lo[t]), k1 = (int64_t)__ldg(&a.t_ka_hi[t]) + 2;   // starts[k0 .. khi+1]
-                        if (k0 > k1 - 2) { k0 = 0; k1 = 0; }
-                        if (k1 > N + 1) k1 = N + 1;
-                        if (k1 - k0 > WIN_ST) k1 = k0 + WIN_ST;
-                        s_wnd[4] = k0; s_wnd[5] = k1;
-                    }
-                    __syncthreads();
-                    for (int q = 0; q < 2; ++q) {
-                        const int64_t w0 = s_wnd[2 * q], w1 = s_wnd[2 * q + 1];
-                        for (int64_t i = w0 + threadIdx.x; i < w1; i += blockDim.x) {
-                            s_chs[q][i - w0] = ld_cg(cv[q].s + i);
-                            s_che[q][i - w0] = ld_cg(cv[q].e + i);
-                        }
-                        wv[q].ws = s_chs[q]; wv[q].we = s_che[q]; wv[q].w0 = w0; wv[q].w1 = w1;
-                        wv[q].lb = w0; wv[q].ub = s_wub[q];
-                    }
-                    for (int64_t k = s_wnd[4] + threadIdx.x; k < s_wnd[5]; k += blockDim.x)
-                        s_st[k - s_wnd[4]] = __ldg(a.starts + k);
-                    sv.w = s_st; sv.w0 = s_wnd[4]; sv.w1 = s_wnd[5];
-                    __syncthreads();
-                }
-                SUB(2);
-                // pass 2: per-candidate evaluation
+                const int8_t st = c >= 0 ? ld_cg(&a.st[c]) : ST_GONE;
                 Key mine = none;
                 if (!(st & ST_GONE)) {
                     int ssd = st & 3, host = (st >> 2) & 3;
                     const int64_t size = __ldg(&a.c_size[c]);
-                    const int64_t ready = __ldg(&a.c_ready[c]), deadline = __ldg(&a.c_deadline[c]);
+                    // round 0: first fits here; later rounds phase R refitted the
+                    // SSD placements the last commit overlapped and flagged them
+                    const bool need = ssd == S_UNK || (st & ST_REFIT);
                     bool moved = false;
-                    if (need && !warp_mode) {
+                    if (ssd == S_UNK) {
                         const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
-                        int64_t h_off = ready, h_pre = deadline;
-                        const bool hinted = ssd == S_OK;
-                        int64_t hp = 0, hq = 0, hn = -1;
-                        if (hinted) {
-                            h_off = ld_cg(&a.place[4 * c]);
-                            h_pre = ld_cg(&a.place[4 * c + 1]) + d1;
-                            hp = ld_cg(&a.hidx[2 * c]); hq = ld_cg(&a.hidx[2 * c + 1]); hn = ld_cg(&a.hver[c]);
-                        }
                         int64_t os, ps, np, nq;
-                        if (fit_pair(wv[0], wv[1], d0, d1, I, h_off, h_pre, &os, &ps, hp, hq, hn, &np, &nq)) {
+                        if (fit_pair(cv[0], cv[1], d0, d1, I, __ldg(&a.c_ready[c]), __ldg(&a.c_deadline[c]),
+                                     &os, &ps, 0, 0, -1, &np, &nq)) {
                             int32_t r[4];
-                            if (hinted) {
-                                int32_t ro[4];
-                                for (int q = 0; q < 4; ++q) ro[q] = ld_cg(&a.rng[4 * c + q]);
-                                covered_ranges_shrunk(sv, I, __ldg(&a.c_wraps[c]), os + d0, ps, ro, r);
-                            } else {
-                                covered_ranges(sv, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
-                                               __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
-                                               os + d0, ps, r);
-                            }
-                            for (int q = 0; q < 4; ++q) a.rng[4 * c + q] = r[q];
+                            covered_ranges(StartsView{a.starts}, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                                           __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
+                                           os + d0, ps, r);
+                            *reinterpret_cast<int4 *>(&a.rng[4 * c]) = make_int4(r[0], r[1], r[2], r[3]);
                             ssd = S_OK;
                             a.place[4 * c] = os;
                             a.place[4 * c + 1] = ps;
@@ -687,6 +615,8 @@ plan_loop_kernel(PlanArgs a) {
                             ssd = S_DEAD;
                             moved = true;
                         }
+                    } else if ((st & ST_REFIT) && ssd == S_DEAD) {
+                        moved = true;
                     }
                     // host path (only consulted once the SSD path is dead: planner.py:211-227)
                     if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
@@ -703,7 +633,7 @@ plan_loop_kernel(PlanArgs a) {
                         }
                         if (refit) {
                             int64_t os, ps;
-                            int64_t g_off = ready, g_pre = deadline;
+                            int64_t g_off = __ldg(&a.c_ready[c]), g_pre = __ldg(&a.c_deadline[c]);
                             if (host != H_UNK) { g_off = ld_cg(&a.place[4 * c + 2]); g_pre = ld_cg(&a.place[4 * c + 3]) + d3; }
                             if (fit_pair(cv[2], cv[3], d2, d3, I, g_off, g_pre, &os, &ps)) {
                                 a.place[4 * c + 2] = os;
@@ -744,19 +674,19 @@ plan_loop_kernel(PlanArgs a) {
                                 if (cached) mine = ck;
                             }
                         }
-                        int32_t r[4];
-                        if (cached) {
-                        } else if (moved) {
-                            const int64_t os = ld_cg(&a.place[4 * c + q0]);
-                            const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
-                            covered_ranges(sv, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
-                                           __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
-                                           os + doff, ps, r);
-                            for (int q = 0; q < 4; ++q) a.rng[4 * c + q] = r[q];
-                        } else {
-                            for (int q = 0; q < 4; ++q) r[q] = ld_cg(&a.rng[4 * c + q]);
-                        }
                         if (!cached) {
+                            int32_t r[4];
+                            if (moved) {
+                                const int64_t os = ld_cg(&a.place[4 * c + q0]);
+                                const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
+                                covered_ranges(StartsView{a.starts}, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                                               __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
+                                               os + doff, ps, r);
+                                *reinterpret_cast<int4 *>(&a.rng[4 * c]) = make_int4(r[0], r[1], r[2], r[3]);
+                            } else {
+                                const int4 rr = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c]));
+                                r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
+                            }
                             int64_t ct = 0;
                             for (int q = 0; q < 4; q += 2) {
                                 if (r[q] <= r[q + 1]) {
@@ -782,10 +712,9 @@ plan_loop_kernel(PlanArgs a) {
                     }
                     if (nst != st) a.st[c] = nst;
                 }
-                SUB(3);
-                const Key tk = block_best(mine, sm_key);
-                if (threadIdx.x == 0) a.tile_best[t] = tk;
-                SUB(4);
+                const Key tk = warp_best(mine);
+                if (lane == 0) a.tile_best[t] = tk;
+                __syncwarp();
             }
             __syncthreads();
         }
@@ -869,50 +798,32 @@ plan_loop_kernel(PlanArgs a) {
         // the new bookings, candidates whose cached placement overlaps them
         if (w.dest == TIO_DEST_SSD) {
             const int qn = (int)(round & 1);
-            if (threadIdx.x == 0) s_ndirty = 0;
-            __syncthreads();
-            for (int64_t j = threadIdx.x; j < my_tiles; j += blockDim.x) {
-                const int64_t t = b + j * G;
-                const int64_t lo = __ldg(&a.t_lo[t]), hi = __ldg(&a.t_hi[t]);
-                if (spans_hit(lo, hi, ns[0], ne[0], nb) || spans_hit(lo, hi, ns[1], ne[1], nb)) {
-                    const int k = atomicAdd(&s_ndirty, 1);
-                    if (k < PLAN_THREADS) s_dirty[k] = (int32_t)t;
+            for (int64_t j0 = 0; j0 < my_tiles; j0 += DIRTY_MAX) {
+                if (threadIdx.x == 0) s_ndirty = 0;
+                __syncthreads();
+                for (int64_t j = j0 + threadIdx.x; j < my_tiles && j < j0 + DIRTY_MAX; j += blockDim.x) {
+                    const int64_t t = b + j * G;
+                    const int64_t lo = __ldg(&a.t_lo[t]), hi = __ldg(&a.t_hi[t]);
+                    if (spans_hit(lo, hi, ns[0], ne[0], nb) || spans_hit(lo, hi, ns[1], ne[1], nb))
+                        s_dirty[atomicAdd(&s_ndirty, 1)] = (int32_t)t;
                 }
-            }
-            __syncthreads();
-            const int nd = s_ndirty < PLAN_THREADS ? s_ndirty : PLAN_THREADS;
-            for (int64_t i = threadIdx.x; i < (int64_t)nd * TILE; i += blockDim.x) {
-                const int64_t c = (int64_t)s_dirty[i / TILE] * TILE + (i % TILE);
-                if (c >= a.P || c == w.idx) continue;
-                const int8_t sc = ld_cg(&a.st[c]);
-                if ((sc & ST_GONE) || (sc & 3) != S_OK) continue;
-                if (overlaps(ld_cg(&a.place[4 * c]), __ldg(&a.c_d[4 * c]), ns[0], ne[0], nb) ||
-                    overlaps(ld_cg(&a.place[4 * c + 1]), __ldg(&a.c_d[4 * c + 1]), ns[1], ne[1], nb)) {
-                    const unsigned long long k =
-                        atomicAdd(reinterpret_cast<unsigned long long *>(&a.scalars[PS_RQ + qn]), 1ull);
-                    a.rq[qn][k] = c;
-                    a.t_refit[c / TILE] = (int32_t)round;
+                __syncthreads();
+                const int nd = s_ndirty;
+                for (int64_t i = threadIdx.x; i < (int64_t)nd * TILE; i += blockDim.x) {
+                    const int64_t t = s_dirty[i / TILE];
+                    const int64_t c = t * TILE + (i % TILE);
+                    if (c >= a.P || c == w.idx) continue;
+                    const int8_t sc = ld_cg(&a.st[c]);
+                    if ((sc & ST_GONE) || (sc & 3) != S_OK) continue;
+                    if (overlaps(ld_cg(&a.place[4 * c]), __ldg(&a.c_d[4 * c]), ns[0], ne[0], nb) ||
+                        overlaps(ld_cg(&a.place[4 * c + 1]), __ldg(&a.c_d[4 * c + 1]), ns[1], ne[1], nb)) {
+                        const unsigned long long k =
+                            atomicAdd(reinterpret_cast<unsigned long long *>(&a.scalars[PS_RQ + qn]), 1ull);
+                        a.rq[qn][k] = c;
+                        a.t_refit[t] = (int32_t)round;
+                    }
                 }
-            }
-            // more dirty tiles than the list holds: the rest, tile by tile
-            for (int64_t j = 0; s_ndirty > PLAN_THREADS && j < my_tiles; ++j) {
-                const int64_t t = b + j * G;
-                const int64_t lo = __ldg(&a.t_lo[t]), hi = __ldg(&a.t_hi[t]);
-                if (!(spans_hit(lo, hi, ns[0], ne[0], nb) || spans_hit(lo, hi, ns[1], ne[1], nb))) continue;
-                bool listed = false;
-                for (int k = 0; k < PLAN_THREADS; ++k) listed |= s_dirty[k] == t;
-                if (listed) continue;
-                const int64_t c = t * TILE + threadIdx.x;
-                if (c >= a.P || c == w.idx) continue;
-                const int8_t sc = ld_cg(&a.st[c]);
-                if ((sc & ST_GONE) || (sc & 3) != S_OK) continue;
-                if (overlaps(ld_cg(&a.place[4 * c]), __ldg(&a.c_d[4 * c]), ns[0], ne[0], nb) ||
-                    overlaps(ld_cg(&a.place[4 * c + 1]), __ldg(&a.c_d[4 * c + 1]), ns[1], ne[1], nb)) {
-                    const unsigned long long k =
-                        atomicAdd(reinterpret_cast<unsigned long long *>(&a.scalars[PS_RQ + qn]), 1ull);
-                    a.rq[qn][k] = c;
-                    a.t_refit[t] = (int32_t)round;
-                }
+                __syncthreads();
             }
         }
         // the queue phase R consumed this round is free again

@@ -7,7 +7,7 @@
 namespace tio {
 
 constexpr int PLAN_THREADS = 256;
-constexpr int TILE = PLAN_THREADS;   // candidates per tile (one block pass)
+constexpr int TILE = 32;             // candidates per tile (one warp)
 
 // candidate SSD/host evaluation state (2 bits each in st[c])
 enum : int { S_UNK = 0, S_OK = 1, S_DEAD = 2 };                   // SSD path
