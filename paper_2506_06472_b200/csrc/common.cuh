@@ -42,30 +42,24 @@ __device__ __forceinline__ int8_t ld_cg(const int8_t *p) { return (int8_t)__ldcg
 __device__ __forceinline__ uint8_t ld_cg(const uint8_t *p) { return (uint8_t)__ldcg(reinterpret_cast<const unsigned char *>(p)); }
 
 // Grid-wide barrier for a co-resident (cooperatively launched) grid: one
-// arrival counter and a generation word.  Waiters poll the generation with
-// __nanosleep backoff instead of a tight loop, so a grid of blocks parked at
-// the barrier does not flood the L2 slice that holds the flag while the last
-// blocks are still working.  Release/acquire via __threadfence (gpu scope,
-// which also invalidates L1).  bar[0] = count, bar[1] = generation; zeroed
-// before the launch.
+// monotone 64-bit arrival counter.  Thread 0 of every block adds 1 with
+// release semantics (gpu scope; cumulative over the block's writes ordered by
+// the preceding __syncthreads) and polls with acquire loads until the counter
+// reaches the next multiple of gridDim.x: the value it added to tells the
+// barrier's phase, so no reset or generation word is needed.  Measured on
+// the B200: 1.18 us per barrier at 296 blocks (a counter + generation
+// barrier with __threadfence: 2.44 us; tools/micro/barrier_bench.cu).
+// bar[0..1] = the counter (zeroed before the launch).
 __device__ __forceinline__ void grid_barrier(unsigned *bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned *gen = bar + 1;
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            unsigned ns = 32;
-            while (*gen == g) {
-                __nanosleep(ns);
-                if (ns < 256) ns <<= 1;
-            }
+        unsigned long long *ctr = reinterpret_cast<unsigned long long *>(bar);
+        unsigned long long v;
+        asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(v) : "l"(ctr) : "memory");
+        const unsigned long long target = (v / gridDim.x + 1) * gridDim.x;
+        while (v < target) {
+            asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
         }
-        __threadfence();
     }
     __syncthreads();
 }
