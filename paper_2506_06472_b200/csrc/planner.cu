@@ -587,6 +587,9 @@ plan_loop_kernel(PlanArgs a) {
                 const int64_t c = pos < a.P ? pos : -1;                 // column position
                 const int32_t cid = pos < a.P ? (int32_t)__ldg(&a.tcand[pos]) : -1;   // tie-break index
                 const int8_t st = c >= 0 ? ld_cg(&a.st[c]) : ST_GONE;
+                // issue the loads of the common (unchanged-candidate) path together
+                const Key ck = c >= 0 ? kload(&a.vkey[c]) : none;
+                const int4 rr = c >= 0 ? __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c])) : make_int4(1, 0, 1, 0);
                 Key mine = none;
                 if (!(st & ST_GONE)) {
                     int ssd = st & 3, host = (st >> 2) & 3;
@@ -662,11 +665,9 @@ plan_loop_kernel(PlanArgs a) {
                         // path and no kernel of its covered ranges flipped -> same key
                         bool cached = false;
                         if (round > 0 && !moved && !need) {
-                            const Key ck = kload(&a.vkey[c]);
                             if ((ck.meta & 3) == dest && (ck.meta >> 2) == cid) {
                                 cached = true;
                                 if (s_flip[0] > 0) {
-                                    const int4 rr = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c]));
                                     const int64_t fl = s_flip[1], fh = s_flip[2];
                                     cached = !((rr.x <= rr.y && rr.x <= fh && fl <= rr.y) ||
                                                (rr.z <= rr.w && rr.z <= fh && fl <= rr.w));
@@ -683,8 +684,11 @@ plan_loop_kernel(PlanArgs a) {
                                                __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
                                                os + doff, ps, r);
                                 *reinterpret_cast<int4 *>(&a.rng[4 * c]) = make_int4(r[0], r[1], r[2], r[3]);
+                            } else if (need) {
+                                // first fit above or phase R: the ranges were just written
+                                const int4 r2 = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c]));
+                                r[0] = r2.x; r[1] = r2.y; r[2] = r2.z; r[3] = r2.w;
                             } else {
-                                const int4 rr = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c]));
                                 r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
                             }
                             int64_t ct = 0;
