@@ -511,14 +511,18 @@ plan_loop_kernel(PlanArgs a) {
             for (int64_t k = gw; k < nq; k += nw) {
                 const int64_t cc = ld_cg(&a.rq[q][k]);
                 const int8_t sc = ld_cg(&a.st[cc]);
-                const int64_t d0 = __ldg(&a.c_d[4 * cc]), d1 = __ldg(&a.c_d[4 * cc + 1]);
-                const int64_t h_off = ld_cg(&a.place[4 * cc]), h_pre = ld_cg(&a.place[4 * cc + 1]) + d1;
-                const int64_t delta = cr[0].n - ld_cg(&a.hver[cc]);
-                const int64_t plo = ld_cg(&a.hidx[2 * cc]), qlo = ld_cg(&a.hidx[2 * cc + 1]);
+                const longlong2 dd = __ldg(reinterpret_cast<const longlong2 *>(&a.c_d[4 * cc]));
+                const longlong2 pl = __ldcg(reinterpret_cast<const longlong2 *>(&a.place[4 * cc]));
+                const int2 hx = __ldcg(reinterpret_cast<const int2 *>(&a.hidx[2 * cc]));
+                const int32_t hv = ld_cg(&a.hver[cc]);
+                const int4 rr = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * cc]));
+                const int64_t d0 = dd.x, d1 = dd.y;
+                const int64_t h_off = pl.x, h_pre = pl.y + d1;
+                const int64_t delta = cr[0].n - hv;
+                const int64_t plo = hx.x, qlo = hx.y;
                 const int64_t phi = plo + delta < cr[0].n ? plo + delta : cr[0].n;
                 const int64_t qhi = qlo + delta < cr[1].n ? qlo + delta : cr[1].n;
-                int32_t ro[4];
-                for (int qq = 0; qq < 4; ++qq) ro[qq] = ld_cg(&a.rng[4 * cc + qq]);
+                const int32_t ro[4] = {rr.x, rr.y, rr.z, rr.w};
                 int64_t os = 0, ps = 0, np = 0, nq2 = 0;
                 const bool ok = warp_fit_pair(cr[0].s, cr[0].e, cr[0].n, cr[1].s, cr[1].e, cr[1].n, d0, d1, I,
                                               h_off, h_pre, plo, phi, qlo, qhi, &os, &ps, &np, &nq2);
@@ -818,9 +822,10 @@ plan_loop_kernel(PlanArgs a) {
                     const int64_t c = t * TILE + (i % TILE);
                     if (c >= a.P || c == w.idx) continue;
                     const int8_t sc = ld_cg(&a.st[c]);
+                    const longlong2 pl = __ldcg(reinterpret_cast<const longlong2 *>(&a.place[4 * c]));
+                    const longlong2 dd = __ldg(reinterpret_cast<const longlong2 *>(&a.c_d[4 * c]));
                     if ((sc & ST_GONE) || (sc & 3) != S_OK) continue;
-                    if (overlaps(ld_cg(&a.place[4 * c]), __ldg(&a.c_d[4 * c]), ns[0], ne[0], nb) ||
-                        overlaps(ld_cg(&a.place[4 * c + 1]), __ldg(&a.c_d[4 * c + 1]), ns[1], ne[1], nb)) {
+                    if (overlaps(pl.x, dd.x, ns[0], ne[0], nb) || overlaps(pl.y, dd.y, ns[1], ne[1], nb)) {
                         const unsigned long long k =
                             atomicAdd(reinterpret_cast<unsigned long long *>(&a.scalars[PS_RQ + qn]), 1ull);
                         a.rq[qn][k] = c;
