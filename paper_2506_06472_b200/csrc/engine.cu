@@ -392,6 +392,24 @@ extern "C" int tio_engine_replay(const tio_trace_desc *d, const tio_entry *entri
             R.host_bytes += align4k(in.size[t]);
         }
     if (R.host_bytes) TIO_CUDA(cudaHostAlloc((void **)&R.host, (size_t)R.host_bytes, cudaHostAllocPortable));
+    // reserve the pool's physical memory up front (kept: release threshold
+    // max) so no allocation inside the timed replay has to map new memory
+    {
+        size_t fr = 0, tot = 0;
+        TIO_CUDA(cudaMemGetInfo(&fr, &tot));
+        const size_t slack = (size_t)4 << 30;
+        size_t want = (size_t)(cfg->capacity + cfg->capacity / 2);
+        if (fr > slack && want > fr - slack) want = fr - slack;
+        if (fr > slack && want > 0) {
+            void *big = nullptr;
+            if (cudaMallocFromPoolAsync(&big, want, R.pool, R.comp) == cudaSuccess) {
+                TIO_CUDA(cudaFreeAsync(big, R.comp));
+            } else {
+                cudaGetLastError();      // best effort: fall back to growing on demand
+            }
+            TIO_CUDA(cudaStreamSynchronize(R.comp));
+        }
+    }
     stats->host_bytes = R.host_bytes;
     TIO_CUDA(cudaMallocAsync((void **)&R.bad, 16, R.pool, R.comp));
     R.sink = R.bad + 1;
