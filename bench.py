@@ -341,12 +341,51 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
     }
 
 
+def sharded_lifetime_leg(config: str, dev, rank: int, world: int) -> dict:
+    """the lifetime stage sharded by tensor id over the ranks
+    (libtio kernels per shard, NCCL all_reduce of timeline/active bytes and
+    all_gather of the period lists; paper_2506_06472_b200/distributed.py),
+    checked against the whole-trace lifetime computed locally.  Wall time,
+    max over ranks, host conversions included."""
+    import hashlib
+    import torch
+    import torch.distributed as dist
+    from paper_2506_06472_b200 import _native
+    from paper_2506_06472_b200.distributed import sharded_lifetime
+    try:
+        tr, cap, rates, hc, desc = _trace(config)
+        a = tr.arrays()
+        full = _native.DeviceTrace(a)
+        ref = full.lifetime()
+        full.close()
+        sharded_lifetime(a, rank, world, device=dev)          # warm-up
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = sharded_lifetime(a, rank, world, device=dev)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        t = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        same = all(np.array_equal(np.asarray(out[k]), np.asarray(ref[k]))
+                   for k in ("timeline", "active", "period_tensor", "period_start", "period_end", "period_wraps"))
+        ok = torch.tensor([1 if same else 0], dtype=torch.int64, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        return {"workload": desc, "ranks": world, "ms_wall_max_over_ranks": float(t.item()) * 1e3,
+                "bit_exact_vs_unsharded": bool(ok.item()), "shard_events": int(a.access_ptr[out["shard"][1]] -
+                                                                               a.access_ptr[out["shard"][0]]),
+                "collectives": f"{dist.get_backend()} all_reduce(int64[2N]) + all_gather(counts, padded period columns)"}
+    except Exception as exc:  # reported, not fatal: the headline line must still print
+        return {"error": f"{type(exc).__name__}: {exc}"}
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     warm = max(args.warmup, 3) if args.warmup >= 3 else args.warmup
     m = measure(args.config, args.steps, warm, dev, rank, world)
+    m_sh = sharded_lifetime_leg(args.config, dev, rank, world) if world > 1 else None
     extra = None
     if args.secondary and args.secondary != args.config:
         extra = measure(args.secondary, args.steps, warm, dev, rank, world)
@@ -367,6 +406,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, rounds, sample_rounds=args.ref_rounds_c3
                                             if args.config == "c3" else args.ref_rounds)
+    if world > 1 and m_sh is not None:
+        line["sharded_lifetime"] = m_sh
     if not args.no_migration and world == 1:
         # C4 on one GPU; at N > 1 the per-rank pinned host extents (24-78 GB
         # each) would exceed the box's host memory, so the leg runs at N = 1 only

@@ -30,7 +30,7 @@ def _oracle_local(sub):
             "period_end": per["end"], "period_wraps": per["wraps"].astype(np.int8)}
 
 
-def _worker(rank, world, port, cases, q):
+def _worker(rank, world, port, cases, q, device_kernels=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -45,7 +45,12 @@ def _worker(rank, world, port, cases, q):
         for kind, arg in cases:
             tr = gen_llama_trace(LlamaTraceConfig(microbatches=arg)) if kind == "llama" else \
                 gen_random_trace(arg, 3 + arg % 50, 1 + arg % 37)
-            r = sharded_lifetime(tr.arrays(), rank, world, local_fn=_oracle_local)
+            if device_kernels:      # libtio lifetime kernels per shard on cuda:0
+                import torch
+                torch.cuda.set_device(0)
+                r = sharded_lifetime(tr.arrays(), rank, world, device=torch.device("cuda", 0))
+            else:
+                r = sharded_lifetime(tr.arrays(), rank, world, local_fn=_oracle_local)
             out.append({k: (v.tolist() if isinstance(v, np.ndarray) else v) for k, v in r.items()})
         q.put((rank, out))
     finally:
@@ -79,6 +84,35 @@ def test_sharded_lifetime_equals_unsharded(world):
             assert got["period_start"] == per["start"].tolist()
             assert got["period_end"] == per["end"].tolist()
             assert got["period_wraps"] == per["wraps"].astype(int).tolist()
+
+
+@pytest.mark.gpu
+def test_sharded_lifetime_device_kernels_equals_oracle():
+    """The same exchange with the libtio kernels computing each shard on the
+    GPU (two ranks sharing cuda:0 over gloo; one GPU per rank would use NCCL)."""
+    from oracle import oracle as O
+    from paper_2506_06472_b200 import gen_random_trace, LlamaTraceConfig, gen_llama_trace
+    world = 2
+    cases = [("random", s) for s in (3, 11)] + [("llama", 2)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, q, True)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for ci, (kind, arg) in enumerate(cases):
+        tr = gen_llama_trace(LlamaTraceConfig(microbatches=arg)) if kind == "llama" else \
+            gen_random_trace(arg, 3 + arg % 50, 1 + arg % 37)
+        per, tl, act = O.lifetime(tr.arrays())
+        for r in range(world):
+            got = results[r][ci]
+            assert got["timeline"] == tl.tolist() and got["active"] == act.tolist()
+            assert got["period_tensor"] == per["tensor"].tolist()
+            assert got["period_start"] == per["start"].tolist() and got["period_end"] == per["end"].tolist()
 
 
 def test_shard_bounds_balanced_and_contiguous():
