@@ -393,6 +393,8 @@ plan_loop_kernel(PlanArgs a) {
     __shared__ int64_t s_flip[3];          // previous round: flipped count, lo, hi
     __shared__ int64_t s_win_tile;
     __shared__ int32_t s_dirty[DIRTY_MAX];
+    __shared__ Key s_rbest[32];            // best key per warp among this round's refits here
+    __shared__ bool s_prev_refit;          // refits ran here last round (their keys are in blk_best)
     __shared__ int32_t s_ndirty;
 
     const int64_t N = a.N, I = a.iteration, cap = a.capacity;
@@ -438,6 +440,7 @@ plan_loop_kernel(PlanArgs a) {
             last.nb = nb;
             s_nocc = 0;
             s_win_tile = -1;
+            s_prev_refit = false;
             for (int q = 0; q < 4; ++q) { ch_n[q] = 0; ch_par[q] = 0; }
             if (b == 0)
                 for (int q = 0; q < 3; ++q) { flip[3 * q] = 0; flip[3 * q + 1] = INT64_MAX; flip[3 * q + 2] = -1; }
@@ -499,51 +502,6 @@ plan_loop_kernel(PlanArgs a) {
         __syncthreads();
         if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
         if (a.max_rounds > 0 && round >= a.max_rounds) break;
-        // ---- phase R: the SSD refits the last commit queued (candidates whose
-        // cached placement its bookings overlap), spread over every warp of
-        // the grid: 32-ary searches and 32-wide fit walks (bandwidth.py:88-120)
-        if (round > 0) {
-            const int q = (int)((round - 1) & 1);
-            const int64_t nq = ld_cg(&a.scalars[PS_RQ + q]);
-            const int64_t gw = ((int64_t)b * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)G * blockDim.x) >> 5;
-            ChanView cr[2];
-            for (int k = 0; k < 2; ++k) { cr[k].s = a.ch_s[k][ch_par[k]]; cr[k].e = a.ch_e[k][ch_par[k]]; cr[k].n = ch_n[k]; }
-            for (int64_t k = gw; k < nq; k += nw) {
-                const int64_t cc = ld_cg(&a.rq[q][k]);
-                const int8_t sc = ld_cg(&a.st[cc]);
-                const longlong2 dd = __ldg(reinterpret_cast<const longlong2 *>(&a.c_d[4 * cc]));
-                const longlong2 pl = __ldcg(reinterpret_cast<const longlong2 *>(&a.place[4 * cc]));
-                const int2 hx = __ldcg(reinterpret_cast<const int2 *>(&a.hidx[2 * cc]));
-                const int32_t hv = ld_cg(&a.hver[cc]);
-                const int4 rr = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * cc]));
-                const int64_t d0 = dd.x, d1 = dd.y;
-                const int64_t h_off = pl.x, h_pre = pl.y + d1;
-                const int64_t delta = cr[0].n - hv;
-                const int64_t plo = hx.x, qlo = hx.y;
-                const int64_t phi = plo + delta < cr[0].n ? plo + delta : cr[0].n;
-                const int64_t qhi = qlo + delta < cr[1].n ? qlo + delta : cr[1].n;
-                const int32_t ro[4] = {rr.x, rr.y, rr.z, rr.w};
-                int64_t os = 0, ps = 0, np = 0, nq2 = 0;
-                const bool ok = warp_fit_pair(cr[0].s, cr[0].e, cr[0].n, cr[1].s, cr[1].e, cr[1].n, d0, d1, I,
-                                              h_off, h_pre, plo, phi, qlo, qhi, &os, &ps, &np, &nq2);
-                int32_t r[4] = {1, 0, 1, 0};
-                if (ok) warp_covered_ranges_shrunk(a.starts, I, __ldg(&a.c_wraps[cc]), os + d0, ps, ro, r);
-                if (lane == 0) {
-                    if (ok) {
-                        a.place[4 * cc] = os;
-                        a.place[4 * cc + 1] = ps;
-                        for (int qq = 0; qq < 4; ++qq) a.rng[4 * cc + qq] = r[qq];
-                        a.hidx[2 * cc] = (int32_t)np;
-                        a.hidx[2 * cc + 1] = (int32_t)nq2;
-                        a.hver[cc] = (int32_t)cr[0].n;
-                    }
-                    a.st[cc] = (int8_t)((sc & ~3) | (ok ? S_OK : S_DEAD) | ST_REFIT);
-                }
-                __syncwarp();
-            }
-            PROF(if (b == 0 && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 9], nq));
-            grid_barrier(a.bar);
-        }
         TICK(0);
         PROF(const int64_t te0 = gtime());
         PROF(if (threadIdx.x == 0) { tsub = te0; for (int q = 0; q < 6; ++q) sub[q] = 0; });
@@ -555,6 +513,187 @@ plan_loop_kernel(PlanArgs a) {
             cv[q].e = a.ch_e[q][ch_par[q]];
             cv[q].n = ch_n[q];
         }
+        // Re-derive candidate c's key against the current state (planner.py:147-262):
+        // first fit (round 0), refit flags from phase R, host path, benefit
+        // from the critical prefix or the cached key; writes st / vkey.
+        auto eval_lane = [&](int64_t c, int32_t cid, int8_t st, const Key &ck, const int4 &rr) -> Key {
+            Key mine = none;
+            if (!(st & ST_GONE)) {
+                int ssd = st & 3, host = (st >> 2) & 3;
+                const int64_t size = __ldg(&a.c_size[c]);
+                // round 0: first fits here; later rounds phase R refitted the
+                // SSD placements the last commit overlapped and flagged them
+                const bool need = ssd == S_UNK || (st & ST_REFIT);
+                bool moved = false;
+                if (ssd == S_UNK) {
+                    const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
+                    int64_t os, ps, np, nq;
+                    if (fit_pair(cv[0], cv[1], d0, d1, I, __ldg(&a.c_ready[c]), __ldg(&a.c_deadline[c]),
+                                 &os, &ps, 0, 0, -1, &np, &nq)) {
+                        int32_t r[4];
+                        covered_ranges(StartsView{a.starts}, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                                       __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
+                                       os + d0, ps, r);
+                        *reinterpret_cast<int4 *>(&a.rng[4 * c]) = make_int4(r[0], r[1], r[2], r[3]);
+                        ssd = S_OK;
+                        a.place[4 * c] = os;
+                        a.place[4 * c + 1] = ps;
+                        a.hidx[2 * c] = (int32_t)np;
+                        a.hidx[2 * c + 1] = (int32_t)nq;
+                        a.hver[c] = (int32_t)cv[0].n;
+                    } else {
+                        ssd = S_DEAD;
+                        moved = true;
+                    }
+                } else if ((st & ST_REFIT) && ssd == S_DEAD) {
+                    moved = true;
+                }
+                // host path (only consulted once the SSD path is dead: planner.py:211-227)
+                if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
+                    const int64_t d2 = __ldg(&a.c_d[4 * c + 2]), d3 = __ldg(&a.c_d[4 * c + 3]);
+                    bool refit = host == H_UNK;
+                    bool recap = false;
+                    if (!refit && last.dest == TIO_DEST_CPU) {
+                        refit = overlaps(ld_cg(&a.place[4 * c + 2]), d2, last.off_s, last.off_e, last.nb) ||
+                                overlaps(ld_cg(&a.place[4 * c + 3]), d3, last.pre_s, last.pre_e, last.nb);
+                        if (!refit && host == H_OK) {
+                            int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
+                            recap = last.occ_s <= hi && last.occ_e > lo;
+                        }
+                    }
+                    if (refit) {
+                        int64_t os, ps;
+                        int64_t g_off = __ldg(&a.c_ready[c]), g_pre = __ldg(&a.c_deadline[c]);
+                        if (host != H_UNK) { g_off = ld_cg(&a.place[4 * c + 2]); g_pre = ld_cg(&a.place[4 * c + 3]) + d3; }
+                        if (fit_pair(cv[2], cv[3], d2, d3, I, g_off, g_pre, &os, &ps)) {
+                            a.place[4 * c + 2] = os;
+                            a.place[4 * c + 3] = ps;
+                            recap = true;
+                            moved = true;
+                        } else {
+                            host = H_DEAD;
+                            moved = true;
+                        }
+                    }
+                    if (recap) {
+                        int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
+                        int64_t occ = host_peak(a.occ_s, a.occ_e, a.occ_size, s_nocc, lo, hi);
+                        host = (occ + size > a.host_cap) ? H_CAPFAIL : H_OK;
+                    }
+                }
+                int dest = ssd == S_OK ? TIO_DEST_SSD : (ssd == S_DEAD && host == H_OK ? TIO_DEST_CPU : 0);
+                int8_t nst = (int8_t)(ssd | (host << 2));
+                if (ssd == S_DEAD && (!a.has_host || host == H_DEAD)) {
+                    nst |= ST_GONE;
+                } else if (dest) {
+                    const int q0 = dest == TIO_DEST_SSD ? 0 : 2;
+                    const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
+                    // unchanged since its last evaluation: same window on the same
+                    // path and no kernel of its covered ranges flipped -> same key
+                    bool cached = false;
+                    if (round > 0 && !moved && !need) {
+                        if ((ck.meta & 3) == dest && (ck.meta >> 2) == cid) {
+                            cached = true;
+                            if (s_flip[0] > 0) {
+                                const int64_t fl = s_flip[1], fh = s_flip[2];
+                                cached = !((rr.x <= rr.y && rr.x <= fh && fl <= rr.y) ||
+                                           (rr.z <= rr.w && rr.z <= fh && fl <= rr.w));
+                            }
+                            if (cached) mine = ck;
+                        }
+                    }
+                    if (!cached) {
+                        int32_t r[4];
+                        if (moved) {
+                            const int64_t os = ld_cg(&a.place[4 * c + q0]);
+                            const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
+                            covered_ranges(StartsView{a.starts}, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
+                                           __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
+                                           os + doff, ps, r);
+                            *reinterpret_cast<int4 *>(&a.rng[4 * c]) = make_int4(r[0], r[1], r[2], r[3]);
+                        } else if (need) {
+                            // first fit above or phase R: the ranges were just written
+                            const int4 r2 = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c]));
+                            r[0] = r2.x; r[1] = r2.y; r[2] = r2.z; r[3] = r2.w;
+                        } else {
+                            r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
+                        }
+                        int64_t ct = 0;
+                        for (int q = 0; q < 4; q += 2) {
+                            if (r[q] <= r[q + 1]) {
+                                int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
+                                ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
+                                      (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
+                            }
+                        }
+                        if (ct == 0) {
+                            // benefit only ever shrinks on a host window or on an SSD
+                            // window without a host path to fall back to
+                            if (dest == TIO_DEST_CPU || !a.has_host) nst |= ST_GONE;
+                        } else {
+                            const u128 bf = (u128)(uint64_t)size * (uint64_t)ct;
+                            mine.blo = (uint64_t)bf;
+                            mine.bhi = (uint64_t)(bf >> 64);
+                            mine.cost = doff + dpre;
+                            mine.meta = 4 * (int64_t)cid + dest;
+                        }
+                        // the key (zero benefit included) for later rounds
+                        kstore(&a.vkey[c], Key{mine.blo, mine.bhi, doff + dpre, 4 * (int64_t)cid + dest});
+                    }
+                }
+                if (nst != st) a.st[c] = nst;
+            }
+            return mine;
+        };
+        // ---- phase R: the SSD refits the last commit queued (candidates whose
+        // cached placement its bookings overlap), spread over every warp of
+        // the grid: 32-ary searches and 32-wide fit walks (bandwidth.py:88-120);
+        // lane 0 then re-derives the key; the block's best refit key joins its
+        // block best.  No barrier: the owners' tile summaries below leave these
+        // candidates out this round (they take them back next round).
+        if (threadIdx.x < 32) s_rbest[threadIdx.x] = none;
+        __syncthreads();
+        if (round > 0) {
+            const int q = (int)((round - 1) & 1);
+            const int64_t nq = ld_cg(&a.scalars[PS_RQ + q]);
+            const int64_t gw = ((int64_t)b * blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)G * blockDim.x) >> 5;
+            for (int64_t k = gw; k < nq; k += nw) {
+                const int64_t cc = ld_cg(&a.rq[q][k]);
+                const int8_t sc = ld_cg(&a.st[cc]);
+                const longlong2 dd = __ldg(reinterpret_cast<const longlong2 *>(&a.c_d[4 * cc]));
+                const longlong2 pl = __ldcg(reinterpret_cast<const longlong2 *>(&a.place[4 * cc]));
+                const int2 hx = __ldcg(reinterpret_cast<const int2 *>(&a.hidx[2 * cc]));
+                const int32_t hv = ld_cg(&a.hver[cc]);
+                const int4 rr = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * cc]));
+                const int64_t d0 = dd.x, d1 = dd.y;
+                const int64_t h_off = pl.x, h_pre = pl.y + d1;
+                const int64_t delta = cv[0].n - hv;
+                const int64_t plo = hx.x, qlo = hx.y;
+                const int64_t phi = plo + delta < cv[0].n ? plo + delta : cv[0].n;
+                const int64_t qhi = qlo + delta < cv[1].n ? qlo + delta : cv[1].n;
+                const int32_t ro[4] = {rr.x, rr.y, rr.z, rr.w};
+                int64_t os = 0, ps = 0, np = 0, nq2 = 0;
+                const bool ok = warp_fit_pair(cv[0].s, cv[0].e, cv[0].n, cv[1].s, cv[1].e, cv[1].n, d0, d1, I,
+                                              h_off, h_pre, plo, phi, qlo, qhi, &os, &ps, &np, &nq2);
+                int32_t r[4] = {1, 0, 1, 0};
+                if (ok) warp_covered_ranges_shrunk(a.starts, I, __ldg(&a.c_wraps[cc]), os + d0, ps, ro, r);
+                if (lane == 0) {
+                    if (ok) {
+                        a.place[4 * cc] = os;
+                        a.place[4 * cc + 1] = ps;
+                        *reinterpret_cast<int4 *>(&a.rng[4 * cc]) = make_int4(r[0], r[1], r[2], r[3]);
+                        a.hidx[2 * cc] = (int32_t)np;
+                        a.hidx[2 * cc + 1] = (int32_t)nq2;
+                        a.hver[cc] = (int32_t)cv[0].n;
+                    }
+                    const int8_t st2 = (int8_t)((sc & ~3) | (ok ? S_OK : S_DEAD) | ST_REFIT);
+                    const Key kk = eval_lane(cc, (int32_t)__ldg(&a.tcand[cc]), st2, none, make_int4(1, 0, 1, 0));
+                    if (kbetter(kk, s_rbest[warp])) s_rbest[warp] = kk;
+                }
+                __syncwarp();
+            }
+            PROF(if (b == 0 && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 9], nq));
+        }
         bool any_dirty = false;
         for (int64_t j0 = 0; j0 < my_tiles; j0 += DIRTY_MAX) {
             // dirty test of up to DIRTY_MAX own tiles, compacted into s_dirty
@@ -562,7 +701,8 @@ plan_loop_kernel(PlanArgs a) {
             __syncthreads();
             for (int64_t j = j0 + threadIdx.x; j < my_tiles && j < j0 + DIRTY_MAX; j += blockDim.x) {
                 const int64_t t = b + j * G;
-                bool d = round == 0 || t == s_win_tile;
+                // tiles whose candidates phase R handled last round take them back
+                bool d = round == 0 || t == s_win_tile || (round > 1 && ld_cg(&a.t_refit[t]) == (int32_t)(round - 2));
                 if (!d && last.dest == TIO_DEST_SSD) {
                     // an SSD commit changes this tile only through the refits it queued
                     d = ld_cg(&a.t_refit[t]) == (int32_t)(round - 1);
@@ -594,132 +734,9 @@ plan_loop_kernel(PlanArgs a) {
                 // issue the loads of the common (unchanged-candidate) path together
                 const Key ck = c >= 0 ? kload(&a.vkey[c]) : none;
                 const int4 rr = c >= 0 ? __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c])) : make_int4(1, 0, 1, 0);
-                Key mine = none;
-                if (!(st & ST_GONE)) {
-                    int ssd = st & 3, host = (st >> 2) & 3;
-                    const int64_t size = __ldg(&a.c_size[c]);
-                    // round 0: first fits here; later rounds phase R refitted the
-                    // SSD placements the last commit overlapped and flagged them
-                    const bool need = ssd == S_UNK || (st & ST_REFIT);
-                    bool moved = false;
-                    if (ssd == S_UNK) {
-                        const int64_t d0 = __ldg(&a.c_d[4 * c]), d1 = __ldg(&a.c_d[4 * c + 1]);
-                        int64_t os, ps, np, nq;
-                        if (fit_pair(cv[0], cv[1], d0, d1, I, __ldg(&a.c_ready[c]), __ldg(&a.c_deadline[c]),
-                                     &os, &ps, 0, 0, -1, &np, &nq)) {
-                            int32_t r[4];
-                            covered_ranges(StartsView{a.starts}, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
-                                           __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
-                                           os + d0, ps, r);
-                            *reinterpret_cast<int4 *>(&a.rng[4 * c]) = make_int4(r[0], r[1], r[2], r[3]);
-                            ssd = S_OK;
-                            a.place[4 * c] = os;
-                            a.place[4 * c + 1] = ps;
-                            a.hidx[2 * c] = (int32_t)np;
-                            a.hidx[2 * c + 1] = (int32_t)nq;
-                            a.hver[c] = (int32_t)cv[0].n;
-                        } else {
-                            ssd = S_DEAD;
-                            moved = true;
-                        }
-                    } else if ((st & ST_REFIT) && ssd == S_DEAD) {
-                        moved = true;
-                    }
-                    // host path (only consulted once the SSD path is dead: planner.py:211-227)
-                    if (ssd == S_DEAD && a.has_host && host != H_DEAD) {
-                        const int64_t d2 = __ldg(&a.c_d[4 * c + 2]), d3 = __ldg(&a.c_d[4 * c + 3]);
-                        bool refit = host == H_UNK;
-                        bool recap = false;
-                        if (!refit && last.dest == TIO_DEST_CPU) {
-                            refit = overlaps(ld_cg(&a.place[4 * c + 2]), d2, last.off_s, last.off_e, last.nb) ||
-                                    overlaps(ld_cg(&a.place[4 * c + 3]), d3, last.pre_s, last.pre_e, last.nb);
-                            if (!refit && host == H_OK) {
-                                int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
-                                recap = last.occ_s <= hi && last.occ_e > lo;
-                            }
-                        }
-                        if (refit) {
-                            int64_t os, ps;
-                            int64_t g_off = __ldg(&a.c_ready[c]), g_pre = __ldg(&a.c_deadline[c]);
-                            if (host != H_UNK) { g_off = ld_cg(&a.place[4 * c + 2]); g_pre = ld_cg(&a.place[4 * c + 3]) + d3; }
-                            if (fit_pair(cv[2], cv[3], d2, d3, I, g_off, g_pre, &os, &ps)) {
-                                a.place[4 * c + 2] = os;
-                                a.place[4 * c + 3] = ps;
-                                recap = true;
-                                moved = true;
-                            } else {
-                                host = H_DEAD;
-                                moved = true;
-                            }
-                        }
-                        if (recap) {
-                            int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
-                            int64_t occ = host_peak(a.occ_s, a.occ_e, a.occ_size, s_nocc, lo, hi);
-                            host = (occ + size > a.host_cap) ? H_CAPFAIL : H_OK;
-                        }
-                    }
-                    int dest = ssd == S_OK ? TIO_DEST_SSD : (ssd == S_DEAD && host == H_OK ? TIO_DEST_CPU : 0);
-                    int8_t nst = (int8_t)(ssd | (host << 2));
-                    if (ssd == S_DEAD && (!a.has_host || host == H_DEAD)) {
-                        nst |= ST_GONE;
-                    } else if (dest) {
-                        const int q0 = dest == TIO_DEST_SSD ? 0 : 2;
-                        const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
-                        // unchanged since its last evaluation: same window on the same
-                        // path and no kernel of its covered ranges flipped -> same key
-                        bool cached = false;
-                        if (round > 0 && !moved && !need) {
-                            if ((ck.meta & 3) == dest && (ck.meta >> 2) == cid) {
-                                cached = true;
-                                if (s_flip[0] > 0) {
-                                    const int64_t fl = s_flip[1], fh = s_flip[2];
-                                    cached = !((rr.x <= rr.y && rr.x <= fh && fl <= rr.y) ||
-                                               (rr.z <= rr.w && rr.z <= fh && fl <= rr.w));
-                                }
-                                if (cached) mine = ck;
-                            }
-                        }
-                        if (!cached) {
-                            int32_t r[4];
-                            if (moved) {
-                                const int64_t os = ld_cg(&a.place[4 * c + q0]);
-                                const int64_t ps = ld_cg(&a.place[4 * c + q0 + 1]);
-                                covered_ranges(StartsView{a.starts}, N, I, __ldg(&a.c_wraps[c]), __ldg(&a.c_sk[c]),
-                                               __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
-                                               os + doff, ps, r);
-                                *reinterpret_cast<int4 *>(&a.rng[4 * c]) = make_int4(r[0], r[1], r[2], r[3]);
-                            } else if (need) {
-                                // first fit above or phase R: the ranges were just written
-                                const int4 r2 = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c]));
-                                r[0] = r2.x; r[1] = r2.y; r[2] = r2.z; r[3] = r2.w;
-                            } else {
-                                r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
-                            }
-                            int64_t ct = 0;
-                            for (int q = 0; q < 4; q += 2) {
-                                if (r[q] <= r[q + 1]) {
-                                    int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
-                                    ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
-                                          (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
-                                }
-                            }
-                            if (ct == 0) {
-                                // benefit only ever shrinks on a host window or on an SSD
-                                // window without a host path to fall back to
-                                if (dest == TIO_DEST_CPU || !a.has_host) nst |= ST_GONE;
-                            } else {
-                                const u128 bf = (u128)(uint64_t)size * (uint64_t)ct;
-                                mine.blo = (uint64_t)bf;
-                                mine.bhi = (uint64_t)(bf >> 64);
-                                mine.cost = doff + dpre;
-                                mine.meta = 4 * (int64_t)cid + dest;
-                            }
-                            // the key (zero benefit included) for later rounds
-                            kstore(&a.vkey[c], Key{mine.blo, mine.bhi, doff + dpre, 4 * (int64_t)cid + dest});
-                        }
-                    }
-                    if (nst != st) a.st[c] = nst;
-                }
+                // queued for a refit by the last commit: phase R owns it this round
+                const bool qround_skip = c >= 0 && round > 0 && ld_cg(&a.qround[c]) == (int32_t)(round - 1);
+                const Key mine = qround_skip ? none : eval_lane(c, cid, st, ck, rr);
                 const Key tk = warp_best(mine);
                 if (lane == 0) a.tile_best[t] = tk;
                 __syncwarp();
@@ -728,9 +745,13 @@ plan_loop_kernel(PlanArgs a) {
         }
         SUB(0);
         TICK(1);
-        // block best over this block's tiles (unchanged when no tile was dirty)
-        if (any_dirty) {
-            Key mine = none;
+        // block best over this block's tiles and its refit keys (unchanged when
+        // no tile was dirty and no refit ran here this round or the last)
+        __syncthreads();
+        bool refits_here = false;
+        for (int q = 0; q < nwarps; ++q) refits_here |= (s_rbest[q].blo | s_rbest[q].bhi) != 0;
+        if (any_dirty || refits_here || s_prev_refit) {
+            Key mine = threadIdx.x < nwarps ? s_rbest[threadIdx.x] : none;
             for (int64_t j = threadIdx.x; j < my_tiles; j += blockDim.x) {
                 const Key o = a.tile_best[b + j * G];
                 if (kbetter(o, mine)) mine = o;
@@ -740,6 +761,8 @@ plan_loop_kernel(PlanArgs a) {
         } else if (round == 0 && threadIdx.x == 0) {
             a.blk_best[b] = none;
         }
+        __syncthreads();
+        if (threadIdx.x == 0) s_prev_refit = refits_here;
         SUB(5);
         PROF(if (threadIdx.x == 0 && gtime() - te0 > 15000) {
             for (int q = 0; q < 6; ++q) slow[q] += sub[q];
@@ -761,8 +784,7 @@ plan_loop_kernel(PlanArgs a) {
         {
             Key w = none;
             for (int j = threadIdx.x; j < G; j += blockDim.x) {
-                const uint64_t *q = reinterpret_cast<const uint64_t *>(&a.blk_best[j]);
-                const Key o{ld_cg(q), ld_cg(q + 1), (int64_t)ld_cg(q + 2), (int64_t)ld_cg(q + 3)};
+                const Key o = kload(&a.blk_best[j]);
                 if (kbetter(o, w)) w = o;
             }
             w = block_best(w, sm_key);
@@ -829,6 +851,7 @@ plan_loop_kernel(PlanArgs a) {
                         const unsigned long long k =
                             atomicAdd(reinterpret_cast<unsigned long long *>(&a.scalars[PS_RQ + qn]), 1ull);
                         a.rq[qn][k] = c;
+                        a.qround[c] = (int32_t)round;
                         a.t_refit[t] = (int32_t)round;
                     }
                 }
