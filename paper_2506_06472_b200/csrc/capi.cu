@@ -452,6 +452,7 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     PTRY(A.alloc(&a.vkey, P));
     PTRY(A.alloc(&a.rq[0], P)); PTRY(A.alloc(&a.rq[1], P));
     PTRY(A.alloc(&a.t_refit, ntiles));
+    PTRY(A.alloc(&a.t_hull, 4 * ntiles));
     PTRY(A.alloc(&a.qround, P));
     PCUDA(cudaMemsetAsync(a.qround, 0xff, 4 * (size_t)(P > 0 ? P : 1), s));
     PCUDA(cudaMemsetAsync(a.t_refit, 0xff, 4 * (size_t)(ntiles > 0 ? ntiles : 1), s));

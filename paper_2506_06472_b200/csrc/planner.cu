@@ -682,6 +682,11 @@ plan_loop_kernel(PlanArgs a) {
                         a.place[4 * cc] = os;
                         a.place[4 * cc + 1] = ps;
                         *reinterpret_cast<int4 *>(&a.rng[4 * cc]) = make_int4(r[0], r[1], r[2], r[3]);
+                        // keep the tile's placement hulls supersets: an offload only
+                        // moves later, a prefetch only earlier
+                        long long *h = reinterpret_cast<long long *>(a.t_hull + 4 * (cc / TILE));
+                        atomicMax(h + 1, (long long)(os + d0));
+                        atomicMin(h + 2, (long long)ps);
                         a.hidx[2 * cc] = (int32_t)np;
                         a.hidx[2 * cc + 1] = (int32_t)nq2;
                         a.hver[cc] = (int32_t)cv[0].n;
@@ -737,6 +742,29 @@ plan_loop_kernel(PlanArgs a) {
                 // queued for a refit by the last commit: phase R owns it this round
                 const bool qround_skip = c >= 0 && round > 0 && ld_cg(&a.qround[c]) == (int32_t)(round - 1);
                 const Key mine = qround_skip ? none : eval_lane(c, cid, st, ck, rr);
+                if (round == 0) {
+                    // hulls of the tile's SSD placements (offload, prefetch); the
+                    // refit queueing tests a commit's bookings against them
+                    int64_t h0 = INT64_MAX, h1 = INT64_MIN, h2 = INT64_MAX, h3 = INT64_MIN;
+                    if (c >= 0) {
+                        const int8_t s2 = ld_cg(&a.st[c]);
+                        if (!(s2 & ST_GONE) && (s2 & 3) == S_OK) {
+                            h0 = ld_cg(&a.place[4 * c]); h1 = h0 + __ldg(&a.c_d[4 * c]);
+                            h2 = ld_cg(&a.place[4 * c + 1]); h3 = h2 + __ldg(&a.c_d[4 * c + 1]);
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        h0 = min(h0, (int64_t)__shfl_xor_sync(0xffffffffu, h0, o));
+                        h1 = max(h1, (int64_t)__shfl_xor_sync(0xffffffffu, h1, o));
+                        h2 = min(h2, (int64_t)__shfl_xor_sync(0xffffffffu, h2, o));
+                        h3 = max(h3, (int64_t)__shfl_xor_sync(0xffffffffu, h3, o));
+                    }
+                    if (lane == 0) {
+                        a.t_hull[4 * t] = h0; a.t_hull[4 * t + 1] = h1;
+                        a.t_hull[4 * t + 2] = h2; a.t_hull[4 * t + 3] = h3;
+                    }
+                }
                 const Key tk = warp_best(mine);
                 if (lane == 0) a.tile_best[t] = tk;
                 __syncwarp();
@@ -833,8 +861,9 @@ plan_loop_kernel(PlanArgs a) {
                 __syncthreads();
                 for (int64_t j = j0 + threadIdx.x; j < my_tiles && j < j0 + DIRTY_MAX; j += blockDim.x) {
                     const int64_t t = b + j * G;
-                    const int64_t lo = __ldg(&a.t_lo[t]), hi = __ldg(&a.t_hi[t]);
-                    if (spans_hit(lo, hi, ns[0], ne[0], nb) || spans_hit(lo, hi, ns[1], ne[1], nb))
+                    const longlong2 h01 = __ldcg(reinterpret_cast<const longlong2 *>(a.t_hull + 4 * t));
+                    const longlong2 h23 = __ldcg(reinterpret_cast<const longlong2 *>(a.t_hull + 4 * t + 2));
+                    if (spans_hit(h01.x, h01.y, ns[0], ne[0], nb) || spans_hit(h23.x, h23.y, ns[1], ne[1], nb))
                         s_dirty[atomicAdd(&s_ndirty, 1)] = (int32_t)t;
                 }
                 __syncthreads();

@@ -63,6 +63,7 @@ struct PlanArgs {
     Key *tile_best;                // [ntiles]
     int64_t *rq[2];                // [P] each: queued SSD refits (positions), alternating by round
     int32_t *t_refit;              // [ntiles] last round whose commit queued a refit in the tile
+    int64_t *t_hull;               // [4 ntiles] supersets of the SSD placements: off lo/hi, pre lo/hi
     int32_t *qround;               // [P] round whose commit queued the candidate's refit (-1 none)
     Key *vkey;                     // [P] key at the last evaluation (reused while unchanged)
     // channels: 4 channels (ssd.off, ssd.pre, host.off, host.pre) x 2 buffers
