@@ -175,7 +175,7 @@ int tio_plan_create(tio_trace *t, int64_t capacity, const tio_rates *rates, int6
 /* Options of tio_plan_create2: max_rounds > 0 stops the greedy loop after
  * that many commits (the plan is then the reference's first max_rounds
  * commits; used to check a prefix of huge plans against the oracle);
- * warp_refit_max: refits per tile served warp-cooperatively (-1: default). */
+ * warp_refit_max: reserved (ignored; the layout is kept for ABI stability). */
 typedef struct tio_plan_opts {
     int64_t max_rounds;
     int32_t warp_refit_max;

@@ -520,9 +520,6 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     a.N = N; a.P = P; a.iteration = I; a.capacity = capacity; a.host_cap = host_cap;
     a.has_host = has_host;
     a.chunk = (int32_t)((N + 1 + G - 1) / G);
-    a.warp_refit_max = 0;     // per-thread refits measured faster on C2 (tools/planner_sweep.sh)
-    if (const char *e = getenv("TIO_WARP_REFIT_MAX")) a.warp_refit_max = atoi(e);
-    if (opts && opts->warp_refit_max >= 0) a.warp_refit_max = opts->warp_refit_max;
     a.max_rounds = opts ? opts->max_rounds : 0;
     a.starts = t->starts; a.dur = t->dur; a.resid = resid; a.local_cp = local_cp; a.chunk_sum = chunk_sum;
     a.c_size = c_size; a.c_sk = c_sk; a.c_ek = c_ek; a.c_first = c_first; a.c_last = c_last; a.c_wraps = c_wraps;

@@ -33,7 +33,7 @@ struct PlanArgs {
     int64_t N, P, iteration, capacity, host_cap;
     int32_t has_host;
     int32_t chunk;                 // kernels per chunk (crit prefix / residual ownership)
-    int32_t warp_refit_max;        // refits per tile served warp-cooperatively (else one per thread)
+    int32_t pad0;
     int64_t max_rounds;            // > 0: stop after that many commits
     // immutable per-kernel data
     const int64_t *starts;         // [N+1]
