@@ -308,6 +308,15 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
         except Exception:
             traffic = None
     rounds = int(info.rounds)
+    ptraffic = None
+    pp = os.path.join(ROOT, "profiles", "planner_traffic.json")
+    if os.path.exists(pp):
+        try:
+            with open(pp) as f:
+                ptraffic = json.load(f).get(config)
+        except Exception:
+            ptraffic = None
+    loop_s = loop_ms / K / 1e3
     return {
         "value": world * E * K / (tot_ms_max / 1e3), "ms_per_step": tot_ms_max / K,
         "config": {"workload": desc, "events": E, "kernels": N, "tensors": T, "periods": P,
@@ -321,10 +330,16 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": B_L,
                      "share_of_step": life_ms / tot_ms},
-        "planner": {"kernel": "plan_loop_kernel", "bound": "latency (2 grid barriers per round)",
+        "planner": {"kernel": "plan_loop_kernel (the step's dominant kernel)",
+                    "bound": "latency (2 grid barriers + dependent L2 loads per round)",
                     "rounds": rounds, "commits": int(info.num_commits),
                     "us_per_round": (loop_ms / K) * 1e3 / max(1, rounds),
                     "share_of_step": loop_ms / tot_ms,
+                    # ncu DRAM bytes of one launch over the measured loop time:
+                    # the dominant kernel is latency-bound, not HBM-bound
+                    "traffic": ptraffic,
+                    "dram_gbs": (ptraffic / loop_s / 1e9) if ptraffic and loop_s > 0 else None,
+                    "frac_of_hbm_peak": (ptraffic / loop_s / 1e9 / peak) if ptraffic and loop_s > 0 else None,
                     **({"debug_build": {
                         "phase_us_per_round_block0": dict(zip(
                             ["prologue", "evaluate", "block_reduce", "barrier1", "argmax", "channel_merge",
