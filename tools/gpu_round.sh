@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU session: smoke, parity tests, bench, launch list, ncu capture of the lifetime kernel.
+# One GPU session: smoke, parity tests, bench, launch list, ncu capture of one kernel (NCU_KERNEL, default k_events).
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 nvidia-smi -L
@@ -11,7 +11,7 @@ if [ -z "$NO_NCU" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 1 --warmup 0 --no-cpu-baseline ${BENCH_ARGS} > /dev/null 2>gpurun_out/ncu1.err
 echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-lifetime_kernel} -c 1 \
-    -o gpurun_out/prof_${NCU_KERNEL:-lifetime_kernel} -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline ${BENCH_ARGS} > /dev/null 2>gpurun_out/ncu2.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_events} -c 1 \
+    -o gpurun_out/prof_${NCU_KERNEL:-k_events} -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline ${BENCH_ARGS} > /dev/null 2>gpurun_out/ncu2.err
 echo "ncu full rc=$?"
 fi
