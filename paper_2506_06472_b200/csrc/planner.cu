@@ -339,6 +339,10 @@ __device__ __forceinline__ void kstore(Key *p, const Key &k) {
     q[1] = make_ulonglong2((unsigned long long)k.cost, (unsigned long long)k.meta);
 }
 
+__device__ __forceinline__ void l2_prefetch(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // ---------------------------------------------------------------- the kernel
 //
 // Tiles.  Candidates are grouped into tiles of TILE consecutive candidates in
@@ -731,6 +735,19 @@ plan_loop_kernel(PlanArgs a) {
             PROF(if (nd && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 8], nd));
             // one warp per dirty tile, one lane per candidate
             for (int di = warp; di < nd; di += nwarps) {
+                if (di + nwarps < nd) {
+                    // pull the warp's next tile toward L2 while this one is evaluated
+                    const int64_t pn = (int64_t)s_dirty[di + nwarps] * TILE + lane;
+                    if (pn < a.P) {
+                        l2_prefetch(&a.vkey[pn]);
+                        l2_prefetch(&a.rng[4 * pn]);
+                        l2_prefetch(&a.c_d[4 * pn]);
+                        if (lane == 0) {
+                            l2_prefetch(&a.st[pn]); l2_prefetch(&a.qround[pn]); l2_prefetch(&a.tcand[pn]);
+                            l2_prefetch(&a.c_size[pn]);
+                        }
+                    }
+                }
                 const int64_t t = s_dirty[di];
                 const int64_t pos = t * TILE + lane;
                 const int64_t c = pos < a.P ? pos : -1;                 // column position
