@@ -399,6 +399,7 @@ plan_loop_kernel(PlanArgs a) {
     __shared__ int32_t s_dirty[DIRTY_MAX];
     __shared__ Key s_rbest[32];            // best key per warp among this round's refits here
     __shared__ bool s_prev_refit;          // refits ran here last round (their keys are in blk_best)
+    __shared__ Key s_tmax;                 // best key over the own tiles (as of their last change)
     __shared__ int32_t s_ndirty;
 
     const int64_t N = a.N, I = a.iteration, cap = a.capacity;
@@ -445,6 +446,7 @@ plan_loop_kernel(PlanArgs a) {
             s_nocc = 0;
             s_win_tile = -1;
             s_prev_refit = false;
+            s_tmax = Key{0, 0, 1, 0};
             for (int q = 0; q < 4; ++q) { ch_n[q] = 0; ch_par[q] = 0; }
             if (b == 0)
                 for (int q = 0; q < 3; ++q) { flip[3 * q] = 0; flip[3 * q + 1] = INT64_MAX; flip[3 * q + 2] = -1; }
@@ -795,16 +797,24 @@ plan_loop_kernel(PlanArgs a) {
         __syncthreads();
         bool refits_here = false;
         for (int q = 0; q < nwarps; ++q) refits_here |= (s_rbest[q].blo | s_rbest[q].bhi) != 0;
-        if (any_dirty || refits_here || s_prev_refit) {
-            Key mine = threadIdx.x < nwarps ? s_rbest[threadIdx.x] : none;
+        if (any_dirty) {
+            // best over the own tiles, kept for the rounds where only refit
+            // keys change the block best
+            Key mine = none;
             for (int64_t j = threadIdx.x; j < my_tiles; j += blockDim.x) {
                 const Key o = a.tile_best[b + j * G];
                 if (kbetter(o, mine)) mine = o;
             }
-            const Key bk = block_best(mine, sm_key);
-            if (threadIdx.x == 0) a.blk_best[b] = bk;
-        } else if (round == 0 && threadIdx.x == 0) {
-            a.blk_best[b] = none;
+            const Key tm = block_best(mine, sm_key);
+            if (threadIdx.x == 0) s_tmax = tm;
+            __syncthreads();
+        }
+        if (any_dirty || refits_here || s_prev_refit || round == 0) {
+            if (warp == 0) {
+                Key k = lane < nwarps ? s_rbest[lane] : (lane == nwarps ? s_tmax : none);
+                k = warp_best(k);
+                if (lane == 0) a.blk_best[b] = k;
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) s_prev_refit = refits_here;
