@@ -139,6 +139,31 @@ def test_random_traces_vs_oracle_wide_fuzz():
         assert np.array_equal(g["residual"], o["residual"]), case
 
 
+def test_random_traces_vs_oracle_many_blocks():
+    """Larger random traces (hundreds of warp tiles spread over the grid's
+    blocks), so refits queued by one block run on others and the owners'
+    summaries leave them out for a round; SSD-only and with a host tier."""
+    import random
+    rng = random.Random(2718)
+    for case in range(6):
+        nk = rng.randint(2_000, 6_000)
+        nt = rng.randint(3_000, 9_000)
+        tr = gen_random_trace(rng.randint(0, 10**9), nk, nt, size_range=(1_000_000, 400_000_000),
+                              duration_range=(10, 5_000), global_fraction=rng.choice((0.05, 0.3)))
+        a = tr.arrays()
+        per, tl, act = O.lifetime(a)
+        cap = max(int(act.max()), int(tl.max() * rng.choice((0.5, 0.7))))
+        ssd = rng.choice((20_000.0, 60_000.0))
+        host = None if case % 2 == 0 else ssd * 2.0
+        hc = 10**11 if host else 0
+        rates = ChannelRates.symmetric(ssd, host=host)
+        o = O.plan(a, cap, ssd, ssd, host, host, hc, lifetime_out=(per, tl, act), max_rounds=400)
+        g = plan_device(tr, cap, rates, hc, max_rounds=400)
+        assert len(o["committed"]) > 20, case
+        assert g["plan_bytes"] == o["plan_bytes"], case
+        assert np.array_equal(g["residual"], o["residual"]), case
+
+
 # ---------------------------------------------------------------- known answers
 # reference tests/test_analysis.py:18-69 and test_planner.py:108-234
 
