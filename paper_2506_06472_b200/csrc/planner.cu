@@ -951,14 +951,25 @@ plan_loop_kernel(PlanArgs a) {
                 if (lo < x0) lo = x0;
                 if (hi > x1 - 1) hi = x1 - 1;
                 if (hi > N - 1) hi = N - 1;
-                for (int64_t k = lo + threadIdx.x; k <= hi; k += blockDim.x) {
-                    int64_t old = ld_cg(&a.resid[k]);
-                    int64_t nw = old - w.size;
-                    a.resid[k] = nw;
-                    if (old > cap && nw <= cap) {
-                        ++flips;
-                        atomicMin(reinterpret_cast<unsigned long long *>(fs + 1), (unsigned long long)k);
-                        atomicMax(reinterpret_cast<long long *>(fs + 2), (long long)k);
+                // 4 kernels per thread per step, loads issued together
+                for (int64_t k0 = lo + threadIdx.x; k0 <= hi; k0 += 4 * (int64_t)blockDim.x) {
+                    int64_t ov[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t k = k0 + (int64_t)u * blockDim.x;
+                        ov[u] = k <= hi ? ld_cg(&a.resid[k]) : 0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t k = k0 + (int64_t)u * blockDim.x;
+                        if (k > hi) break;
+                        const int64_t nw = ov[u] - w.size;
+                        a.resid[k] = nw;
+                        if (ov[u] > cap && nw <= cap) {
+                            ++flips;
+                            atomicMin(reinterpret_cast<unsigned long long *>(fs + 1), (unsigned long long)k);
+                            atomicMax(reinterpret_cast<long long *>(fs + 2), (long long)k);
+                        }
                     }
                 }
             }
