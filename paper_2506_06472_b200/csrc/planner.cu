@@ -419,15 +419,19 @@ plan_loop_kernel(PlanArgs a) {
     if (ld_cg(&a.scalars[PS_STATUS]) != 0) return;  // unsatisfiable (set by setup)
 
     // ---- setup: chunk prefix of critical durations
+    // prefix of duration x [residual > capacity] over this block's chunk,
+    // two kernels per thread per block scan
     auto rebuild_chunk = [&]() {
         int64_t run = 0;
-        for (int64_t base = x0; base < x1; base += blockDim.x) {
-            int64_t x = base + threadIdx.x;
-            int64_t w = 0;
-            if (x < x1 && x < N && ld_cg(&a.resid[x]) > cap) w = __ldg(&a.dur[x]);
+        for (int64_t base = x0; base < x1; base += 2 * (int64_t)blockDim.x) {
+            const int64_t x = base + 2 * (int64_t)threadIdx.x;
+            int64_t w0 = 0, w1 = 0;
+            if (x < x1 && x < N && ld_cg(&a.resid[x]) > cap) w0 = __ldg(&a.dur[x]);
+            if (x + 1 < x1 && x + 1 < N && ld_cg(&a.resid[x + 1]) > cap) w1 = __ldg(&a.dur[x + 1]);
             int64_t tot;
-            int64_t ex = block_exclusive_sum<int64_t>(w, sm_scan, &tot);
+            const int64_t ex = block_exclusive_sum<int64_t>(w0 + w1, sm_scan, &tot);
             if (x < x1) a.local_cp[x] = run + ex;
+            if (x + 1 < x1) a.local_cp[x + 1] = run + ex + w0;
             run += tot;
         }
         if (threadIdx.x == 0) a.chunk_sum[b] = run;
