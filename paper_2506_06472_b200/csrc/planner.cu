@@ -420,18 +420,22 @@ plan_loop_kernel(PlanArgs a) {
 
     // ---- setup: chunk prefix of critical durations
     // prefix of duration x [residual > capacity] over this block's chunk,
-    // two kernels per thread per block scan
+    // four kernels per thread per block scan
     auto rebuild_chunk = [&]() {
         int64_t run = 0;
-        for (int64_t base = x0; base < x1; base += 2 * (int64_t)blockDim.x) {
-            const int64_t x = base + 2 * (int64_t)threadIdx.x;
-            int64_t w0 = 0, w1 = 0;
-            if (x < x1 && x < N && ld_cg(&a.resid[x]) > cap) w0 = __ldg(&a.dur[x]);
-            if (x + 1 < x1 && x + 1 < N && ld_cg(&a.resid[x + 1]) > cap) w1 = __ldg(&a.dur[x + 1]);
+        for (int64_t base = x0; base < x1; base += 4 * (int64_t)blockDim.x) {
+            const int64_t x = base + 4 * (int64_t)threadIdx.x;
+            int64_t wv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                wv[u] = (x + u < x1 && x + u < N && ld_cg(&a.resid[x + u]) > cap) ? __ldg(&a.dur[x + u]) : 0;
             int64_t tot;
-            const int64_t ex = block_exclusive_sum<int64_t>(w0 + w1, sm_scan, &tot);
-            if (x < x1) a.local_cp[x] = run + ex;
-            if (x + 1 < x1) a.local_cp[x + 1] = run + ex + w0;
+            int64_t ex = run + block_exclusive_sum<int64_t>(wv[0] + wv[1] + wv[2] + wv[3], sm_scan, &tot);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (x + u < x1) a.local_cp[x + u] = ex;
+                ex += wv[u];
+            }
             run += tot;
         }
         if (threadIdx.x == 0) a.chunk_sum[b] = run;
