@@ -632,14 +632,17 @@ plan_loop_kernel(PlanArgs a) {
                         } else {
                             r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
                         }
+                        // sum of critical durations over the <= 2 covered ranges: the
+                        // four prefix loads issued together, 32-bit chunk division
+                        const bool v0 = r[0] <= r[1], v1 = r[2] <= r[3];
+                        const int32_t xa0 = v0 ? r[0] : 0, xb0 = v0 ? r[1] + 1 : 0;
+                        const int32_t xa1 = v1 ? r[2] : 0, xb1 = v1 ? r[3] + 1 : 0;
+                        const int64_t la0 = ld_cg(&a.local_cp[xa0]), lb0 = ld_cg(&a.local_cp[xb0]);
+                        const int64_t la1 = ld_cg(&a.local_cp[xa1]), lb1 = ld_cg(&a.local_cp[xb1]);
+                        const int32_t kc = (int32_t)KC;
                         int64_t ct = 0;
-                        for (int q = 0; q < 4; q += 2) {
-                            if (r[q] <= r[q + 1]) {
-                                int64_t xa = r[q], xb = (int64_t)r[q + 1] + 1;
-                                ct += (cp_prefix[xb / KC] + ld_cg(&a.local_cp[xb])) -
-                                      (cp_prefix[xa / KC] + ld_cg(&a.local_cp[xa]));
-                            }
-                        }
+                        if (v0) ct += (cp_prefix[xb0 / kc] + lb0) - (cp_prefix[xa0 / kc] + la0);
+                        if (v1) ct += (cp_prefix[xb1 / kc] + lb1) - (cp_prefix[xa1 / kc] + la1);
                         if (ct == 0) {
                             // benefit only ever shrinks on a host window or on an SSD
                             // window without a host path to fall back to
