@@ -129,16 +129,8 @@ struct EvSmem {
     int32_t ptr[LT_MAXO + 1];   // staged CSR offsets relative to the tile's first event
     int16_t own[LT_TILE];       // staged owner index of every event of the tile
     union {
-        struct {                // during the walks
-            int64_t size[LT_MAXO];
-            int8_t kind[LT_MAXO];
-        };
-        struct {                // afterwards: the tile's period records, tile-local order
-            int32_t start[LT_TILE];
-            int32_t end[LT_TILE];
-            int16_t tensor[LT_TILE];
-            int8_t wraps[LT_TILE];
-        } rec;
+        uint64_t sk[LT_MAXO];   // during the walks: size | kind << 63 of the staged tensors
+        int16_t rec[LT_TILE];   // afterwards: the event opening each period, tile-local order
     };
     int32_t scan32[40];
     int64_t scan[40];
@@ -203,8 +195,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
             sm.ptr[i] = (int32_t)(p - e0 < INT32_MIN ? INT32_MIN : (p - e0 > INT32_MAX ? INT32_MAX : p - e0));
         }
         for (int64_t i = threadIdx.x; i < no; i += blockDim.x) {
-            sm.size[i] = __ldg(a.size + o0 + i);
-            sm.kind[i] = __ldg(a.kind + o0 + i);
+            sm.sk[i] = (uint64_t)__ldg(a.size + o0 + i) | ((uint64_t)(__ldg(a.kind + o0 + i) == 1) << 63);
         }
     }
     if (((uintptr_t)a.acc & 15) == 0 && ne == LT_TILE) {
@@ -236,7 +227,10 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
         }
         const int32_t ex = block_exclusive_max(run, sm.scan32);
 #pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) own[j] = own[j] > ex ? own[j] : ex;
+        for (int j = 0; j < LT_EPT; ++j) {
+            own[j] = own[j] > ex ? own[j] : ex;
+            if (frel + j < LT_TILE) sm.own[frel + j] = (int16_t)own[j];   // resolved, for the record pass
+        }
     }
     int32_t k[LT_EPT + 1];
 #pragma unroll
@@ -259,7 +253,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
             const int32_t k2 = k[j + 1];
             if (k2 <= kk) flags |= LF_NOT_INCREASING;
             else if (k2 - kk > 1) { pmask |= 1u << j; ++cnt; }
-        } else if (sm.kind[o] == 1) {
+        } else if (sm.sk[o] >> 63) {
             const int32_t fk = beg >= 0 ? sm.acc[beg] : __ldg(a.acc + e0 + beg);
             if ((N - 1 - kk) + fk > 0) { pmask |= 1u << j; ++cnt; }
         }
@@ -280,9 +274,9 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
             if (j >= nv) break;
             const int32_t e = frel + j, o = own[j];
             const int32_t kk = k[j];
-            const int64_t sz = sm.size[o];
+            const int64_t sz = (int64_t)(sm.sk[o] & ~(1ull << 63));
             atomic_add_i64(&a.active[kk], sz);                     // per_kernel_active_bytes (:111-117)
-            if (sm.kind[o] == 0) {                                 // compute_memory_timeline (:97-108)
+            if (!(sm.sk[o] >> 63)) {                               // compute_memory_timeline (:97-108)
                 if (e == sm.ptr[o]) atomic_add_i64(&a.diff[kk], sz);
                 if (e == sm.ptr[o + 1] - 1) atomic_add_i64(&a.diff[kk + 1], -sz);
             }
@@ -299,20 +293,8 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     if (pmask && flags == 0) {
         int32_t q = (int32_t)loc;
 #pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) {
-            if (!(pmask & (1u << j))) continue;
-            const int32_t e = frel + j, o = own[j];
-            const int32_t kk = k[j];
-            if (e != sm.ptr[o + 1] - 1) {
-                sm.rec.start[q] = kk + 1; sm.rec.end[q] = k[j + 1] - 1; sm.rec.wraps[q] = 0;
-            } else {
-                const int32_t beg = sm.ptr[o];
-                const int32_t fk = beg >= 0 ? sm.acc[beg] : __ldg(a.acc + e0 + beg);
-                sm.rec.start[q] = (kk + 1) % N; sm.rec.end[q] = ((fk - 1) % N + N) % N; sm.rec.wraps[q] = 1;
-            }
-            sm.rec.tensor[q] = (int16_t)o;
-            ++q;
-        }
+        for (int j = 0; j < LT_EPT; ++j)
+            if (pmask & (1u << j)) sm.rec[q++] = (int16_t)(frel + j);
     }
 
     // ---- tile prefix
@@ -342,13 +324,19 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
             if (pmask & (1u << j)) ++q;
         }
     }
-    // coalesced copy of the staged records
+    // period records, stored coalesced: the staged event and the staged
+    // accesses / owner map give the record back
     for (int64_t i = threadIdx.x; i < tot; i += blockDim.x) {
+        const int32_t e = sm.rec[i], o = sm.own[e], kk = sm.acc[e];
         const int64_t g = prefix + i;
-        a.p_tensor[g] = o0 + sm.rec.tensor[i];
-        a.p_start[g] = sm.rec.start[i];
-        a.p_end[g] = sm.rec.end[i];
-        a.p_wraps[g] = sm.rec.wraps[i];
+        a.p_tensor[g] = o0 + o;
+        if (e != sm.ptr[o + 1] - 1) {
+            a.p_start[g] = kk + 1; a.p_end[g] = sm.acc[e + 1] - 1; a.p_wraps[g] = 0;
+        } else {
+            const int32_t beg = sm.ptr[o];
+            const int32_t fk = beg >= 0 ? sm.acc[beg] : __ldg(a.acc + e0 + beg);
+            a.p_start[g] = (kk + 1) % N; a.p_end[g] = ((fk - 1) % N + N) % N; a.p_wraps[g] = 1;
+        }
     }
     return flags;
 }
