@@ -262,12 +262,9 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     // successors' look-backs only wait for this counting walk
     int64_t tot;
     const int64_t loc = block_exclusive_sum<int64_t>(cnt, sm.scan, &tot);
-#ifndef LT_EXP_NOLB
     if (threadIdx.x < 32) lookback_publish(est, tile, tot);
-#endif
 
     // ---- walk 2: per-kernel active bytes and the timeline difference array
-#ifndef LT_EXP_NORED
     if (!(flags & (LF_ACCESS_RANGE | LF_BAD_PTR))) {
 #pragma unroll
         for (int j = 0; j < LT_EPT; ++j) {
@@ -282,14 +279,10 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
             }
         }
     }
-#endif
     __syncthreads();                         // sizes / kinds no longer needed: records reuse them
 
     // ---- walk 3: period records in reference order (analysis.py:68-82:
     // tensor order, gaps ascending, wrap last) at tile-local offsets
-#ifdef LT_EXP_NOREC
-    pmask = 0;
-#endif
     if (pmask && flags == 0) {
         int32_t q = (int32_t)loc;
 #pragma unroll
@@ -299,12 +292,8 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
 
     // ---- tile prefix
     if (threadIdx.x < 32) {
-#ifndef LT_EXP_NOLB
         int64_t pre;
         lookback_resolve<1>(est, 0, tile, &tot, &pre);
-#else
-        int64_t pre = tile * (LT_TILE / 2);
-#endif
         if (threadIdx.x == 0) sm.prefix = pre;
     }
     __syncthreads();
