@@ -1,7 +1,7 @@
 // planner.cu — Algorithm 1 (reference planner.py:267-370) as one persistent
-// cooperative kernel: every round evaluates all live candidates in parallel,
-// reduces the exact argmax of benefit/cost, and commits it, with two grid
-// barriers per round.
+// cooperative kernel: every round re-derives, in parallel, exactly the
+// candidates the last commit can have changed, reduces the exact argmax of
+// benefit/cost, and commits it, with two grid barriers per round.
 //
 // Exactness — how each reference rule is kept:
 //   * channel searches (bandwidth.py:88-120) run on sorted, pairwise disjoint
@@ -22,9 +22,9 @@
 //     (:295-310);
 //   * commit: bookings + shadows, residual -= size on every covered kernel,
 //     host occupancy (:314-348).
-// Candidates that can never win again are dropped from the live lists:
-// infeasible on both paths, or zero benefit on a path whose window can only
-// shrink (SSD without a host path, or host).
+// Candidates that can never win again are dropped (st GONE): infeasible on
+// both paths, or zero benefit on a path whose window can only shrink (SSD
+// without a host path, or host).
 #include "common.cuh"
 #include "block_scan.cuh"
 #include "planner.cuh"
@@ -345,21 +345,31 @@ __device__ __forceinline__ void l2_prefetch(const void *p) {
 
 // ---------------------------------------------------------------- the kernel
 //
-// Tiles.  Candidates are grouped into tiles of TILE consecutive candidates in
-// ready-time order (a permutation built by the setup; the candidate index,
-// i.e. the (tensor_id, start_kernel) rank, stays the tie-break key).  Every
-// tile has a static time span [min ready, max deadline) that contains every
-// placement its candidates can ever have, and two kernel hulls that contain
-// every kernel its candidates can ever cover.  A tile is re-evaluated in a
-// round only when it can have changed:
-//   * it held the last winner (the winner left the candidate set),
-//   * the last commit's bookings (with their +-iteration images) intersect
-//     its span (a cached placement may have moved or died),
-//   * kernels flipped from critical to non-critical inside one of its hulls
-//     (a cached benefit may have dropped),
-//   * a CPU commit's host occupancy intersects its span (host cap test).
-// Otherwise its cached tile best is provably the tile's current best.  A block
-// whose tiles are all clean keeps last round's block best as well.
+// Tiles.  Candidates are grouped into tiles of TILE (= 32, one warp)
+// consecutive candidates in ready-time order (a permutation built by the
+// setup; the candidate index, i.e. the (tensor_id, start_kernel) rank, stays
+// the tie-break key).  Every tile has a static time span [min ready, max
+// deadline) that contains every placement its candidates can ever have, two
+// kernel hulls that contain every kernel they can ever cover, and a superset
+// hull of its current SSD placements.  Round r:
+//   phase R + E (no barrier between them)
+//     * every warp of the grid takes SSD refits the last commit queued
+//       (candidates whose cached placement its bookings overlap): warp
+//       searches from the cached placement, then lane 0 re-derives the key
+//       and folds it into its block's best;
+//     * each block re-derives its own tiles that can have changed: refits were
+//       queued there (those candidates are left out this round, taken back
+//       the next), it held the last winner, kernels flipped from critical to
+//       non-critical inside one of its kernel hulls, or a CPU commit's
+//       bookings / host occupancy meet its span.  Unchanged candidates reuse
+//       their cached key; a clean tile keeps its tile best, a block with no
+//       change keeps its block best.
+//   grid barrier
+//   phase C (every block, redundantly): exact global argmax, then the commit:
+//     channel merge (all blocks), residual update + flip detection + critical
+//     prefix rebuild (chunk owners), refit queueing for the next round (tile
+//     owners, against the placement hulls), commit record (block 0).
+//   grid barrier
 __device__ __forceinline__ int64_t gtime() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
