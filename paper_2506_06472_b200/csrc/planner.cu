@@ -544,7 +544,6 @@ plan_loop_kernel(PlanArgs a) {
             Key mine = none;
             if (!(st & ST_GONE)) {
                 int ssd = st & 3, host = (st >> 2) & 3;
-                const int64_t size = __ldg(&a.c_size[c]);
                 // round 0: first fits here; later rounds phase R refitted the
                 // SSD placements the last commit overlapped and flagged them
                 const bool need = ssd == S_UNK || (st & ST_REFIT);
@@ -602,7 +601,7 @@ plan_loop_kernel(PlanArgs a) {
                     if (recap) {
                         int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
                         int64_t occ = host_peak(a.occ_s, a.occ_e, a.occ_size, s_nocc, lo, hi);
-                        host = (occ + size > a.host_cap) ? H_CAPFAIL : H_OK;
+                        host = (occ + __ldg(&a.c_size[c]) > a.host_cap) ? H_CAPFAIL : H_OK;
                     }
                 }
                 int dest = ssd == S_OK ? TIO_DEST_SSD : (ssd == S_DEAD && host == H_OK ? TIO_DEST_CPU : 0);
@@ -611,7 +610,6 @@ plan_loop_kernel(PlanArgs a) {
                     nst |= ST_GONE;
                 } else if (dest) {
                     const int q0 = dest == TIO_DEST_SSD ? 0 : 2;
-                    const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
                     // unchanged since its last evaluation: same window on the same
                     // path and no kernel of its covered ranges flipped -> same key
                     bool cached = false;
@@ -627,6 +625,8 @@ plan_loop_kernel(PlanArgs a) {
                         }
                     }
                     if (!cached) {
+                        const int64_t doff = __ldg(&a.c_d[4 * c + q0]), dpre = __ldg(&a.c_d[4 * c + q0 + 1]);
+                        const int64_t size = __ldg(&a.c_size[c]);
                         int32_t r[4];
                         if (moved) {
                             const int64_t os = ld_cg(&a.place[4 * c + q0]);
@@ -764,11 +764,7 @@ plan_loop_kernel(PlanArgs a) {
                     if (pn < a.P) {
                         l2_prefetch(&a.vkey[pn]);
                         l2_prefetch(&a.rng[4 * pn]);
-                        l2_prefetch(&a.c_d[4 * pn]);
-                        if (lane == 0) {
-                            l2_prefetch(&a.st[pn]); l2_prefetch(&a.qround[pn]); l2_prefetch(&a.tcand[pn]);
-                            l2_prefetch(&a.c_size[pn]);
-                        }
+                        if (lane == 0) { l2_prefetch(&a.st[pn]); l2_prefetch(&a.qround[pn]); l2_prefetch(&a.tcand[pn]); }
                     }
                 }
                 const int64_t t = s_dirty[di];
