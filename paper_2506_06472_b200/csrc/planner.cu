@@ -764,7 +764,7 @@ plan_loop_kernel(PlanArgs a) {
                     if (pn < a.P) {
                         l2_prefetch(&a.vkey[pn]);
                         l2_prefetch(&a.rng[4 * pn]);
-                        if (lane == 0) { l2_prefetch(&a.st[pn]); l2_prefetch(&a.qround[pn]); l2_prefetch(&a.tcand[pn]); }
+                        if (lane == 0) { l2_prefetch(&a.st[pn]); l2_prefetch(&a.tcand[pn]); }
                     }
                 }
                 const int64_t t = s_dirty[di];
@@ -776,7 +776,8 @@ plan_loop_kernel(PlanArgs a) {
                 const Key ck = c >= 0 ? kload(&a.vkey[c]) : none;
                 const int4 rr = c >= 0 ? __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c])) : make_int4(1, 0, 1, 0);
                 // queued for a refit by the last commit: phase R owns it this round
-                const bool qround_skip = c >= 0 && round > 0 && ld_cg(&a.qround[c]) == (int32_t)(round - 1);
+                const bool tile_queued = round > 0 && ld_cg(&a.t_refit[t]) == (int32_t)(round - 1);
+                const bool qround_skip = tile_queued && c >= 0 && ld_cg(&a.qround[c]) == (int32_t)(round - 1);
                 const Key mine = qround_skip ? none : eval_lane(c, cid, st, ck, rr);
                 if (round == 0) {
                     // hulls of the tile's SSD placements (offload, prefetch); the
