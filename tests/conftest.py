@@ -68,6 +68,7 @@ def regen(rec):
     from paper_2506_06472_b200 import gen_random_trace, write_trace
     g = rec["gen"]
     tr = gen_random_trace(g["seed"], g["num_kernels"], g["num_tensors"],
-                          size_range=tuple(g["size_range"]), duration_range=tuple(g["duration_range"]))
+                          size_range=tuple(g["size_range"]), duration_range=tuple(g["duration_range"]),
+                          global_fraction=g.get("global_fraction", 0.3))
     assert hashlib.sha256(write_trace(tr)).hexdigest() == rec["trace_sha256"]
     return tr

@@ -18,6 +18,8 @@ Corpora (the reference's own acceptance generators, test_acceptance.py):
   crit2   criterion 2 (:64-101), random.Random(2024), 1000 traces
   crit3   criterion 3 (:104-131), random.Random(7), eligible instances of the
           first 5000 attempts
+  extreme edge magnitudes (benefits past 2^64, fractional rates), all-equal
+          sizes/durations (ties everywhere), 1-3 kernel traces; 300 cases
   c1      config C1: GPT-2 small transformer trace, 4 rate setups
   llama1  Appendix-C Llama-3-8B trace with 1 microbatch (E=4,579; slow)
 
@@ -131,6 +133,48 @@ def crit3(ref):
     return cases
 
 
+def extreme(ref):
+    """Edge magnitudes and ties (not in the reference's own corpora):
+    sizes 2^40-2^50 B with kernel durations up to 1e9 us (benefits past
+    2^64, fractional rates -> exact Fraction transfer durations), all-equal
+    sizes and durations (every ratio ties: the lowest candidate index must
+    win), and 1-3 kernel traces (no gaps, only wraps)."""
+    rng = random.Random(4242)
+    cases = []
+    for i in range(300):
+        kind = i % 3
+        if kind == 0:
+            nk, nt = rng.randint(4, 48), rng.randint(2, 24)
+            sr, dr = (1 << 40, 1 << 50), (1_000_000, 1_000_000_000)
+            ssd = rng.choice((1_100_000, 33_000_000, 1_234_567.5, 987_654.321))
+        elif kind == 1:
+            nk, nt = rng.randint(4, 64), rng.randint(2, 32)
+            s, d = rng.choice((50_000_000, 1 << 30)), rng.choice((1_000, 7))
+            sr, dr = (s, s), (d, d)
+            ssd = s / (d * rng.choice((0.25, 0.5, 1.5)))
+        else:
+            nk, nt = rng.randint(1, 3), rng.randint(1, 6)
+            sr, dr = (1_000, 900_000), (10, 400)
+            ssd = rng.choice((50_000, 5_000_000, 123_456.75))
+        seed = rng.randint(0, 10**9)
+        gf = rng.choice((0.0, 0.3, 0.8))
+        trace = ref.gen_random_trace(seed, nk, nt, size_range=sr, duration_range=dr, global_fraction=gf)
+        peak = ref.compute_memory_timeline(trace).peak()
+        floor = max(ref.per_kernel_active_bytes(trace), default=0)
+        capacity = max(floor, int(peak * rng.choice((0.5, 0.7, 0.9))))
+        if rng.random() < 0.3:
+            rates = ref.ChannelRates.symmetric(ssd, host=ssd * 2)
+            host_cap = rng.choice((0, int(peak // 3)))
+        else:
+            rates = ref.ChannelRates.symmetric(ssd)
+            host_cap = 0
+        rec = _record(ref, trace, capacity, rates, host_cap)
+        rec["gen"] = {"seed": seed, "num_kernels": nk, "num_tensors": nt, "size_range": list(sr),
+                      "duration_range": list(dr), "global_fraction": gf}
+        cases.append(rec)
+    return cases
+
+
 C1_SETUPS = [  # (compute_rate, ssd, host, host_cap) — SURVEY §8d
     (1_000_000_000, 16_000, None, 0),
     (1_000_000_000, 64_000, None, 0),
@@ -191,18 +235,23 @@ def _sim_record(ref, trace, plan_text, capacity, rates):
 
 
 def sim(ref):
-    """simulate / simulate_on_demand on the criterion-2 corpus (every case,
-    with its reference plan) and on C1 + llama1."""
+    """simulate / simulate_on_demand on the criterion-2 and extreme corpora
+    (every case, with its reference plan)."""
     cases = []
-    for rec in json.load(gzip.open(os.path.join(HERE, "crit2.json.gz"), "rt")):
-        g = rec["gen"]
-        trace = ref.gen_random_trace(g["seed"], g["num_kernels"], g["num_tensors"],
-                                     size_range=tuple(g["size_range"]), duration_range=tuple(g["duration_range"]))
-        so, sp, ho, hp = rec["rates"]
-        rates = ref.ChannelRates(so, sp, ho, hp)
-        out = _sim_record(ref, trace, rec.get("plan"), rec["capacity"], rates)
-        out.update({"corpus": "crit2", "gen": g, "trace_sha256": rec["trace_sha256"]})
-        cases.append(out)
+    for corpus in ("crit2", "extreme"):
+        for rec in json.load(gzip.open(os.path.join(HERE, f"{corpus}.json.gz"), "rt")):
+            if "unsat_kernel" in rec:
+                continue
+            g = rec["gen"]
+            trace = ref.gen_random_trace(g["seed"], g["num_kernels"], g["num_tensors"],
+                                         size_range=tuple(g["size_range"]),
+                                         duration_range=tuple(g["duration_range"]),
+                                         global_fraction=g.get("global_fraction", 0.3))
+            so, sp, ho, hp = rec["rates"]
+            rates = ref.ChannelRates(so, sp, ho, hp)
+            out = _sim_record(ref, trace, rec.get("plan"), rec["capacity"], rates)
+            out.update({"corpus": corpus, "gen": g, "trace_sha256": rec["trace_sha256"]})
+            cases.append(out)
     return cases
 
 
@@ -219,7 +268,7 @@ def main(argv=None):
     ap.add_argument("--only", default=None)
     args = ap.parse_args(argv)
     ref = _ref()
-    todo = {"crit2": crit2, "crit3": crit3, "c1": c1, "sim": sim}
+    todo = {"crit2": crit2, "crit3": crit3, "extreme": extreme, "c1": c1, "sim": sim}
     if args.llama1:
         todo["llama1"] = llama1
     for name, fn in todo.items():

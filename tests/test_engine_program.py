@@ -47,7 +47,7 @@ def _check(tr, xs, starts, kseq, loc):
 
 def test_engine_program_consistent_on_corpus():
     sims = load_golden("sim")
-    plans = {r["trace_sha256"]: r for r in load_golden("crit2")}
+    plans = {r["trace_sha256"]: r for r in load_golden("crit2") + load_golden("extreme")}
     n = 0
     for rec in sims:
         base = plans[rec["trace_sha256"]]

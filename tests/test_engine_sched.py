@@ -28,8 +28,9 @@ def _cmp(got, want):
 
 
 def test_scheduler_matches_reference_simulate_on_crit2_corpus():
+    """Criterion-2 corpus plus the extreme-magnitude / tie corpus."""
     sims = load_golden("sim")
-    plans = {r["trace_sha256"]: r for r in load_golden("crit2")}
+    plans = {r["trace_sha256"]: r for r in load_golden("crit2") + load_golden("extreme")}
     checked = 0
     for rec in sims:
         tr = regen({**rec, "gen": rec["gen"]})

@@ -63,7 +63,7 @@ def _check_case(tr, rec):
 
 # ---------------------------------------------------------------- golden corpora
 
-@pytest.mark.parametrize("corpus", ["crit2", "crit3"])
+@pytest.mark.parametrize("corpus", ["crit2", "crit3", "extreme"])
 def test_fuzz_corpus_bit_exact_vs_reference(corpus):
     for rec in load_golden(corpus):
         _check_case(regen(rec), rec)

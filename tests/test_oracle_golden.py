@@ -46,10 +46,10 @@ def _check_plan(arrays, rec, lo=None):
     assert got == rec["committed"]
 
 
-@pytest.mark.parametrize("corpus", ["crit2", "crit3"])
+@pytest.mark.parametrize("corpus", ["crit2", "crit3", "extreme"])
 def test_oracle_matches_reference_fuzz_corpus(corpus):
     cases = load_golden(corpus)
-    assert len(cases) >= 1000 if corpus == "crit2" else len(cases) >= 3000
+    assert len(cases) >= {"crit2": 1000, "crit3": 3000, "extreme": 300}[corpus]
     for rec in cases:
         tr = regen(rec)
         a = tr.arrays()
