@@ -148,8 +148,9 @@ def cpu_baseline(config: str, rounds_total: int | None, sample_rounds: int = 40,
     from oracle import oracle as O
     tr, cap, rates, hc, _ = _trace(config)
     a = tr.arrays()
-    if threads:
-        os.environ["OMP_NUM_THREADS"] = str(threads)
+    # every host thread this process may use (torchrun exports OMP_NUM_THREADS=1;
+    # the oracle's libgomp reads the variable when the library is first loaded)
+    os.environ["OMP_NUM_THREADS"] = str(threads or len(os.sched_getaffinity(0)))
     L = O.lib()
     t0 = time.perf_counter()
     lo = O.lifetime(a)
