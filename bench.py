@@ -417,10 +417,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if extra is not None:
         extra.pop("clocks", None)
         rx = extra.pop("rounds")
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             extra["cpu_baseline"] = cpu_baseline(args.secondary, rx, sample_rounds=args.ref_rounds)
         line[args.secondary] = extra
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:     # rank 0 at N = 1 only (the reference arm covers N > 1)
         line["cpu_baseline"] = cpu_baseline(args.config, rounds, sample_rounds=args.ref_rounds_c3
                                             if args.config == "c3" else args.ref_rounds)
     if world > 1 and m_sh is not None:
