@@ -330,7 +330,10 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
         "roofline": {"kernel": "lifetime (k_tile_owners + k_events + k_kernels)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": B_L,
-                     "share_of_step": life_ms / tot_ms},
+                     "share_of_step": life_ms / tot_ms,
+                     "note": "the step's dominant kernel is plan_loop_kernel (see 'planner'): sequential greedy "
+                             "rounds, latency-bound, no byte/flop roofline (SURVEY 8d); this is the HBM "
+                             "roofline of the lifetime kernels"},
         "planner": {"kernel": "plan_loop_kernel (the step's dominant kernel)",
                     "bound": "latency (2 grid barriers + dependent L2 loads per round)",
                     "rounds": rounds, "commits": int(info.num_commits),
