@@ -39,8 +39,11 @@ enum : unsigned long long {
 constexpr int LT_EPT = 8;                           // events per thread
 constexpr int LT_TILE = LIFETIME_THREADS * LT_EPT;  // events per tile
 constexpr int LT_MAXO = LT_TILE + 2;                // staged tensors per tile
+#ifndef KT_THREADS
+#define KT_THREADS 256
+#endif
 constexpr int KT_EPT = 8;                           // kernels per thread
-constexpr int KT_TILE = LIFETIME_THREADS * KT_EPT;
+constexpr int KT_TILE = KT_THREADS * KT_EPT;
 
 __host__ __device__ int64_t lifetime_event_tiles(int64_t E) { return (E + LT_TILE - 1) / LT_TILE; }
 __host__ __device__ int64_t lifetime_kernel_tiles(int64_t N) { return (N + KT_TILE - 1) / KT_TILE; }
@@ -367,7 +370,7 @@ k_events(LifetimeArgs a) {
 }
 
 // ---------------------------------------------------------------- kernels
-__global__ void __launch_bounds__(LIFETIME_THREADS, 4)
+__global__ void __launch_bounds__(KT_THREADS, 1024 / KT_THREADS)
 k_kernels(LifetimeArgs a) {
     __shared__ int64_t scan[40];
     __shared__ int64_t s_pre[2];
@@ -467,7 +470,7 @@ int launch_lifetime(const LifetimeArgs &args, cudaStream_t stream) {
     k_events<<<(unsigned)nb, LIFETIME_THREADS, sizeof(EvSmem), stream>>>(args);
     count_launch();
     if (NTk > 0) {
-        k_kernels<<<(unsigned)NTk, LIFETIME_THREADS, 0, stream>>>(args);
+        k_kernels<<<(unsigned)NTk, KT_THREADS, 0, stream>>>(args);
         count_launch();
     }
     TIO_CUDA(cudaGetLastError());

@@ -33,7 +33,14 @@ def main():
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         ts = sorted(ts[2:])
-        print(os.path.basename(so), cfg, "lifetime ms min %.4f med %.4f" % (ts[0], ts[len(ts) // 2]), flush=True)
+        import hashlib
+        import numpy as np
+        out = dt.lifetime()
+        h = hashlib.sha256(b"".join(np.ascontiguousarray(np.asarray(out[k])).tobytes() for k in
+                                    ("timeline", "active", "period_tensor", "period_start", "period_end",
+                                     "period_wraps"))).hexdigest()[:16]
+        print(os.path.basename(so), cfg, "lifetime ms min %.4f med %.4f" % (ts[0], ts[len(ts) // 2]), h,
+              flush=True)
 
 
 if __name__ == "__main__":
