@@ -437,14 +437,13 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     }
     // ---- tiles: candidates in ready-time order (planner.cu).  The planner's
     // candidate columns are stored in tile order (position p) so a tile's
-    // data is contiguous; tcand[p] = candidate index (the tie-break key),
-    // cpos[c] = its position.
+    // data is contiguous; tcand[p] = candidate index (the tie-break key; the
+    // argmax key carries both).
     const int64_t ntiles = (P + TILE - 1) / TILE;
     uint32_t *tcand;
-    int32_t *cpos, *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;
+    int32_t *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;
     int64_t *t_lo, *t_hi;
     Key *tile_best;
-    PTRY(A.alloc(&cpos, P));
     PTRY(A.alloc(&t_lo, ntiles)); PTRY(A.alloc(&t_hi, ntiles));
     PTRY(A.alloc(&t_ka_lo, ntiles)); PTRY(A.alloc(&t_ka_hi, ntiles));
     PTRY(A.alloc(&t_kb_lo, ntiles)); PTRY(A.alloc(&t_kb_hi, ntiles));
@@ -475,7 +474,7 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
         }
         tcand = in_tmp ? v1 : v0;
         if (P > 0) {
-            k_permute_candidates<<<grid_for(P), 256, 0, s>>>(tcand, P, src, dst, cpos); ::tio::count_launch();
+            k_permute_candidates<<<grid_for(P), 256, 0, s>>>(tcand, P, src, dst); ::tio::count_launch();
             k_tile_spans<<<grid_for(ntiles * 32), 256, 0, s>>>(nullptr, P, ntiles, TILE, N, dst.ready, dst.deadline,
                                                               dst.wraps, dst.sk, dst.ek, dst.first, dst.last, nullptr, t_lo,
                                                               t_hi, t_ka_lo, t_ka_hi, t_kb_lo, t_kb_hi); ::tio::count_launch();
@@ -485,7 +484,7 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     c_size = dst.size; c_ready = dst.ready; c_deadline = dst.deadline; c_d = dst.d; c_tid = dst.tid;
     c_sk = dst.sk; c_ek = dst.ek; c_first = dst.first; c_last = dst.last; c_tpos = dst.tpos;
     c_wraps = dst.wraps; st = dst.st;
-    a.ntiles = ntiles; a.tcand = tcand; a.cpos = cpos; a.t_lo = t_lo; a.t_hi = t_hi;
+    a.ntiles = ntiles; a.tcand = tcand; a.t_lo = t_lo; a.t_hi = t_hi;
     a.t_ka_lo = t_ka_lo; a.t_ka_hi = t_ka_hi; a.t_kb_lo = t_kb_lo; a.t_kb_hi = t_kb_hi; a.tile_best = tile_best;
     int G = 0;
     PTRY(plan_loop_grid(&G));

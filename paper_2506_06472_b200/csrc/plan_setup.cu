@@ -146,7 +146,7 @@ __global__ void k_tile_spans(const uint32_t *tcand, int64_t P, int64_t ntiles, i
 }
 
 // candidate columns from planner order (index c) into tile order (position p)
-__global__ void k_permute_candidates(const uint32_t *tcand, int64_t P, CandCols src, CandCols dst, int32_t *cpos) {
+__global__ void k_permute_candidates(const uint32_t *tcand, int64_t P, CandCols src, CandCols dst) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = tcand[p];
         dst.size[p] = src.size[c]; dst.ready[p] = src.ready[c]; dst.deadline[p] = src.deadline[c];
@@ -155,7 +155,6 @@ __global__ void k_permute_candidates(const uint32_t *tcand, int64_t P, CandCols 
         dst.sk[p] = src.sk[c]; dst.ek[p] = src.ek[c]; dst.first[p] = src.first[c]; dst.last[p] = src.last[c];
         dst.tpos[p] = src.tpos[c];
         dst.wraps[p] = src.wraps[c]; dst.st[p] = src.st[c];
-        cpos[c] = (int32_t)p;
     }
 }
 

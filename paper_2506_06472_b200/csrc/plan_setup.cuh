@@ -42,7 +42,7 @@ struct CandCols {
     int32_t *sk, *ek, *first, *last, *tpos;
     int8_t *wraps, *st;
 };
-__global__ void k_permute_candidates(const uint32_t *tcand, int64_t P, CandCols src, CandCols dst, int32_t *cpos);
+__global__ void k_permute_candidates(const uint32_t *tcand, int64_t P, CandCols src, CandCols dst);
 __global__ void k_ready_keys(const int64_t *ready, int64_t P, uint64_t *keys, uint32_t *vals);
 __global__ void k_tile_spans(const uint32_t *tcand, int64_t P, int64_t ntiles, int tile, int64_t N,
                              const int64_t *ready, const int64_t *deadline, const int8_t *wraps,

@@ -280,8 +280,13 @@ __device__ __forceinline__ bool overlaps(int64_t x, int64_t d, const int64_t *s,
 
 // ---------------------------------------------------------------- argmax keys
 // The round's argmax carries 4 words: the exact benefit (u128), the cost and
-// meta = 4 * candidate index + destination.  Everything else about the
-// winner is re-read from the candidate arrays once it is known.
+// meta = candidate index << 33 | column position << 2 | destination (both
+// < 2^31), compared unsigned: the tie-break is the candidate index.  The rest
+// of the winner is re-read from its column once it is known.
+__device__ __forceinline__ int64_t key_meta(int64_t cid, int64_t c, int dest) {
+    return (int64_t)(((uint64_t)cid << 33) | ((uint64_t)c << 2) | (uint64_t)dest);
+}
+
 __device__ __forceinline__ bool kbetter(const Key &a, const Key &b) {
     const bool az = (a.blo | a.bhi) == 0, bz = (b.blo | b.bhi) == 0;
     if (az) return false;
@@ -289,7 +294,7 @@ __device__ __forceinline__ bool kbetter(const Key &a, const Key &b) {
     const u128 ab = ((u128)a.bhi << 64) | a.blo, bb = ((u128)b.bhi << 64) | b.blo;
     if (ratio_gt(ab, a.cost, bb, b.cost)) return true;
     if (ratio_gt(bb, b.cost, ab, a.cost)) return false;
-    return a.meta < b.meta;   // tie: lowest candidate index = first in (tensor_id, start_kernel) order
+    return (uint64_t)a.meta < (uint64_t)b.meta;   // tie: lowest candidate index = first in (tensor_id, start_kernel) order
 }
 
 __device__ __forceinline__ Key kshfl(const Key &k, int src) {
@@ -614,7 +619,7 @@ plan_loop_kernel(PlanArgs a) {
                     // path and no kernel of its covered ranges flipped -> same key
                     bool cached = false;
                     if (round > 0 && !moved && !need) {
-                        if ((ck.meta & 3) == dest && (ck.meta >> 2) == cid) {
+                        if ((ck.meta & 3) == dest && ((uint64_t)ck.meta >> 33) == (uint64_t)cid) {
                             cached = true;
                             if (s_flip[0] > 0) {
                                 const int64_t fl = s_flip[1], fh = s_flip[2];
@@ -662,10 +667,10 @@ plan_loop_kernel(PlanArgs a) {
                             mine.blo = (uint64_t)bf;
                             mine.bhi = (uint64_t)(bf >> 64);
                             mine.cost = doff + dpre;
-                            mine.meta = 4 * (int64_t)cid + dest;
+                            mine.meta = key_meta(cid, c, dest);
                         }
                         // the key (zero benefit included) for later rounds
-                        kstore(&a.vkey[c], Key{mine.blo, mine.bhi, doff + dpre, 4 * (int64_t)cid + dest});
+                        kstore(&a.vkey[c], Key{mine.blo, mine.bhi, doff + dpre, key_meta(cid, c, dest)});
                     }
                 }
                 if (nst != st) a.st[c] = nst;
@@ -864,7 +869,7 @@ plan_loop_kernel(PlanArgs a) {
             if (threadIdx.x == 0) {
                 WinInfo wi;
                 wi.blo = w.blo; wi.bhi = w.bhi; wi.cost = w.cost;
-                wi.idx = (w.blo | w.bhi) != 0 ? __ldg(&a.cpos[w.meta >> 2]) : 0;   // column position
+                wi.idx = (w.blo | w.bhi) != 0 ? (int64_t)(((uint64_t)w.meta >> 2) & 0x7fffffffu) : 0;   // column position
                 wi.dest = w.meta & 3;
                 if ((w.blo | w.bhi) != 0) {
                     const int64_t c = wi.idx;

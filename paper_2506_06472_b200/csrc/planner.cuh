@@ -22,7 +22,7 @@ enum {
     PS_DBG = 17 /* 16 debug counters */, PS_RQ = 33 /* 2 refit-queue counts */, PS_COUNT = 35
 };
 
-// argmax key of a candidate (benefit 0 = none); meta = 4 * index + destination
+// argmax key of a candidate (benefit 0 = none); meta = index << 33 | column << 2 | destination
 struct Key {
     uint64_t blo, bhi;     // benefit = size x critical duration (u128)
     int64_t cost;          // offload + prefetch duration
@@ -57,7 +57,6 @@ struct PlanArgs {
     // tiles: candidates in ready-time order, TILE per tile
     int64_t ntiles;
     const uint32_t *tcand;         // [P] candidate index (planner order) at tile position
-    const int32_t *cpos;           // [P] tile position of a candidate index
     const int64_t *t_lo, *t_hi;    // [ntiles] span [min ready, max deadline)
     const int32_t *t_ka_lo, *t_ka_hi, *t_kb_lo, *t_kb_hi;  // [ntiles] kernel hulls (lo > hi: empty)
     Key *tile_best;                // [ntiles]
