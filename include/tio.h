@@ -40,7 +40,8 @@ enum {
     TIO_ERR_NOMEM = -5,
     TIO_ERR_INTERNAL = -6,       /* planner.py:316-320 divergence assert / invariant   */
     TIO_ERR_OVERFLOW = -7,       /* value outside the int64 domain                     */
-    TIO_ERR_SIMULATION = -8      /* simulator.py:51-52 SimulationError                 */
+    TIO_ERR_SIMULATION = -8,     /* simulator.py:51-52 SimulationError                 */
+    TIO_ERR_CONFIG = -9          /* simulator.py:55-56 ConfigurationError              */
 };
 
 enum { TIO_MEM_HOST = 0, TIO_MEM_DEVICE = 1 };
@@ -216,6 +217,17 @@ typedef struct tio_sim_report {
 int tio_simulate(const tio_trace_desc *trace, const tio_entry *entries, int64_t num_entries,
                  int64_t capacity, const tio_rates *rates, tio_sim_report *report,
                  int64_t *per_kernel_start, int64_t *stall_per_kernel, int64_t *per_kernel_resident);
+
+/* Replaces simulator.py:549-560 simulate_layer_granularity (policy
+ * simulator.py:95-177): no plan; when the memory-timeline peak exceeds
+ * capacity, each layer block's still-needed tensors are offloaded to the SSD
+ * tier as one batch when execution leaves the block, and prefetch batches run
+ * one block ahead.  kernel_layer[N] / tensor_layer[T]: layer ids, INT64_MIN =
+ * none (the caller applies any tensor layer map).  TIO_ERR_CONFIG
+ * (ConfigurationError) for a missing layer id once the policy engages. */
+int tio_simulate_layers(const tio_trace_desc *trace, const int64_t *kernel_layer, const int64_t *tensor_layer,
+                        int64_t capacity, const tio_rates *rates, tio_sim_report *report,
+                        int64_t *per_kernel_start, int64_t *stall_per_kernel, int64_t *per_kernel_resident);
 
 /* The engine program behind a run: every transfer the scheduler starts (in
  * start order) and every kernel's start time, model microseconds.

@@ -27,6 +27,7 @@ TIO_ERR_NOMEM = -5
 TIO_ERR_INTERNAL = -6
 TIO_ERR_OVERFLOW = -7
 TIO_ERR_SIMULATION = -8
+TIO_ERR_CONFIG = -9
 
 TIO_MEM_HOST = 0
 TIO_MEM_DEVICE = 1
@@ -100,7 +101,7 @@ ENTRY_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("trigger_u
 EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_device_info", "tio_trace_create",
            "tio_trace_destroy", "tio_lifetime", "tio_lifetime_view_get", "tio_lifetime_copy_out",
            "tio_plan_create", "tio_plan_create2", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
-           "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate",
+           "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate", "tio_simulate_layers",
            "tio_engine_replay", "tio_pack", "tio_unpack", "tio_schedule", "tio_trace_parse",
            "tio_parsed_sizes", "tio_parsed_copy", "tio_parsed_destroy")
 

@@ -722,9 +722,10 @@ int tio_plan_host(const tio_trace_desc *desc, int64_t capacity, const tio_rates 
 }  // extern "C"
 
 // ---- engine scheduler (simulator.py:178-560) ----------------------------------
-extern "C" int tio_simulate(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries, int64_t capacity,
-                            const tio_rates *rates, tio_sim_report *report, int64_t *per_kernel_start,
-                            int64_t *stall_per_kernel, int64_t *per_kernel_resident) {
+static int simulate_impl(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries, int64_t capacity,
+                         const tio_rates *rates, const int64_t *k_layer, const int64_t *t_layer,
+                         tio_sim_report *report, int64_t *per_kernel_start, int64_t *stall_per_kernel,
+                         int64_t *per_kernel_resident) {
     if (!d || !rates || !report || (num_entries > 0 && !entries)) return fail(TIO_ERR_INVALID, "null argument");
     SchedInput in;
     in.N = d->num_kernels; in.T = d->num_tensors;
@@ -743,6 +744,8 @@ extern "C" int tio_simulate(const tio_trace_desc *d, const tio_entry *entries, i
     in.rate[0] = rates->ssd_offload; in.rate[1] = rates->ssd_prefetch;
     in.rate[2] = rates->host_offload; in.rate[3] = rates->host_prefetch;
     in.has_host = rates->has_host;
+    in.layer_policy = k_layer != nullptr;
+    in.k_layer = k_layer; in.t_layer = t_layer;
     for (int64_t t = 0; t < in.T; ++t)
         for (int64_t j = in.ptr[t]; j < in.ptr[t + 1]; ++j)
             if (in.acc[j] < 0 || in.acc[j] >= in.N) return fail(TIO_ERR_INVALID, "access out of range");
@@ -765,6 +768,25 @@ extern "C" int tio_simulate(const tio_trace_desc *d, const tio_entry *entries, i
         if (per_kernel_resident) memcpy(per_kernel_resident, out.resident.data(), nb);
     }
     return TIO_OK;
+}
+
+extern "C" int tio_simulate(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries, int64_t capacity,
+                            const tio_rates *rates, tio_sim_report *report, int64_t *per_kernel_start,
+                            int64_t *stall_per_kernel, int64_t *per_kernel_resident) {
+    return simulate_impl(d, entries, num_entries, capacity, rates, nullptr, nullptr, report, per_kernel_start,
+                         stall_per_kernel, per_kernel_resident);
+}
+
+extern "C" int tio_simulate_layers(const tio_trace_desc *d, const int64_t *kernel_layer, const int64_t *tensor_layer,
+                                   int64_t capacity, const tio_rates *rates, tio_sim_report *report,
+                                   int64_t *per_kernel_start, int64_t *stall_per_kernel,
+                                   int64_t *per_kernel_resident) {
+    if (!d || (d->num_kernels > 0 && !kernel_layer) || (d->num_tensors > 0 && !tensor_layer))
+        return fail(TIO_ERR_INVALID, "null argument");
+    static const int64_t none = INT64_MIN;
+    return simulate_impl(d, nullptr, 0, capacity, rates, kernel_layer ? kernel_layer : &none,
+                         tensor_layer ? tensor_layer : &none, report, per_kernel_start, stall_per_kernel,
+                         per_kernel_resident);
 }
 
 // The engine program: the scheduler's transfers (start order per run) and

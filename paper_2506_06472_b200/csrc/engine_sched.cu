@@ -67,6 +67,14 @@ struct Engine {
     std::priority_queue<Ev, std::vector<Ev>, EvLess> events;
     int64_t seq = 0, resident = 0, peak = 0;
     int64_t order = 0;                          // processing order of transfer starts and kernel launches
+    // layer policy (simulator.py:95-177): blocks of consecutive kernels with
+    // one layer id; tensors of each layer in id order; in-flight batch prefetches
+    bool pol = false;
+    std::vector<int64_t> blk_layer, blk_first, blk_last;
+    std::vector<int64_t> block_of;
+    std::unordered_map<int64_t, std::vector<int64_t>> layer_tensors;
+    std::vector<char> outstanding;              // per transfer: an in-flight batch prefetch
+    int64_t n_out = 0, exec_block = 0, next_batch = 0;
 
     Engine(const SchedInput &i, SchedOutput &o, std::string &e)
         : in(i), out(o), err(e), N(i.N), T(i.T), cap(i.capacity) {}
@@ -157,6 +165,7 @@ struct Engine {
         tr.urgent = urgent; tr.emergency = emergency; tr.started = false; tr.end = 0;
         trs.push_back(tr);
         tr_sched.push_back(-1);
+        outstanding.push_back(0);
         return (int)trs.size() - 1;
     }
 
@@ -196,6 +205,99 @@ struct Engine {
             loc[tr.t] = LOC_GPU;
         }
         pump_all(now);
+        if (pol) on_transfer_complete(x, now);
+    }
+
+    // ---- layer policy hooks (simulator.py:137-177)
+    void maybe_issue(int64_t now) {
+        const int64_t nblocks = (int64_t)blk_layer.size();
+        while (n_out == 0 && next_batch < nblocks && next_batch <= exec_block + 1) {
+            const int64_t batch = next_batch++;
+            // the block's active tensors, in id order (_block_tensors)
+            std::vector<int64_t> ts;
+            for (int64_t k = blk_first[batch]; k <= blk_last[batch]; ++k)
+                ts.insert(ts.end(), act.begin() + act_ptr[k], act.begin() + act_ptr[k + 1]);
+            std::sort(ts.begin(), ts.end(), [&](int64_t x, int64_t y) { return in.tid[x] < in.tid[y]; });
+            ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+            for (int64_t t : ts) {
+                if ((loc[t] == LOC_SSD || loc[t] == LOC_HOST) && engaged[t] < 0) {
+                    const int x = new_tr(t, A_PRE, loc[t], false, false);
+                    enqueue(x, now);
+                    outstanding[x] = 1;
+                    ++n_out;
+                }
+            }
+        }
+    }
+    void on_transfer_complete(int x, int64_t now) {
+        if (outstanding[x]) { outstanding[x] = 0; --n_out; }
+        if (n_out == 0) maybe_issue(now);
+    }
+    void on_kernel_launched(int64_t k, int64_t now) {
+        exec_block = block_of[k];
+        maybe_issue(now);
+    }
+    void on_kernel_end(int64_t k, int64_t now) {
+        const int64_t b = block_of[k];
+        if (k != blk_last[b]) return;
+        // the layer's still-needed GPU tensors go out as one batch, id order
+        auto it = layer_tensors.find(blk_layer[b]);
+        if (it != layer_tensors.end())
+            for (int64_t t : it->second) {
+                int64_t use;
+                if (loc[t] == LOC_GPU && engaged[t] < 0 && next_use(t, k, &use))
+                    enqueue(new_tr(t, A_OFF, LOC_SSD, false, false), now);
+            }
+        maybe_issue(now);
+    }
+    int setup_layer_policy() {
+        // simulator.py:549-560: engaged only when the timeline peak exceeds capacity
+        std::vector<int64_t> diff(N + 1, 0);
+        int64_t glob = 0;
+        for (int64_t t = 0; t < T; ++t) {
+            if (in.ptr[t + 1] == in.ptr[t]) continue;
+            if (is_global(t)) { glob += in.size[t]; continue; }
+            diff[in.acc[in.ptr[t]]] += in.size[t];
+            diff[in.acc[in.ptr[t + 1] - 1] + 1] -= in.size[t];
+        }
+        int64_t run = 0, pk = 0;
+        for (int64_t k = 0; k < N; ++k) {
+            run += diff[k];
+            if (glob + run > pk) pk = glob + run;
+        }
+        if (pk <= cap) return TIO_OK;
+        const int64_t NONE = INT64_MIN;
+        for (int64_t k = 0; k < N; ++k)
+            if (in.k_layer[k] == NONE) {
+                char b[96];
+                snprintf(b, sizeof(b), "kernel %lld has no layer id", (long long)k);
+                err = b;
+                return TIO_ERR_CONFIG;
+            }
+        for (int64_t t = 0; t < T; ++t)
+            if (in.t_layer[t] == NONE) {
+                char b[96];
+                snprintf(b, sizeof(b), "tensor %lld has no layer id", (long long)in.tid[t]);
+                err = b;
+                return TIO_ERR_CONFIG;
+            }
+        block_of.assign(N, 0);
+        for (int64_t k = 0; k < N; ++k) {
+            if (!blk_layer.empty() && blk_layer.back() == in.k_layer[k]) {
+                blk_last.back() = k;
+            } else {
+                blk_layer.push_back(in.k_layer[k]);
+                blk_first.push_back(k);
+                blk_last.push_back(k);
+            }
+            block_of[k] = (int64_t)blk_layer.size() - 1;
+        }
+        std::vector<int64_t> by_id(T);
+        for (int64_t t = 0; t < T; ++t) by_id[t] = t;
+        std::sort(by_id.begin(), by_id.end(), [&](int64_t x, int64_t y) { return in.tid[x] < in.tid[y]; });
+        for (int64_t t : by_id) layer_tensors[in.t_layer[t]].push_back(t);
+        pol = true;
+        return TIO_OK;
     }
 
     // simulator.py:384-397
@@ -408,6 +510,10 @@ struct Engine {
         engaged.assign(T, -1);
         int rc0 = install_plan();
         if (rc0 != TIO_OK) return rc0;
+        if (in.layer_policy) {
+            rc0 = setup_layer_policy();
+            if (rc0 != TIO_OK) return rc0;
+        }
         out.initial_loc = loc;
         // initial residency (simulator.py:234-239)
         for (int64_t t = 0; t < T; ++t)
@@ -420,6 +526,7 @@ struct Engine {
         out.resident.assign(N, 0);
         out.kseq.assign(N, 0);
         int64_t now = 0;
+        if (pol) maybe_issue(now);                  // on_start (simulator.py:477-478)
         for (int64_t k = 0; k < N; ++k) {
             const int64_t ready = now;
             while (true) {
@@ -443,6 +550,7 @@ struct Engine {
                 if (loc[t] == LOC_NONE) { loc[t] = LOC_GPU; grow(in.size[t]); }
             }
             out.resident[k] = resident;
+            if (pol) on_kernel_launched(k, now);
             now += in.dur[k];
             for (int64_t j = act_ptr[k]; j < act_ptr[k + 1]; ++j) {
                 const int64_t t = act[j];
@@ -452,6 +560,7 @@ struct Engine {
                 }
             }
             pump_all(now);
+            if (pol) on_kernel_end(k, now);
         }
         out.total_time = now;
         out.ideal_time = iteration;

@@ -46,6 +46,11 @@ struct SchedInput {
     int64_t capacity;
     double rate[4];             // ssd.off, ssd.pre, host.off, host.pre
     int has_host;
+    // layer-granularity baseline policy (simulator.py:95-177, :549-560):
+    // engaged when the memory-timeline peak exceeds capacity; layers per
+    // kernel and per tensor, INT64_MIN = none
+    int layer_policy = 0;
+    const int64_t *k_layer = nullptr, *t_layer = nullptr;
 };
 
 struct SchedOutput {
@@ -57,7 +62,7 @@ struct SchedOutput {
     std::vector<int8_t> initial_loc;                // location at t = 0 (after plan folding)
 };
 
-// Returns 0, or TIO_ERR_SIMULATION / TIO_ERR_INVALID with *err set.
+// Returns 0, or TIO_ERR_SIMULATION / TIO_ERR_INVALID / TIO_ERR_CONFIG with *err set.
 int engine_schedule(const SchedInput &in, SchedOutput *out, std::string *err);
 
 }  // namespace tio

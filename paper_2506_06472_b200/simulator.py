@@ -8,8 +8,9 @@ Belady emergency eviction, steady-state plan folding.  The same scheduler
 drives the GPU executor (`paper_2506_06472_b200.engine`), so this is also
 the step-time predictor of a plan before it runs.
 
-The layer-granularity baseline (`simulate_layer_granularity`, :550-560) is a
-ZeRO-Infinity-style comparison policy, out of the hot-path scope.
+The layer-granularity baseline (`simulate_layer_granularity`, :549-560,
+policy :95-177) runs on the same scheduler with the
+layer-batch hooks (`tio_simulate_layers`).
 """
 
 from __future__ import annotations
@@ -25,7 +26,7 @@ import numpy as np
 from . import _native
 from .bandwidth import ChannelRates
 from .planner import MigrationPlan, PlanEntry, _rates_struct
-from .trace import Trace
+from .trace import NONE_I64, Trace
 
 
 class SimulationError(RuntimeError):
@@ -78,7 +79,7 @@ def entries_array(entries) -> np.ndarray:
 _CHANNELS = ("ssd.offload", "ssd.prefetch", "host.offload", "host.prefetch")
 
 
-def _run(trace: Trace, entries: np.ndarray, capacity: int, rates: ChannelRates) -> SimReport:
+def _run(trace: Trace, entries: np.ndarray, capacity: int, rates: ChannelRates, layers=None) -> SimReport:
     lib = _native.load()
     cols = _native.HostColumns(trace.arrays())
     desc = cols.desc()
@@ -88,11 +89,19 @@ def _run(trace: Trace, entries: np.ndarray, capacity: int, rates: ChannelRates) 
     resid = np.zeros(n, np.int64)
     rep = _native.SimReportC()
     r = _rates_struct(rates)
-    rc = lib.tio_simulate(ctypes.byref(desc), _native._ptr(entries), ctypes.c_int64(entries.shape[0]),
-                          ctypes.c_int64(capacity), ctypes.byref(r), ctypes.byref(rep), _native._ptr(start),
-                          _native._ptr(stall), _native._ptr(resid))
+    if layers is None:
+        rc = lib.tio_simulate(ctypes.byref(desc), _native._ptr(entries), ctypes.c_int64(entries.shape[0]),
+                              ctypes.c_int64(capacity), ctypes.byref(r), ctypes.byref(rep), _native._ptr(start),
+                              _native._ptr(stall), _native._ptr(resid))
+    else:
+        kl, tl = layers
+        rc = lib.tio_simulate_layers(ctypes.byref(desc), _native._ptr(kl), _native._ptr(tl), ctypes.c_int64(capacity),
+                                     ctypes.byref(r), ctypes.byref(rep), _native._ptr(start), _native._ptr(stall),
+                                     _native._ptr(resid))
     if rc == _native.TIO_ERR_SIMULATION:
         raise SimulationError(_native.last_error())
+    if rc == _native.TIO_ERR_CONFIG:
+        raise ConfigurationError(_native.last_error())
     _native.check(rc)
     total = int(rep.total_time)
     ideal = int(rep.ideal_time)
@@ -144,8 +153,18 @@ def simulate_on_demand(trace: Trace, capacity: int, rates: ChannelRates) -> SimR
 
 
 def simulate_layer_granularity(trace: Trace, capacity: int, rates: ChannelRates, layer_map=None) -> SimReport:
-    raise ConfigurationError("the layer-granularity baseline policy is outside this build's scope "
-                             "(reference simulator.py:97-177, SURVEY.md §2 S5)")
+    """Baseline: batch offload/prefetch at whole-layer granularity
+    (simulator.py:549-560, policy :95-177), run by the native scheduler
+    (`tio_simulate_layers`).  Engages only when the trace oversubscribes
+    capacity; `layer_map` ({tensor id: layer}) overrides tensor layers."""
+    a = trace.arrays()
+    kl = np.ascontiguousarray(a.kernel_layer, dtype=np.int64)
+    tl = np.array(a.tensor_layer, dtype=np.int64, copy=True)
+    if layer_map:
+        for i, tid in enumerate(a.tensor_id.tolist()):
+            if tid in layer_map:
+                tl[i] = NONE_I64 if layer_map[tid] is None else int(layer_map[tid])
+    return _run(trace, entries_array([]), capacity, rates, layers=(kl, tl))
 
 
 # --- report serialization (reference simulator.py:565-585) ----------------------

@@ -20,6 +20,8 @@ Corpora (the reference's own acceptance generators, test_acceptance.py):
           first 5000 attempts
   extreme edge magnitudes (benefits past 2^64, fractional rates), all-equal
           sizes/durations (ties everywhere), 1-3 kernel traces; 300 cases
+  layers  simulate_layer_granularity on transformer traces (+ layer maps) and
+          layer-less random traces
   c1      config C1: GPT-2 small transformer trace, 4 rate setups
   llama1  Appendix-C Llama-3-8B trace with 1 microbatch (E=4,579; slow)
 
@@ -175,6 +177,69 @@ def extreme(ref):
     return cases
 
 
+LAYER_FIELDS = ("total_time", "ideal_time", "per_kernel_start", "stall_per_kernel", "per_kernel_resident",
+                "stall_time_total", "peak_resident_bytes", "channel_utilization", "emergency_offloads",
+                "throughput_vs_ideal")
+
+
+def _layer_record(ref, trace, capacity, rates, layer_map=None):
+    try:
+        r = ref.simulate_layer_granularity(trace, capacity, rates, layer_map=layer_map)
+    except (ref.SimulationError, ref.ConfigurationError) as exc:
+        return {"error": f"{type(exc).__name__}: {exc}"}
+    return {f: getattr(r, f) for f in LAYER_FIELDS}
+
+
+def layers(ref):
+    """simulate_layer_granularity (simulator.py:549-560, policy :95-177) on
+    transformer traces (C1 and random small shapes) across capacities and
+    rates, with tensor layer maps, plus layer-less random traces (the
+    ConfigurationError path when the policy engages)."""
+    rng = random.Random(555)
+    cases = []
+    gens = [dict(num_layers=12, hidden_dim=768, num_heads=12, batch=8, seq_len=1024, bytes_per_element=4,
+                 compute_rate=cr, seed=0) for cr in (1_000_000_000, 10_000_000)]
+    for _ in range(40):
+        gens.append(dict(num_layers=rng.randint(1, 6), hidden_dim=rng.choice((64, 128, 256)), num_heads=4,
+                         batch=rng.randint(1, 4), seq_len=rng.choice((64, 128, 512)), bytes_per_element=rng.choice((2, 4)),
+                         compute_rate=rng.choice((1_000, 100_000, 10_000_000)), seed=rng.randint(0, 999)))
+    for g in gens:
+        trace = ref.gen_transformer_trace(ref.TransformerGenConfig(**g))
+        peak = ref.compute_memory_timeline(trace).peak()
+        floor = max(ref.per_kernel_active_bytes(trace), default=0)
+        for _ in range(3):
+            capacity = max(floor, int(peak * rng.choice((0.3, 0.5, 0.7, 0.9, 1.0))))
+            ssd = rng.choice((1_000, 16_000, 64_000, 2_500.5))
+            rates = ref.ChannelRates.symmetric(ssd, host=ssd * 2) if rng.random() < 0.3 else \
+                ref.ChannelRates.symmetric(ssd)
+            lmap = None
+            if rng.random() < 0.3:
+                ids = [t.id for t in trace.tensors]
+                lmap = {i: rng.randint(0, g["num_layers"] - 1) for i in rng.sample(ids, max(1, len(ids) // 4))}
+            rec = _layer_record(ref, trace, capacity, rates, lmap)
+            rec.update({"gen": {"transformer": g}, "trace_sha256": hashlib.sha256(ref.write_trace(trace)).hexdigest(),
+                        "capacity": capacity, "rates": [rates.ssd_offload, rates.ssd_prefetch, rates.host_offload,
+                                                        rates.host_prefetch],
+                        "layer_map": sorted(lmap.items()) if lmap else None})
+            cases.append(rec)
+    for _ in range(20):   # no layer ids: ConfigurationError once the policy engages, a plain run otherwise
+        seed = rng.randint(0, 10**9)
+        gen = {"seed": seed, "num_kernels": rng.randint(3, 30), "num_tensors": rng.randint(2, 12),
+               "size_range": [500_000, 60_000_000], "duration_range": [200, 5_000]}
+        trace = ref.gen_random_trace(seed, gen["num_kernels"], gen["num_tensors"], size_range=(500_000, 60_000_000),
+                                     duration_range=(200, 5_000))
+        peak = ref.compute_memory_timeline(trace).peak()
+        floor = max(ref.per_kernel_active_bytes(trace), default=0)
+        capacity = max(floor, int(peak * rng.choice((0.6, 1.0))))
+        rates = ref.ChannelRates.symmetric(10_000)
+        rec = _layer_record(ref, trace, capacity, rates)
+        rec.update({"gen": gen, "trace_sha256": hashlib.sha256(ref.write_trace(trace)).hexdigest(),
+                    "capacity": capacity, "rates": [rates.ssd_offload, rates.ssd_prefetch, rates.host_offload,
+                                                    rates.host_prefetch], "layer_map": None})
+        cases.append(rec)
+    return cases
+
+
 C1_SETUPS = [  # (compute_rate, ssd, host, host_cap) — SURVEY §8d
     (1_000_000_000, 16_000, None, 0),
     (1_000_000_000, 64_000, None, 0),
@@ -268,7 +333,7 @@ def main(argv=None):
     ap.add_argument("--only", default=None)
     args = ap.parse_args(argv)
     ref = _ref()
-    todo = {"crit2": crit2, "crit3": crit3, "extreme": extreme, "c1": c1, "sim": sim}
+    todo = {"crit2": crit2, "crit3": crit3, "extreme": extreme, "c1": c1, "sim": sim, "layers": layers}
     if args.llama1:
         todo["llama1"] = llama1
     for name, fn in todo.items():

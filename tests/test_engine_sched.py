@@ -84,3 +84,69 @@ def test_wrap_plan_folds_to_steady_state():
     r = simulate(tr, plan, CAP, ChannelRates.symmetric(20_000))
     assert r.total_time == 50_000 and r.stall_time_total == 0 and r.emergency_offloads == 0
     assert r.peak_resident_bytes <= CAP
+
+
+def test_layer_granularity_matches_reference():
+    """simulate_layer_granularity (reference simulator.py:549-560, policy
+    :95-177) on the reference's outputs (tests/golden/layers.json.gz)."""
+    import hashlib
+
+    from paper_2506_06472_b200 import ConfigurationError, TransformerGenConfig, gen_transformer_trace, write_trace
+    from paper_2506_06472_b200.simulator import simulate_layer_granularity
+    cases = load_golden("layers")
+    assert len(cases) >= 140
+    for rec in cases:
+        g = rec["gen"]
+        if "transformer" in g:
+            tr = gen_transformer_trace(TransformerGenConfig(**g["transformer"]))
+            assert hashlib.sha256(write_trace(tr)).hexdigest() == rec["trace_sha256"]
+        else:
+            tr = regen(rec)
+        so, sp, ho, hp = rec["rates"]
+        rates = ChannelRates(so, sp, ho, hp)
+        lmap = dict((int(k), v) for k, v in rec["layer_map"]) if rec["layer_map"] else None
+        if "error" in rec:
+            kind, msg = rec["error"].split(": ", 1)
+            exc = {"ConfigurationError": ConfigurationError, "SimulationError": SimulationError}[kind]
+            with pytest.raises(exc) as ei:
+                simulate_layer_granularity(tr, rec["capacity"], rates, layer_map=lmap)
+            assert str(ei.value) == msg
+            continue
+        _cmp(simulate_layer_granularity(tr, rec["capacity"], rates, layer_map=lmap), rec)
+
+
+# reference test_simulator.py:79-125 (layer-granularity baseline)
+def _layered_ex1():
+    from paper_2506_06472_b200 import KernelRecord, TensorKind, TensorRecord, make_trace
+    kernels = [KernelRecord(i, f"k{i}", 10_000, None, layer) for i, layer in enumerate([0, 0, 1, 1, 2])]
+    tensors = [TensorRecord(0, MB100, TensorKind.INTERMEDIATE, (0, 4), 0),
+               TensorRecord(1, MB100, TensorKind.INTERMEDIATE, (2,), 1)]
+    return make_trace(kernels, tensors)
+
+
+def test_layer_granularity_known_answers(ex1, rates20k):
+    from paper_2506_06472_b200 import (ConfigurationError, KernelRecord, TensorKind, TensorRecord, make_trace)
+    from paper_2506_06472_b200.simulator import simulate_layer_granularity
+    with pytest.raises(ConfigurationError):
+        simulate_layer_granularity(ex1, CAP, rates20k)
+    kernels = [KernelRecord(i, f"k{i}", 10_000, None, layer) for i, layer in enumerate([0, 0, 1, 1, 2])]
+    tensors = [TensorRecord(0, MB100, TensorKind.INTERMEDIATE, (0, 4)),
+               TensorRecord(1, MB100, TensorKind.INTERMEDIATE, (2,))]
+    assert simulate_layer_granularity(make_trace(kernels, tensors), CAP, rates20k,
+                                      layer_map={0: 0, 1: 1}).total_time >= 50_000
+    r = simulate_layer_granularity(_layered_ex1(), 250_000_000, rates20k)
+    assert r.total_time == 50_000 and all(v == 0.0 for v in r.channel_utilization.values())
+    kernels = [KernelRecord(i, f"k{i}", 10_000, None, 0) for i in range(5)]
+    tensors = [TensorRecord(0, MB100, TensorKind.INTERMEDIATE, (0, 4), 0),
+               TensorRecord(1, MB100, TensorKind.INTERMEDIATE, (2,), 0)]
+    one = make_trace(kernels, tensors)
+    assert simulate_layer_granularity(one, CAP, rates20k).total_time == simulate_on_demand(one, CAP, rates20k).total_time
+
+
+@pytest.mark.gpu
+def test_layer_granularity_never_beats_lifetime_plan(rates20k):
+    from paper_2506_06472_b200 import plan_migrations
+    from paper_2506_06472_b200.simulator import simulate_layer_granularity
+    tr = _layered_ex1()
+    planned = simulate(tr, plan_migrations(tr, CAP, rates20k), CAP, rates20k)
+    assert simulate_layer_granularity(tr, CAP, rates20k).total_time >= planned.total_time
