@@ -229,6 +229,20 @@ int tio_simulate_layers(const tio_trace_desc *trace, const int64_t *kernel_layer
                         int64_t capacity, const tio_rates *rates, tio_sim_report *report,
                         int64_t *per_kernel_start, int64_t *stall_per_kernel, int64_t *per_kernel_resident);
 
+/* ---- roofline sweep --------------------------------------------------------
+ * Replaces roofline.py:39-125: total iteration time (us) under the roofline
+ * policy at each bandwidth (bytes/us, both directions; exact ceil of bytes /
+ * rate as transfer_duration), host trace columns in.  info: iteration length,
+ * memory-timeline peak, pressured = peak > capacity (totals are then the
+ * iteration length), period count and largest period size (for
+ * saturation_bandwidth).  num_bandwidths = 0 fills info only. */
+typedef struct tio_roofline_info {
+    int64_t ideal_us, peak_bytes, pressured, num_periods, max_period_bytes;
+} tio_roofline_info;
+
+int tio_roofline(const tio_trace_desc *trace, int64_t capacity, const double *bandwidth, int64_t num_bandwidths,
+                 int64_t *total_us, tio_roofline_info *info);
+
 /* The engine program behind a run: every transfer the scheduler starts (in
  * start order) and every kernel's start time, model microseconds.
  * initial_loc[t]: 0 unallocated, 1 GPU, 2 SSD, 3 host at t = 0 (after plan

@@ -84,6 +84,10 @@ class SimReportC(ctypes.Structure):
                                     "emergency_offloads")] + [("channel_busy", _i64 * 4), ("num_transfers", _i64)]
 
 
+class RooflineInfoC(ctypes.Structure):
+    _fields_ = [(n, _i64) for n in ("ideal_us", "peak_bytes", "pressured", "num_periods", "max_period_bytes")]
+
+
 COMMIT_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("start_kernel", "<i8"),
                          ("end_kernel", "<i8"), ("wraps", "<i8"), ("destination", "<i8"),
                          ("off_start", "<i8"), ("off_end", "<i8"), ("pre_start", "<i8"),
@@ -101,7 +105,7 @@ ENTRY_DTYPE = np.dtype([("tensor_id", "<i8"), ("tensor_pos", "<i8"), ("trigger_u
 EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_device_info", "tio_trace_create",
            "tio_trace_destroy", "tio_lifetime", "tio_lifetime_view_get", "tio_lifetime_copy_out",
            "tio_plan_create", "tio_plan_create2", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
-           "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate", "tio_simulate_layers",
+           "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate", "tio_simulate_layers", "tio_roofline",
            "tio_engine_replay", "tio_pack", "tio_unpack", "tio_schedule", "tio_trace_parse",
            "tio_parsed_sizes", "tio_parsed_copy", "tio_parsed_destroy")
 

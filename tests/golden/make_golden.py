@@ -22,6 +22,7 @@ Corpora (the reference's own acceptance generators, test_acceptance.py):
           sizes/durations (ties everywhere), 1-3 kernel traces; 300 cases
   layers  simulate_layer_granularity on transformer traces (+ layer maps) and
           layer-less random traces
+  roofline roofline_curve + saturation_bandwidth on random traces and C1
   c1      config C1: GPT-2 small transformer trace, 4 rate setups
   llama1  Appendix-C Llama-3-8B trace with 1 microbatch (E=4,579; slow)
 
@@ -240,6 +241,43 @@ def layers(ref):
     return cases
 
 
+def roofline(ref):
+    """roofline_curve / saturation_bandwidth (roofline.py:39-125) on random
+    traces (the reference's test_roofline generator and wider ones, globals
+    included) and on C1, over integer and fractional bandwidth grids."""
+    rng = random.Random(777)
+    cases = []
+    for i in range(120):
+        seed = rng.randint(0, 10**9)
+        nk, nt = (10, 8) if i < 30 else (rng.randint(2, 60), rng.randint(1, 30))
+        sr, dr = ((1_000, 80_000), (50, 500)) if i < 30 else ((500_000, 60_000_000), (200, 5_000))
+        gf = 0.3 if i < 30 else rng.choice((0.0, 0.3, 0.9))
+        trace = ref.gen_random_trace(seed, nk, nt, size_range=sr, duration_range=dr, global_fraction=gf)
+        if i < 30:
+            capacity = max(1, sum(t.size_bytes for t in trace.tensors) // 2)
+            grid = [10, 30, 100, 300, 1_000, 10_000]
+        else:
+            capacity = max(1, int(ref.compute_memory_timeline(trace).peak() * rng.choice((0.3, 0.6, 0.9, 1.1))))
+            grid = sorted(rng.sample([7.5, 100, 1_000, 2_500.25, 10_000, 16_000, 40_000, 123_456.5, 1e6], 5))
+        pts = ref.roofline_curve(trace, capacity, grid)
+        cases.append({"gen": {"seed": seed, "num_kernels": nk, "num_tensors": nt, "size_range": list(sr),
+                              "duration_range": list(dr), "global_fraction": gf},
+                      "trace_sha256": hashlib.sha256(ref.write_trace(trace)).hexdigest(),
+                      "capacity": capacity, "grid": grid,
+                      "points": [p.normalized_throughput for p in pts],
+                      "saturation": ref.saturation_bandwidth(trace)})
+    cfg = ref.TransformerGenConfig(num_layers=12, hidden_dim=768, num_heads=12, batch=8, seq_len=1024,
+                                   bytes_per_element=4, compute_rate=1_000_000_000, seed=0)
+    trace = ref.gen_transformer_trace(cfg)
+    grid = [1_000, 4_000, 16_000, 64_000, 256_000, 1_000_000]
+    capacity = ref.compute_memory_timeline(trace).peak() // 2
+    cases.append({"gen": {"c1": True}, "trace_sha256": hashlib.sha256(ref.write_trace(trace)).hexdigest(),
+                  "capacity": capacity, "grid": grid,
+                  "points": [p.normalized_throughput for p in ref.roofline_curve(trace, capacity, grid)],
+                  "saturation": ref.saturation_bandwidth(trace)})
+    return cases
+
+
 C1_SETUPS = [  # (compute_rate, ssd, host, host_cap) — SURVEY §8d
     (1_000_000_000, 16_000, None, 0),
     (1_000_000_000, 64_000, None, 0),
@@ -333,7 +371,7 @@ def main(argv=None):
     ap.add_argument("--only", default=None)
     args = ap.parse_args(argv)
     ref = _ref()
-    todo = {"crit2": crit2, "crit3": crit3, "extreme": extreme, "c1": c1, "sim": sim, "layers": layers}
+    todo = {"crit2": crit2, "crit3": crit3, "extreme": extreme, "c1": c1, "sim": sim, "layers": layers, "roofline": roofline}
     if args.llama1:
         todo["llama1"] = llama1
     for name, fn in todo.items():
