@@ -314,3 +314,37 @@ def test_c3_lifetime_and_plan_prefix_vs_oracle():
     assert int(g["info"].num_commits) == len(o["committed"]) == R
     assert g["plan_bytes"] == o["plan_bytes"]
     assert np.array_equal(g["residual"], o["residual"])
+
+
+def test_criterion_6_characterization_regime():
+    """Reference test_acceptance.py:181-188: the default transformer trace at
+    half its peak is a capacity problem, not an active-bytes one."""
+    from paper_2506_06472_b200 import TransformerGenConfig, gen_transformer_trace
+    from paper_2506_06472_b200.analysis import characterize
+    tr = gen_transformer_trace(TransformerGenConfig())
+    demand = compute_memory_timeline(tr).peak()
+    report = characterize(tr, demand // 2)
+    assert report.max_active_fraction < 0.15
+
+
+def test_characterization_known_answers(ex1):
+    """Reference test_analysis.py:37-41 (wrap interior) and :72-101
+    (characterize, CSV shapes) over the device lifetime columns."""
+    from paper_2506_06472_b200.analysis import (characterize, fractions_csv, histogram_csv,
+                                                period_interior_duration)
+    wrap = mk_trace([10] * 5, [(0, 7, "global", [1, 2])])
+    assert period_interior_duration(compute_inactive_periods(wrap)[0], wrap) == 30   # k3, k4, k0
+    rep = characterize(ex1, capacity=150_000_000, size_buckets=(10_000_000, 1_000_000_000),
+                       duration_buckets=(1_000, 100_000))
+    third = 100_000_000 / 150_000_000
+    assert rep.active_fraction == [third, 0.0, third, 0.0, third]
+    assert rep.histogram == {("[10000000,1000000000)", "[1000,100000)"): 1}
+    assert rep.total_periods == 1 and rep.max_active_fraction == pytest.approx(third)
+    empty = characterize(mk_trace([], []), capacity=100)
+    assert empty.active_bytes == [] and empty.histogram == {} and empty.mean_active_fraction == 0.0
+    with pytest.raises(ValueError):
+        characterize(ex1, capacity=0)
+    rep = characterize(ex1, capacity=150_000_000)
+    assert fractions_csv(rep).splitlines()[0] == "kernel,active_bytes,active_fraction"
+    assert len(fractions_csv(rep).splitlines()) == 6
+    assert histogram_csv(rep).splitlines()[0] == "size_class_bytes,duration_class_us,count"

@@ -73,3 +73,23 @@ def test_csv_reports_gbps(ex1):
     lines = roofline_csv(roofline_curve(ex1, CAP, [16_000])).splitlines()
     assert lines[0] == "bandwidth_gbps,normalized_throughput"
     assert lines[1].startswith("16.0,")
+
+
+def test_criterion_4_roofline_properties():
+    """Reference test_acceptance.py:134-150 (the timeline peak from the
+    oracle: this test runs without a GPU)."""
+    import random
+
+    from oracle import oracle as O
+    rng = random.Random(11)
+    grid = [5, 20, 80, 320, 1_280, 20_000]
+    for case in range(100):
+        trace = gen_random_trace(rng.randint(0, 10**9), rng.randint(2, 12), rng.randint(1, 8),
+                                 size_range=(10_000, 500_000), duration_range=(500, 5_000))
+        tl = O.lifetime(trace.arrays())[1]
+        capacity = max(1, (int(tl.max()) if len(tl) else 0) // 2)
+        values = [p.normalized_throughput for p in roofline_curve(trace, capacity, grid)]
+        assert values == sorted(values), case
+        assert all(0 < v <= 1.0 for v in values), case
+        (top,) = roofline_curve(trace, capacity, [saturation_bandwidth(trace)])
+        assert top.normalized_throughput == 1.0, case
