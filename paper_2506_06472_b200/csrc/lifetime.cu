@@ -116,8 +116,14 @@ __device__ void lookback_resolve(int64_t *st, int64_t cstride, int64_t tile, con
 
 // ---------------------------------------------------------------- owners
 // owner[t] = largest i in [0, T) with ptr[i] <= e_t, e_t = min(t * LT_TILE, E - 1)
-__global__ void k_tile_owners(const int64_t *ptr, int64_t T, int64_t E, int64_t ntiles, int64_t *owner) {
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// Also zeroes the tile counters and the look-back status words for the two
+// kernels that follow (work[0, 2) and zero[0, nzero)).
+__global__ void k_tile_owners(const int64_t *ptr, int64_t T, int64_t E, int64_t ntiles, int64_t *owner,
+                              int64_t *work, int64_t *zero, int64_t nzero) {
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gtid < 2) work[gtid] = 0;
+    for (int64_t i = gtid; i < nzero; i += (int64_t)gridDim.x * blockDim.x) zero[i] = 0;
+    const int64_t warp = gtid >> 5;
     if (warp > ntiles) return;
     int64_t e = warp * LT_TILE;
     if (e > E - 1) e = E - 1;
@@ -338,6 +344,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
 #endif
 __global__ void __launch_bounds__(LIFETIME_THREADS, LT_MINB)
 k_events(LifetimeArgs a) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");      // owners + zeroed status (programmatic launch)
     extern __shared__ __align__(16) unsigned char smraw[];
     EvSmem &sm = *reinterpret_cast<EvSmem *>(smraw);
     const int64_t T = a.T, E = a.E;
@@ -372,6 +379,7 @@ k_events(LifetimeArgs a) {
 // ---------------------------------------------------------------- kernels
 __global__ void __launch_bounds__(KT_THREADS, 1024 / KT_THREADS)
 k_kernels(LifetimeArgs a) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");      // k_events complete (programmatic launch)
     __shared__ int64_t scan[40];
     __shared__ int64_t s_pre[2];
     __shared__ int64_t s_tile;
@@ -458,19 +466,37 @@ int launch_lifetime(const LifetimeArgs &args, cudaStream_t stream) {
         attr = true;
     }
     const int64_t NTe = lifetime_event_tiles(args.E), NTk = lifetime_kernel_tiles(args.N);
-    // counters + event / kernel look-back status
-    TIO_CUDA(cudaMemsetAsync(args.work, 0, sizeof(int64_t) * 2, stream));
-    TIO_CUDA(cudaMemsetAsync(args.work + 2 + owners_len(NTe), 0, sizeof(int64_t) * (2 * NTe + 4 * NTk), stream));
+    // counters + event / kernel look-back status: zeroed by k_tile_owners
+    int64_t *status = args.work + 2 + owners_len(NTe);
+    const int64_t nstatus = 2 * NTe + 4 * NTk;
     if (NTe > 0) {
         const int64_t thr = 32 * (NTe + 1);
-        k_tile_owners<<<(unsigned)((thr + 255) / 256), 256, 0, stream>>>(args.ptr, args.T, args.E, NTe, args.work + 2);
+        k_tile_owners<<<(unsigned)((thr + 255) / 256), 256, 0, stream>>>(args.ptr, args.T, args.E, NTe, args.work + 2,
+                                                                          args.work, status, nstatus);
         count_launch();
+    } else {
+        TIO_CUDA(cudaMemsetAsync(args.work, 0, sizeof(int64_t) * 2, stream));
+        TIO_CUDA(cudaMemsetAsync(status, 0, sizeof(int64_t) * nstatus, stream));
     }
-    const int64_t nb = NTe > 0 ? NTe : 1;            // >= 1 block: the tensor-table checks
-    k_events<<<(unsigned)nb, LIFETIME_THREADS, sizeof(EvSmem), stream>>>(args);
+    // the next two kernels launch programmatically (PDL): their blocks become
+    // resident while the previous grid drains and wait in griddepcontrol.wait
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = stream;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3((unsigned)(NTe > 0 ? NTe : 1));     // >= 1 block: the tensor-table checks
+    cfg.blockDim = dim3(LIFETIME_THREADS);
+    cfg.dynamicSmemBytes = sizeof(EvSmem);
+    TIO_CUDA(cudaLaunchKernelEx(&cfg, k_events, args));
     count_launch();
     if (NTk > 0) {
-        k_kernels<<<(unsigned)NTk, KT_THREADS, 0, stream>>>(args);
+        cfg.gridDim = dim3((unsigned)NTk);
+        cfg.blockDim = dim3(KT_THREADS);
+        cfg.dynamicSmemBytes = 0;
+        TIO_CUDA(cudaLaunchKernelEx(&cfg, k_kernels, args));
         count_launch();
     }
     TIO_CUDA(cudaGetLastError());
