@@ -6,7 +6,10 @@
 
 namespace tio {
 
-constexpr int PLAN_THREADS = 256;
+#ifndef TIO_PLAN_THREADS
+#define TIO_PLAN_THREADS 256
+#endif
+constexpr int PLAN_THREADS = TIO_PLAN_THREADS;   // per block; 2 blocks per SM at 256
 constexpr int TILE = 32;             // candidates per tile (one warp)
 
 // candidate SSD/host evaluation state (2 bits each in st[c])
