@@ -18,6 +18,7 @@ constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 
 __global__ void __launch_bounds__(RS_THREADS)
 rs_hist(const uint64_t *keys, int64_t n, int shift, int64_t *hist, int64_t ntiles) {
+    pdl_wait();
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
@@ -33,6 +34,7 @@ rs_hist(const uint64_t *keys, int64_t n, int shift, int64_t *hist, int64_t ntile
 __global__ void __launch_bounds__(RS_THREADS)
 rs_scatter(const uint64_t *kin, const uint32_t *vin, uint64_t *kout, uint32_t *vout, int64_t n,
            int shift, const int64_t *offs, int64_t ntiles) {
+    pdl_wait();
     __shared__ uint64_t sk[2][RS_TILE];
     __shared__ uint32_t sv[2][RS_TILE];
     __shared__ uint32_t dstart[256];
@@ -99,9 +101,12 @@ int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *keys_tmp, uint32_
     uint64_t *ka = keys, *kb = keys_tmp;
     uint32_t *va = vals, *vb = vals_tmp;
     for (int shift = 0; shift < bits; shift += 8) {
-        rs_hist<<<(unsigned)ntiles, RS_THREADS, 0, stream>>>(ka, n, shift, hist, ntiles); ::tio::count_launch();
+        TIO_CUDA(launch_pdl(rs_hist, dim3((unsigned)ntiles), dim3(RS_THREADS), 0, stream, ka, n, shift, hist, ntiles));
+        ::tio::count_launch();
         TIO_TRY(exclusive_scan(hist, hist, 256 * ntiles, hist + 256 * ntiles, nullptr, stream));
-        rs_scatter<<<(unsigned)ntiles, RS_THREADS, 0, stream>>>(ka, va, kb, vb, n, shift, hist, ntiles); ::tio::count_launch();
+        TIO_CUDA(launch_pdl(rs_scatter, dim3((unsigned)ntiles), dim3(RS_THREADS), 0, stream, ka, va, kb, vb, n, shift,
+                            hist, ntiles));
+        ::tio::count_launch();
         TIO_CUDA(cudaGetLastError());
         uint64_t *tk = ka; ka = kb; kb = tk;
         uint32_t *tv = va; va = vb; vb = tv;

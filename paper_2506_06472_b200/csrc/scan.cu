@@ -13,6 +13,7 @@ constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
 // out[i] = exclusive prefix within the tile; tot[tile] = tile sum
 __global__ void __launch_bounds__(SC_THREADS)
 scan_tiles(const int64_t *in, int64_t *out, int64_t n, int64_t *tot) {
+    pdl_wait();
     __shared__ int64_t sm[40];
     const int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_ITEMS;
     int64_t v[SC_ITEMS];
@@ -34,6 +35,7 @@ scan_tiles(const int64_t *in, int64_t *out, int64_t n, int64_t *tot) {
 
 __global__ void __launch_bounds__(1024)
 scan_totals(int64_t *tot, int64_t m, int64_t *grand) {
+    pdl_wait();
     __shared__ int64_t sm[40];
     const int64_t per = (m + blockDim.x - 1) / blockDim.x;
     const int64_t b0 = threadIdx.x * per;
@@ -52,6 +54,7 @@ scan_totals(int64_t *tot, int64_t m, int64_t *grand) {
 
 __global__ void __launch_bounds__(SC_THREADS)
 scan_add(int64_t *out, int64_t n, const int64_t *tot) {
+    pdl_wait();
     const int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_ITEMS;
     const int64_t add = tot[blockIdx.x];
 #pragma unroll
@@ -68,9 +71,12 @@ int exclusive_scan(const int64_t *in, int64_t *out, int64_t n, int64_t *tmp, int
         return TIO_OK;
     }
     const int64_t tiles = (n + SC_TILE - 1) / SC_TILE;
-    scan_tiles<<<(unsigned)tiles, SC_THREADS, 0, stream>>>(in, out, n, tmp); ::tio::count_launch();
-    scan_totals<<<1, 1024, 0, stream>>>(tmp, tiles, grand); ::tio::count_launch();
-    scan_add<<<(unsigned)tiles, SC_THREADS, 0, stream>>>(out, n, tmp); ::tio::count_launch();
+    TIO_CUDA(launch_pdl(scan_tiles, dim3((unsigned)tiles), dim3(SC_THREADS), 0, stream, in, out, n, tmp));
+    ::tio::count_launch();
+    TIO_CUDA(launch_pdl(scan_totals, dim3(1), dim3(1024), 0, stream, tmp, tiles, grand));
+    ::tio::count_launch();
+    TIO_CUDA(launch_pdl(scan_add, dim3((unsigned)tiles), dim3(SC_THREADS), 0, stream, out, n, (const int64_t *)tmp));
+    ::tio::count_launch();
     TIO_CUDA(cudaGetLastError());
     return TIO_OK;
 }
