@@ -24,3 +24,43 @@ REFERENCE_NAMES = (
 def test_every_reference_name_is_exported():
     missing = [n for n in REFERENCE_NAMES if not hasattr(offloader, n)]
     assert missing == []
+
+
+# parameter names of the reference functions (same source as REFERENCE_NAMES)
+REFERENCE_SIGNATURES = {
+    'candidate_benefit': ('window', 'period', 'residual', 'capacity', 'trace'),
+    'candidate_window': ('period', 'trace', 'offload_channel', 'prefetch_channel', 'destination'),
+    'channel_utilization': ('channel', 'window_start', 'window_end'),
+    'characterize': ('trace', 'capacity', 'size_buckets', 'duration_buckets'),
+    'compute_inactive_periods': ('trace',),
+    'compute_memory_timeline': ('trace',),
+    'gen_random_trace': ('seed', 'num_kernels', 'num_tensors', 'size_range', 'duration_range', 'global_fraction'),
+    'gen_transformer_trace': ('cfg',),
+    'load_trace': ('path',),
+    'make_trace': ('kernels', 'tensors', 'meta'),
+    'mark_urgent': ('plan', 'trace'),
+    'parse_plan': ('data',),
+    'parse_trace': ('data',),
+    'per_kernel_active_bytes': ('trace',),
+    'plan_migrations': ('trace', 'capacity', 'rates', 'host_cap'),
+    'roofline_curve': ('trace', 'capacity', 'bandwidth_list'),
+    'saturation_bandwidth': ('trace',),
+    'save_trace': ('trace', 'path'),
+    'select_destination': ('period', 'trace', 'ssd_channels', 'host_channels', 'host_cap', 'host_occupancy'),
+    'simulate': ('trace', 'plan', 'capacity', 'rates'),
+    'simulate_ideal': ('trace',),
+    'simulate_layer_granularity': ('trace', 'capacity', 'rates', 'layer_map'),
+    'simulate_on_demand': ('trace', 'capacity', 'rates'),
+    'transfer_duration': ('channel', 'nbytes'),
+    'transformer_peak_bytes': ('cfg',),
+    'validate_trace': ('trace',),
+    'write_plan': ('plan',),
+    'write_trace': ('trace',),
+}
+
+
+def test_function_parameters_match_the_reference():
+    import inspect
+    bad = {n: tuple(inspect.signature(getattr(offloader, n)).parameters) for n, p in REFERENCE_SIGNATURES.items()
+           if tuple(inspect.signature(getattr(offloader, n)).parameters) != p}
+    assert bad == {}
