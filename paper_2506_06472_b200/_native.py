@@ -184,7 +184,12 @@ class HostColumns:
         self.size = np.ascontiguousarray(arrays.size_bytes, dtype=np.int64)
         self.kind = np.ascontiguousarray(arrays.kind, dtype=np.int8)
         self.ptr = np.ascontiguousarray(arrays.access_ptr, dtype=np.int64)
-        self.acc = np.ascontiguousarray(arrays.accesses, dtype=np.int32)
+        acc = np.asarray(arrays.accesses)
+        if acc.size and (int(acc.min()) < np.iinfo(np.int32).min or int(acc.max()) > np.iinfo(np.int32).max):
+            # an unvalidated trace: keep the value out of range instead of wrapping it
+            # into a valid kernel index (libtio range-checks every access against N)
+            acc = np.clip(acc, -1, np.iinfo(np.int32).max)
+        self.acc = np.ascontiguousarray(acc, dtype=np.int32)
 
     def desc(self) -> TraceDesc:
         return TraceDesc(self.dur.shape[0], _ptr(self.dur), self.tid.shape[0], _ptr(self.tid),

@@ -62,14 +62,16 @@ class LifetimeArrays:
 
 
 def _device_trace(trace: Trace) -> "_native.DeviceTrace":
+    arrays = trace.arrays()          # drops every cached device product if the records changed
     dt = trace.device_cache.get("trace")
     if dt is None:
-        dt = _native.DeviceTrace(trace.arrays())
+        dt = _native.DeviceTrace(arrays)
         trace.device_cache["trace"] = dt
     return dt
 
 
 def lifetime_arrays(trace: Trace) -> LifetimeArrays:
+    trace.arrays()                   # staleness check first (see Trace.arrays)
     cached = trace.device_cache.get("lifetime")
     if cached is None:
         r = _device_trace(trace).lifetime()

@@ -86,7 +86,7 @@ int decode_rate(double rate, RateCode *rc) {
     uint64_t m = (uint64_t)std::ldexp(mant, 53);
     int k = 53 - ex;
     while (k > 0 && (m & 1u) == 0) { m >>= 1; --k; }
-    if (k > 64) return fail(TIO_ERR_CHANNEL_CONFIG, "rate %.17g has more than 64 fractional bits", rate);
+    // any k is exact: duration_of takes a long-division path past 64 bits
     rc->num = (int64_t)m;
     rc->shift = k;
     return TIO_OK;

@@ -95,6 +95,23 @@ __host__ __device__ __forceinline__ int64_t duration_of(const RateCode &r, int64
     if (nbytes <= 0) return 0;
     if (r.huge) return 1;
     if (r.shift == 0) return nbytes / r.num + (nbytes % r.num != 0);
+    if (r.shift > 64) {
+        // ceil(nbytes * 2^shift / num) by long division, 8 bits at a time
+        // (num < 2^53, so the shifted remainder stays below 2^61); only very
+        // small fractional rates (< ~5e-4 B/us) take this path
+        const uint64_t m = (uint64_t)r.num;
+        uint64_t q = (uint64_t)nbytes / m, rem = (uint64_t)nbytes % m;
+        for (int left = r.shift; left > 0;) {
+            const int c = left < 8 ? left : 8;
+            if (q >> (63 - c)) return INT64_MAX;   // saturates: > any iteration
+            rem <<= c;
+            q = (q << c) | (rem / m);
+            rem %= m;
+            left -= c;
+        }
+        q += rem != 0;
+        return q > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)q;
+    }
     u128 num = ((u128)(uint64_t)nbytes) << r.shift;
     u128 m = (u128)(uint64_t)r.num;
     u128 q = num / m + (num % m != 0);

@@ -472,12 +472,13 @@ struct Engine {
     }
 
     int run() {
-        for (int c = 0; c < 4; ++c) {
-            if (c >= 2 && !in.has_host) { chan_exists[c] = false; continue; }
-            chan_exists[c] = true;
-            const int r = decode_rate(in.rate[c], &rc[c]);
-            if (r != TIO_OK) { err = "channel rate must be > 0"; return r; }
-        }
+        for (int64_t t = 0; t < T; ++t)
+            for (int64_t j = in.ptr[t]; j < in.ptr[t + 1]; ++j)
+                if (in.acc[j] < 0 || in.acc[j] >= N) {
+                    err = "tensor " + std::to_string(in.tid[t]) + ": access " + std::to_string(in.acc[j]) +
+                          " out of range";
+                    return TIO_ERR_INVALID;
+                }
         for (int64_t k = 0; k < N; ++k) iteration += in.dur[k];
         // active_at[k] sorted by tensor id (simulator.py:187-198)
         act_ptr.assign(N + 1, 0);
@@ -504,6 +505,15 @@ struct Engine {
                 err = buf;
                 return TIO_ERR_SIMULATION;
             }
+        }
+        // simulator.py:206-216: the channels are built after the active-bytes
+        // check, so a bad rate surfaces only on a satisfiable trace
+        static const char *names[4] = {"ssd.offload", "ssd.prefetch", "host.offload", "host.prefetch"};
+        for (int c = 0; c < 4; ++c) {
+            if (c >= 2 && !in.has_host) { chan_exists[c] = false; continue; }
+            chan_exists[c] = true;
+            const int r = decode_rate(in.rate[c], &rc[c]);
+            if (r != TIO_OK) { err = std::string("channel ") + names[c] + ": rate must be > 0"; return r; }
         }
         loc.assign(T, LOC_NONE);
         for (int64_t t = 0; t < T; ++t) loc[t] = is_global(t) ? LOC_GPU : LOC_NONE;

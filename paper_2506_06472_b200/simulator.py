@@ -102,6 +102,9 @@ def _run(trace: Trace, entries: np.ndarray, capacity: int, rates: ChannelRates, 
         raise SimulationError(_native.last_error())
     if rc == _native.TIO_ERR_CONFIG:
         raise ConfigurationError(_native.last_error())
+    if rc == _native.TIO_ERR_CHANNEL_CONFIG:
+        from .bandwidth import ChannelConfigError
+        raise ChannelConfigError(_native.last_error())      # "channel ssd.offload: rate must be > 0"
     _native.check(rc)
     total = int(rep.total_time)
     ideal = int(rep.ideal_time)

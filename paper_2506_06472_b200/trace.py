@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import io
 import json
+import operator
 from dataclasses import dataclass, field
 from enum import Enum
 from typing import IO, Iterable
@@ -218,7 +219,11 @@ class Trace:
     Construct from record lists like the reference (`Trace(kernels, tensors,
     meta)`), or from columns with `Trace.from_arrays`.  `arrays()` returns the
     column form the device path consumes; for record-built traces it is
-    rebuilt whenever the record lists change.
+    rebuilt whenever the record lists change: the records are frozen, so the
+    lists are compared element by element (by identity) with the snapshot
+    the columns were built from; the snapshot holds the records, so their
+    ids cannot be reused while it exists.  Every device-side cache entry
+    (`device_cache`) is dropped with the columns.
     """
 
     def __init__(self, kernels: list[KernelRecord] | None = None,
@@ -228,7 +233,7 @@ class Trace:
         self._tensors = tensors if tensors is not None else []
         self.meta = meta if meta is not None else {}
         self._arrays: TraceArrays | None = None
-        self._arrays_key = None
+        self._snap: tuple | None = None
         self._from_arrays = False
         self.device_cache: dict = {}
 
@@ -247,7 +252,7 @@ class Trace:
             self._kernels, self._tensors = records_from_arrays(self._arrays)
             # from now on the lists are the source of truth
             self._from_arrays = False
-            self._arrays_key = self._key()
+            self._snap = self._snapshot()
 
     @property
     def kernels(self) -> list[KernelRecord]:
@@ -269,17 +274,23 @@ class Trace:
         self._materialise()
         self._tensors = value
 
-    def _key(self):
-        return (id(self._kernels), len(self._kernels), hash(tuple(map(id, self._kernels))),
-                id(self._tensors), len(self._tensors), hash(tuple(map(id, self._tensors))))
+    def _snapshot(self) -> tuple:
+        return tuple(self._kernels), tuple(self._tensors)
+
+    def _stale(self) -> bool:
+        if self._arrays is None or self._snap is None:
+            return True
+        for cur, old in ((self._kernels, self._snap[0]), (self._tensors, self._snap[1])):
+            if len(cur) != len(old) or not all(map(operator.is_, cur, old)):
+                return True
+        return False
 
     def arrays(self) -> TraceArrays:
         if self._from_arrays:
             return self._arrays
-        key = self._key()
-        if self._arrays is None or key != self._arrays_key:
+        if self._stale():
             self._arrays = arrays_from_records(self._kernels, self._tensors)
-            self._arrays_key = key
+            self._snap = self._snapshot()
             self.device_cache.clear()
         return self._arrays
 
@@ -521,7 +532,11 @@ def _fast_parse(raw: bytes):
     arrays = TraceArrays(duration_us=k_dur, kernel_index=k_index, kernel_name_code=k_code, name_table=table,
                          kernel_stage=k_stage, kernel_layer=k_layer, tensor_id=t_id, size_bytes=t_size,
                          kind=t_kind, tensor_layer=t_layer, access_ptr=ptr, accesses=acc)
-    return arrays, json.loads(meta.raw[:MB].decode("utf-8"))
+    try:
+        meta_obj = json.loads(meta.raw[:MB].decode("utf-8"))
+    except (UnicodeDecodeError, json.JSONDecodeError):
+        return None          # not valid JSON after all: the exact parser raises the reference's error
+    return arrays, meta_obj
 
 
 def parse_trace(data: bytes | str | IO) -> Trace:

@@ -173,3 +173,28 @@ def test_criterion_5_baseline_numbers_are_the_references():
     assert simulate_layer_granularity(tr, cap, rates).total_time == 137_072
     fat = ChannelRates.symmetric(int(max(tr.arrays().size_bytes)))
     assert simulate(tr, plan_migrations(tr, cap, fat), cap, fat).total_time == simulate_ideal(tr)
+
+
+def test_tiny_fractional_rates_are_exact(ex1):
+    """rates with more than 64 fractional bits (< ~5e-4 B/us) are
+    exact like the reference's Fraction(float) path (bandwidth.py:81-84)."""
+    from fractions import Fraction
+    import math
+    from paper_2506_06472_b200._native import transfer_duration as native_duration
+    for rate in (0.0001, 3.3e-7, 1e-12, 0.000123456789, 5e-300):
+        for nb in (1, 7, 100_000_000, 2**40 + 3):
+            want = math.ceil(Fraction(nb) / Fraction(rate))
+            got = native_duration(rate, nb)
+            assert got == min(want, 2**63 - 1), (rate, nb)
+    od = simulate_on_demand(ex1, CAP, ChannelRates.symmetric(0.0001))
+    assert od.total_time == 2_000_000_050_000          # the reference's answer
+
+
+def test_bad_rate_raises_channel_config_error_after_capacity_check(ex1):
+    """simulator.py:200-216: the active-bytes SimulationError comes first, then
+    the channel constructor's ChannelConfigError."""
+    from paper_2506_06472_b200 import ChannelConfigError
+    with pytest.raises(ChannelConfigError, match="channel ssd.offload: rate must be > 0"):
+        simulate_on_demand(ex1, CAP, ChannelRates.symmetric(0))
+    with pytest.raises(SimulationError, match="kernel 0 actively uses"):
+        simulate_on_demand(ex1, 90_000_000, ChannelRates.symmetric(0))

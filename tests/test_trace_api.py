@@ -80,3 +80,28 @@ def test_round_trips():
 def test_mutated_traces_fail_validation(mutant):
     with pytest.raises(TraceValidationError):
         parse_trace(mutant)
+
+
+def test_record_edits_invalidate_columns_and_device_cache():
+    """edits to the record lists rebuild the columns and drop every
+    device-side cache entry (the planner would otherwise plan a stale trace)."""
+    tr = parse_trace(EX1)
+    ks, ts = list(tr.kernels), list(tr.tensors)
+    tr2 = Trace(ks, ts, {})
+    a0 = tr2.arrays()
+    assert tr2.arrays() is a0                      # unchanged lists: cached
+    tr2.device_cache["lifetime"] = "stale"
+    tr2.tensors.append(TensorRecord(9, 50_000_000, TensorKind.INTERMEDIATE, (1, 2), None))
+    a1 = tr2.arrays()
+    assert a1 is not a0 and a1.num_tensors == 3 and "lifetime" not in tr2.device_cache
+    # replacing one kernel record twice (ids of dropped records may be reused)
+    for d in (20_000, 30_000):
+        tr2.kernels[1] = KernelRecord(1, "k1", d, None, None)
+        assert tr2.iteration_length() == 40_000 + d
+        assert tr2.kernel_start_times()[2] == 10_000 + d
+
+
+def test_fast_parser_bad_meta_raises_reference_error():
+    bad = EX1.replace('{"version": 1, "meta": {"model": "ex1"}}', '{"version": 1, "meta": {"model": "ex1",}}')
+    with pytest.raises(TraceParseError, match="line 1"):
+        parse_trace(bad)
