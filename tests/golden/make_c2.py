@@ -1,7 +1,10 @@
 """Fingerprints of the C2 / C3 plans computed by the CPU oracle (slow: tens
 of minutes on 8 cores each; run once in the build container).
 
-    python tests/golden/make_c2.py [c2|c3]
+    python tests/golden/make_c2.py [c2|c3|c2host|c3host]
+
+`*host` adds the host tier of SURVEY §8(d): host 50,000 B/us both ways,
+host_cap 256e9 (output: tests/golden/<config>.json.gz).
 
 The reference planner cannot run at C2 (~8 h per round), so the
 C2/C3 checker is the oracle (oracle/tio_oracle.c), whose bit-exactness against
@@ -27,18 +30,26 @@ def main(config: str = "c2"):
     from oracle import oracle as O
     from paper_2506_06472_b200 import LLAMA3_8B, LLAMA3_70B, gen_llama_trace, write_trace
     from paper_2506_06472_b200.tracegen import llama_peak_bytes
-    tr = gen_llama_trace({"c2": LLAMA3_8B, "c3": LLAMA3_70B}[config])
+    host = config.endswith("host")
+    tr = gen_llama_trace({"c2": LLAMA3_8B, "c3": LLAMA3_70B}[config[:2]])
     a = tr.arrays()
     cap = llama_peak_bytes(tr) // 2
+    rates = [16000, 16000, 50000, 50000] if host else [16000, 16000, None, None]
+    host_cap = 256 * 10**9 if host else 0
     t0 = time.time()
-    p = O.plan(a, cap, 16000.0, 16000.0, verbose=True)
+    if host:
+        p = O.plan(a, cap, 16000.0, 16000.0, 50000.0, 50000.0, host_cap, verbose=True)
+    else:
+        p = O.plan(a, cap, 16000.0, 16000.0, verbose=True)
     rec = {
         "trace_sha256": hashlib.sha256(write_trace(tr)).hexdigest(),
-        "num_events": a.num_events, "capacity": cap, "rates": [16000, 16000, None, None], "host_cap": 0,
+        "num_events": a.num_events, "capacity": cap, "rates": rates, "host_cap": host_cap,
         "rounds": int(p["rounds"]), "num_commits": len(p["committed"]),
         "plan_sha256": hashlib.sha256(p["plan_bytes"]).hexdigest(),
         "residual_sha256": hashlib.sha256(p["residual"].astype("<i8").tobytes()).hexdigest(),
         "over_capacity_kernels": len(p["over_capacity_kernels"]),
+        "host_commits": int(sum(1 for c in p["committed"] if c[4] == "CPU")),
+        "planned_host_bytes": int(p["planned_host_bytes"]),
         "oracle_seconds": round(time.time() - t0, 1), "oracle_threads": int(O.lib().tio_oracle_threads()),
     }
     with gzip.open(os.path.join(HERE, f"{config}.json.gz"), "wt") as f:

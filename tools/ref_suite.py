@@ -1,0 +1,81 @@
+"""Run the REFERENCE's own test suite against this package (drop-in proof,
+SURVEY §7 step 2).
+
+    python tools/ref_suite.py prepare     # build container: stage the suite
+    python tools/ref_suite.py run [-- pytest args]   # GPU box: run it
+
+`prepare` copies /root/reference/pkg/tests/*.py (the reference's tests,
+fixtures and brute-force oracles) and the reference's out-of-scope CLI module
+(cli.py: argparse front-end + Table-2 cost model) into
+oracle/_ref/ref_suite/ — git-ignored (reference code stays out of this repo's
+history) but not gpurun-ignored, so it travels to the GPU box, where
+/root/reference does not exist.
+
+`run` registers this package as `offloader` (and its modules as
+`offloader.analysis`, `.bandwidth`, `.planner`, `.roofline`, `.simulator`,
+`.trace`, `.tracegen`) before pytest imports the suite; `offloader.cli` is
+the staged reference CLI, whose relative imports (`from . import planner`)
+therefore resolve to this package — every planner / lifetime / engine call
+the suite makes runs on libtio.  The reference itself reports 134 pass / 2
+fail (criteria 3 and 5 of test_acceptance.py).
+"""
+
+from __future__ import annotations
+
+import glob
+import importlib.util
+import os
+import shutil
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+STAGE = os.path.join(ROOT, "oracle", "_ref", "ref_suite")
+REF = "/root/reference/pkg"
+
+
+def prepare() -> None:
+    os.makedirs(STAGE, exist_ok=True)
+    for f in glob.glob(os.path.join(REF, "tests", "*.py")):
+        shutil.copy(f, STAGE)
+    shutil.copy(os.path.join(REF, "src", "offloader", "cli.py"), os.path.join(STAGE, "_ref_cli.py"))
+    print("staged", len(os.listdir(STAGE)), "files in", STAGE)
+
+
+def install_alias() -> None:
+    """sys.modules['offloader*'] -> this package (the `-p` plugin hook)."""
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
+    import paper_2506_06472_b200 as P
+    from paper_2506_06472_b200 import analysis, bandwidth, planner, roofline, simulator, trace, tracegen
+    sys.modules["offloader"] = P
+    for name, mod in (("analysis", analysis), ("bandwidth", bandwidth), ("planner", planner),
+                      ("roofline", roofline), ("simulator", simulator), ("trace", trace),
+                      ("tracegen", tracegen)):
+        sys.modules["offloader." + name] = mod
+    cli_path = os.path.join(STAGE, "_ref_cli.py")
+    if os.path.exists(cli_path):
+        spec = importlib.util.spec_from_file_location("offloader.cli", cli_path)
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules["offloader.cli"] = mod
+        spec.loader.exec_module(mod)
+
+
+def run(args: list[str]) -> int:
+    import pytest
+    if not os.path.isdir(STAGE):
+        print("ref suite not staged (python tools/ref_suite.py prepare in the build container)")
+        return 2
+    sys.path.insert(0, STAGE)            # `from conftest import mk_trace`, `from oracle_plan import ...`
+    install_alias()
+    return pytest.main([STAGE, "-p", "no:cacheprovider", "-q", "-rf"] + args)
+
+
+if __name__ == "__main__":
+    cmd = sys.argv[1] if len(sys.argv) > 1 else "run"
+    if cmd == "prepare":
+        prepare()
+    else:
+        extra = sys.argv[2:]
+        if extra and extra[0] == "--":
+            extra = extra[1:]
+        sys.exit(run(extra))
