@@ -26,6 +26,7 @@ key.  Both plans are bit-exact with the oracle fingerprints in tests/golden.
 
 --impl reference times that CPU path (the reference's algorithm; the Python
 reference itself cannot run here: ~8 h per planner round at C2)
+over one FULL lifetime + plan of the trace (measured, with its plan sha256)
 and prints its own JSON line.  Multi-GPU (torchrun): each rank plans its own
 replica of the trace ("replicas only" for this config), timing is
 the max over ranks.
@@ -168,32 +169,62 @@ def cpu_baseline(config: str, rounds_total: int | None, sample_rounds: int = 40,
 
 
 def run_reference(args, rank: int, world: int):
+    """The reference arm: the reference's algorithm on this host's cores — the
+    oracle port (oracle/tio_oracle.c, OpenMP over candidates; the Python
+    reference itself needs ~716 h per planner round at C3).
+
+    Each timed step is one FULL lifetime + plan of the config's trace (C3:
+    ~150 s on 16 threads), so the value is measured, not extrapolated, and the
+    arm prints the plan's sha256 (equal to the GPU arm's and to
+    tests/golden/<config>.json.gz).  At most --ref-full-steps of the requested
+    K steps are run (a full C3 plan per step); warm-up steps run the lifetime
+    stage only (page-in, thread pool start).  The old 12-round extrapolation is
+    kept under "sampled_extrapolation" as a labelled secondary."""
     if rank != 0:
         return
-    # the oracle port as the reference's CPU path, all host threads
+    import hashlib
+    from oracle import oracle as O
     tr, cap, rates, hc, desc = _trace(args.config)
-    rounds_total = args.ref_rounds_total
-    vals = []
+    a = tr.arrays()
+    E = a.num_events
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
+    L = O.lib()
     for _ in range(args.warmup):
-        cpu_baseline(args.config, rounds_total, sample_rounds=args.ref_rounds_c3
-                     if args.config == "c3" else args.ref_rounds)
-    t0 = time.perf_counter()
-    last = None
-    for _ in range(args.steps):
-        last = cpu_baseline(args.config, rounds_total, sample_rounds=args.ref_rounds_c3
-                            if args.config == "c3" else args.ref_rounds)
-        vals.append(last["value"])
-    wall = time.perf_counter() - t0
-    v = statistics.mean(vals)
-    E = tr.arrays().num_events
+        O.lifetime(a)
+    steps = max(1, min(args.steps, args.ref_full_steps))
+    t_life, t_plan, shas, rounds = [], [], set(), 0
+    wall0 = time.perf_counter()
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        lo = O.lifetime(a)
+        t1 = time.perf_counter()
+        p = O.plan(a, cap, rates.ssd_offload, rates.ssd_prefetch, rates.host_offload, rates.host_prefetch, hc,
+                   lifetime_out=lo)
+        t2 = time.perf_counter()
+        t_life.append(t1 - t0)
+        t_plan.append(t2 - t1)
+        shas.add(hashlib.sha256(p["plan_bytes"]).hexdigest())
+        rounds = int(p["rounds"])
+    wall = time.perf_counter() - wall0
+    sec = sum(t_life) + sum(t_plan)
+    v = E * steps / sec
+    sample = (f"oracle/tio_oracle.c on {args.config}: {steps} full lifetime + plan pass(es) "
+              f"(lifetime {statistics.mean(t_life):.2f} s, plan {statistics.mean(t_plan):.1f} s, "
+              f"{rounds} rounds), measured")
     line = {"metric": "trace events/s (lifetime+plan)", "value": v, "unit": "events/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * E / v,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": desc, "events": E, "capacity": cap, "rates": "ssd 16000 B/us symmetric"},
-            "cpu_baseline": {**last, "value": v},
+            "steps": steps, "steps_requested": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sec / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": desc, "events": E, "capacity": cap, "rates": "ssd 16000 B/us symmetric",
+                       "host_cap": hc, "plan_sha256": sorted(shas)[0] if len(shas) == 1 else sorted(shas)},
+            "cpu_baseline": {"value": v, "unit": "events/s", "cores": int(L.tio_oracle_threads()), "kind": "port",
+                             "sample": sample},
             "e2e": {"value": v, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "wall_s": wall}
+            "breakdown_s": {"lifetime": statistics.mean(t_life), "plan": statistics.mean(t_plan)},
+            "rounds": rounds, "wall_s": wall}
+    if args.ref_sampled:
+        line["sampled_extrapolation"] = cpu_baseline(args.config, rounds, sample_rounds=args.ref_rounds_c3
+                                                     if args.config == "c3" else args.ref_rounds)
     print(json.dumps(line), flush=True)
 
 
@@ -494,7 +525,11 @@ def main(argv=None):
     ap.add_argument("--ref-rounds", type=int, default=40, help="planner rounds in the CPU sample (C2)")
     ap.add_argument("--ref-rounds-c3", type=int, default=12, help="planner rounds in the CPU sample (C3)")
     ap.add_argument("--ref-rounds-total", type=int, default=None,
-                    help="total rounds of the full plan (for the reference arm's extrapolation)")
+                    help="total rounds of the full plan (for the sampled extrapolation)")
+    ap.add_argument("--ref-full-steps", type=int, default=1,
+                    help="reference arm: full lifetime+plan passes actually timed (each ~150 s at C3)")
+    ap.add_argument("--ref-sampled", action="store_true",
+                    help="reference arm: also report the old sampled-round extrapolation")
     args = ap.parse_args(argv)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -348,3 +348,31 @@ def test_characterization_known_answers(ex1):
     assert fractions_csv(rep).splitlines()[0] == "kernel,active_bytes,active_fraction"
     assert len(fractions_csv(rep).splitlines()) == 6
     assert histogram_csv(rep).splitlines()[0] == "size_class_bytes,duration_class_us,count"
+
+
+@pytest.mark.parametrize("config", ["c2", "c3"])
+def test_lifetime_vs_reference_itself_at_scale(config):
+    """C2 (1.0M events) and C3 (9.9M events) lifetime products against the
+    REFERENCE's own outputs (tests/golden/make_ref_lifetime.py ran
+    compute_inactive_periods / compute_memory_timeline / per_kernel_active_bytes
+    of /root/reference on the same trace: 237 s at C3), as sha256 of the
+    int64 rows (tensor_id, size, start, end, wraps), timeline and active bytes."""
+    import json
+    import os
+    from paper_2506_06472_b200 import LLAMA3_8B, LLAMA3_70B, gen_llama_trace
+    path = os.path.join(os.path.dirname(__file__), "golden", f"{config}_lifetime_ref.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    with open(path) as f:
+        rec = json.load(f)
+    tr = gen_llama_trace({"c2": LLAMA3_8B, "c3": LLAMA3_70B}[config])
+    a = tr.arrays()
+    assert a.num_events == rec["num_events"]
+    la = lifetime_arrays(tr)
+    rows = np.stack([a.tensor_id[la.period_tensor], a.size_bytes[la.period_tensor], la.period_start.astype(np.int64),
+                     la.period_end.astype(np.int64), la.period_wraps.astype(np.int64)], axis=1)
+    h = lambda x: hashlib.sha256(np.ascontiguousarray(x, dtype="<i8").tobytes()).hexdigest()  # noqa: E731
+    assert rows.shape[0] == rec["num_periods"]
+    assert h(rows) == rec["periods_sha256"]
+    assert h(la.timeline) == rec["timeline_sha256"]
+    assert h(la.active) == rec["active_sha256"]

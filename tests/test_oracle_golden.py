@@ -105,3 +105,19 @@ def test_oracle_timeline_matches_bruteforce_residency():
         assert np.array_equal(timeline, want)
         assert np.array_equal(active, want_act)
         assert (active <= timeline).all()
+
+
+def test_oracle_lifetime_vs_reference_itself_at_c2():
+    """C2 (1.0M events): the oracle's lifetime products against the
+    reference's own (tests/golden/c2_lifetime_ref.json, make_ref_lifetime.py)."""
+    import json
+    import os
+    from paper_2506_06472_b200 import LLAMA3_8B, gen_llama_trace
+    with open(os.path.join(os.path.dirname(__file__), "golden", "c2_lifetime_ref.json")) as f:
+        rec = json.load(f)
+    a = gen_llama_trace(LLAMA3_8B).arrays()
+    per, tl, act = O.lifetime(a)
+    rows = np.stack([a.tensor_id[per["tensor"]], a.size_bytes[per["tensor"]], per["start"].astype(np.int64),
+                     per["end"].astype(np.int64), per["wraps"].astype(np.int64)], axis=1)
+    h = lambda x: hashlib.sha256(np.ascontiguousarray(x, dtype="<i8").tobytes()).hexdigest()  # noqa: E731
+    assert (h(rows), h(tl), h(act)) == (rec["periods_sha256"], rec["timeline_sha256"], rec["active_sha256"])
