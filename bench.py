@@ -464,10 +464,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         # each) would exceed the box's host memory, so the leg runs at N = 1 only
         from paper_2506_06472_b200 import engine
         link = engine.measure_link()
-        # (microbatches, capacity / peak): the heavy-pressure point at 4
-        # microbatches (its pinned host extents are ~72 GB), the lighter ones
-        # at 8 (a longer step to hide the transfers in)
-        line["migration"] = [migration_bench(mb, link=link, cap_frac=f) for mb, f in ((4, 0.5), (8, 0.8), (8, 0.9))]
+        line["migration"] = real_step_bench(link=link, model=args.offload_model)
+        if args.replay_leg:
+            # the synthetic Appendix-C replay against placeholder kernels (round 1's leg)
+            line["migration_replay"] = [migration_bench(mb, link=link, cap_frac=f)
+                                        for mb, f in ((4, 0.5), (8, 0.8), (8, 0.9))]
     print(json.dumps(line), flush=True)
 
 
@@ -510,6 +511,143 @@ def migration_bench(microbatches: int = 8, verify: bool = True, link: dict | Non
     }
 
 
+def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = None, model: str = "8b") -> dict:
+    """Configs C4 (BASELINE.json configs[3]): the migration engine executing
+    the plan of a REAL Llama-3-8B training step on 1 B200 (random init bf16
+    weights, fp32 AdamW moments, synthetic 8,192-token batch;
+    paper_2506_06472_b200/llama_step.py).
+
+    ideal   the same step, no engine, capacity unconstrained;
+    profile one step under TraceProfiler -> trace (every aten operator a
+            kernel, CUDA-event durations) -> device plan at capacity =
+            frac x the trace's memory-timeline peak, channel rates = the
+            measured pinned link (both directions busy);
+    run     fresh model, same step sequence, OffloadMode (libtio online
+            engine: storages freed / restored on side streams, event gated).
+
+    Each timed step (K back to back, CUDA events on the compute stream, the
+    last step fenced on every transfer) includes the batch H2D from pinned
+    host and the loss D2H.  Checked: losses and the checksum of every weight /
+    moment after the timed steps equal the ideal run's; one verification step
+    (checksum of every tensor at offload and after prefetch) before timing."""
+    import gc
+    import torch
+    from paper_2506_06472_b200 import ChannelRates, compute_memory_timeline, engine, plan_migrations
+    from paper_2506_06472_b200.llama_step import LLAMA3_8B_MODEL, TINY, Step
+    from paper_2506_06472_b200.profiler import profile_step
+    cfg = LLAMA3_8B_MODEL if model == "8b" else TINY
+    dev = torch.device("cuda")
+    link = link or engine.measure_link()
+    rate = float(int(link["bidir_gbs_each"] * 1e3))            # bytes/us, integral
+    rates = ChannelRates.symmetric(rate)
+    stream = torch.cuda.current_stream()
+    loss_host = torch.empty((), dtype=torch.float32, pin_memory=True)
+
+    def run(s, n, mode=None):
+        losses = []
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(n):
+            batch = s.host_batch.to(dev, non_blocking=True)
+            if mode is None:
+                loss = s(batch)
+            else:
+                with mode.step(done_stream=stream if i == n - 1 else None):
+                    loss = s(batch)
+            loss_host.copy_(loss, non_blocking=True)
+            losses.append(loss)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n, [float(x.item()) for x in losses], torch.cuda.max_memory_allocated()
+
+    def digest(s):
+        names = sorted(s.globals_of())
+        g = s.globals_of()
+        return engine.checksums([g[n] for n in names])
+
+    def free(*objs):
+        del objs
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+    # ---- ideal: plain PyTorch, capacity unconstrained
+    s = Step(cfg, seed=0)
+    for _ in range(3):
+        s()
+    ideal_ms, ideal_losses, ideal_peak = run(s, steps)
+    ideal_digest = digest(s)
+    free(s)
+    s = None
+
+    # ---- profile (step 2 of a fresh model) -> trace
+    s = Step(cfg, seed=0)
+    s()
+    t0 = time.perf_counter()
+    tr = profile_step(s, globals_=s.globals_of(), meta={"generator": "TraceProfiler", "model": f"llama3-{model}"})
+    t_prof = time.perf_counter() - t0
+    a = tr.arrays()
+    peak = compute_memory_timeline(tr).peak()
+    out = {"workload": f"Llama-3-{model.upper()} real training step (random init bf16 weights, fp32 AdamW, "
+                       f"1 x {cfg.seq} synthetic tokens); trace of the profiled step: {a.num_kernels} kernels "
+                       f"(aten operators), {a.num_tensors} tensors, {a.num_events} events, peak {peak} B",
+           "link": link, "plan_rates_bytes_per_us": rate,
+           "ideal": {"step_ms": ideal_ms, "allocator_peak_bytes": ideal_peak, "losses": ideal_losses},
+           "profile_s": t_prof, "runs": []}
+    first = True
+    for frac in fracs:
+        cap = int(peak * frac)
+        t0 = time.perf_counter()
+        plan = plan_migrations(tr, cap, rates)
+        t_plan = time.perf_counter() - t0
+        if not first:
+            s = Step(cfg, seed=0)
+            for _ in range(2):
+                s()
+        first = False
+        mode = engine.OffloadMode(tr, plan, cap, rates, s.globals_of(), verify=True)
+        with mode.step():                      # step 3: sets up the steady state, checksums every round trip
+            s()
+        torch.cuda.synchronize()
+        vst = mode.stats()
+        mode.set_verify(False)
+        ms, losses, apeak = run(s, steps, mode)
+        st = mode.stats()
+        dg = digest(s)
+        info = mode.info
+        off_gbs = st["last_offload_bytes"] / (st["last_offload_busy_ms"] * 1e6) if st["last_offload_busy_ms"] else 0.0
+        pre_gbs = st["last_prefetch_bytes"] / (st["last_prefetch_busy_ms"] * 1e6) if st["last_prefetch_busy_ms"] else 0.0
+        per_step_off = st["offload_bytes"] / max(1, st["steps"])
+        per_step_pre = st["prefetch_bytes"] / max(1, st["steps"])
+        lb_ms = max(per_step_off / (link["d2h_gbs"] * 1e6), per_step_pre / (link["h2d_gbs"] * 1e6))
+        out["runs"].append({
+            "capacity_frac_of_trace_peak": frac, "capacity": cap,
+            "plan": {"entries": len(plan.entries), "warning": plan.warning,
+                     "over_capacity_kernels": len(plan.over_capacity_kernels), "seconds": t_plan},
+            "step_ms": ms, "step_vs_ideal": ms / ideal_ms,
+            "model_step_vs_ideal": info["model_total_us"] / max(1, info["model_ideal_us"]),
+            "link_lower_bound_ms": lb_ms, "link_lower_bound_vs_ideal": max(1.0, lb_ms / ideal_ms),
+            "allocator_peak_bytes": apeak, "allocator_peak_vs_capacity": apeak / cap,
+            "model_peak_resident": info["model_peak_resident"],
+            "offload_gbs": off_gbs, "prefetch_gbs": pre_gbs,
+            "offload_frac_of_link_d2h": off_gbs / link["d2h_gbs"] if link["d2h_gbs"] else None,
+            "prefetch_frac_of_link_h2d": pre_gbs / link["h2d_gbs"] if link["h2d_gbs"] else None,
+            "bytes_per_step": {"offload": per_step_off, "prefetch": per_step_pre, "host_extents": info["host_bytes"]},
+            "transfers_per_step": {"offloads": info["model_offloads"], "prefetches": info["model_prefetches"],
+                                   "emergency": info["emergency_offloads"]},
+            "verify": {"round_trips_checked": vst["n_prefetches"], "mismatches": vst["verify_mismatches"]},
+            "losses": losses, "losses_equal_ideal": losses == ideal_losses,
+            "state_checksums_equal_ideal": dg == ideal_digest,
+        })
+        mode.close()
+        free(mode, s)
+        s = None
+    out["tier"] = "pinned host extents (4 KB aligned) via cudaMemcpyAsync on per-channel side streams"
+    return out
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -521,7 +659,11 @@ def main(argv=None):
     ap.add_argument("--secondary", default="c2", choices=["", "c1", "c2", "c3", "llama1"],
                     help="second workload reported under its own key (default C2, BASELINE configs[1])")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-migration", action="store_true", help="skip the C4 engine replay leg")
+    ap.add_argument("--no-migration", action="store_true", help="skip the C4 offloaded-step leg")
+    ap.add_argument("--offload-model", default="8b", choices=["8b", "tiny"],
+                    help="model of the C4 leg (8b = Llama-3-8B; tiny for quick checks)")
+    ap.add_argument("--replay-leg", action="store_true",
+                    help="also run the Appendix-C replay against placeholder kernels")
     ap.add_argument("--ref-rounds", type=int, default=40, help="planner rounds in the CPU sample (C2)")
     ap.add_argument("--ref-rounds-c3", type=int, default=12, help="planner rounds in the CPU sample (C3)")
     ap.add_argument("--ref-rounds-total", type=int, default=None,

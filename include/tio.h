@@ -294,6 +294,62 @@ typedef struct tio_engine_stats {
 int tio_engine_replay(const tio_trace_desc *trace, const tio_entry *entries, int64_t num_entries,
                       const tio_engine_config *cfg, void *stream, tio_engine_stats *stats);
 
+/* ---- online migration engine (a real training step) -------------------------
+ * The engine program of tio_engine_replay, driven by the framework around
+ * every operator of the real step instead of placeholder kernels
+ * (simulator.py:178-528 `_Engine` semantics, PAPER.md:429-444 runtime):
+ * create() schedules the plan once over the profiled durations; per step the
+ * framework calls step_begin, then before_kernel(k) / after_kernel(k) around
+ * kernel (operator) k of the profiled trace, then step_end.  Device memory
+ * stays the framework's: the engine calls
+ *   alloc_cb(user, tensor_pos, bytes, &dev_ptr)  when a prefetch starts (the
+ *       framework allocates on the compute stream; the engine orders the copy
+ *       after the compute stream's current position), and
+ *   free_cb(user, tensor_pos, stream)            after an offload's D2H copy is
+ *       enqueued on `stream` (the framework frees once that stream passes
+ *       this point, e.g. record_stream + storage resize to 0).
+ * Both return 0 on success.  bind() tells the engine the device address of
+ * a tensor it may move (globals before the first step; tensors created by
+ * kernel k via after_kernel).  Tiers: pinned host extents (4 KB aligned) on
+ * one side stream per channel (ssd / host x offload / prefetch).
+ * cfg.verify: checksum every tensor at offload and after prefetch, mismatches
+ * counted on the device (tio_engine_stats_get). */
+typedef int (*tio_alloc_cb)(void *user, int64_t tensor_pos, int64_t bytes, void **dev_ptr);
+typedef int (*tio_free_cb)(void *user, int64_t tensor_pos, void *stream);
+typedef struct tio_engine tio_engine;
+
+typedef struct tio_engine_info_t {
+    int64_t num_kernels, num_tensors, num_transfers, host_bytes;
+    int64_t model_total_us, model_ideal_us, model_stall_us, model_peak_resident, emergency_offloads;
+    int64_t model_offload_bytes, model_prefetch_bytes, model_offloads, model_prefetches;
+} tio_engine_info_t;
+
+typedef struct tio_engine_online_stats {
+    int64_t steps, offload_bytes, prefetch_bytes, n_offloads, n_prefetches;   /* all steps */
+    double last_offload_busy_ms, last_prefetch_busy_ms;                      /* last step, per-copy device time */
+    int64_t last_offload_bytes, last_prefetch_bytes;
+    int64_t verify, verify_mismatches;
+} tio_engine_online_stats;
+
+int tio_engine_create(const tio_trace_desc *trace, const tio_entry *entries, int64_t num_entries,
+                      const tio_engine_config *cfg, void *compute_stream, tio_alloc_cb alloc_cb, tio_free_cb free_cb,
+                      void *user, tio_engine **out);
+/* movable (optional, [num_tensors]): 1 for tensors the engine may move (bind these) */
+int tio_engine_info(const tio_engine *eng, tio_engine_info_t *info, uint8_t *movable);
+int tio_engine_bind(tio_engine *eng, int64_t n, const int64_t *tensor_pos, void *const *dev_ptr);
+int tio_engine_step_begin(tio_engine *eng);
+int tio_engine_before_kernel(tio_engine *eng, int64_t k);
+int tio_engine_after_kernel(tio_engine *eng, int64_t k, int64_t n_new, const int64_t *new_pos, void *const *new_ptr);
+/* done_stream (optional): made to wait for every transfer issued so far */
+int tio_engine_step_end(tio_engine *eng, void *done_stream);
+int tio_engine_stats_get(tio_engine *eng, tio_engine_online_stats *stats);
+int tio_engine_destroy(tio_engine *eng);
+/* turn checksum verification on / off between steps */
+int tio_engine_set_verify(tio_engine *eng, int verify);
+/* the engine's verification checksum of a device buffer (order-independent
+ * 64-bit sum of mixed words), written to *dev_out on `stream` */
+int tio_checksum(const void *dev_ptr, int64_t bytes, unsigned long long *dev_out, void *stream);
+
 /* K10: gather n device buffers into 4 KB-aligned extents of `staging`
  * (offsets[i] out) / scatter them back, with TMA bulk copies.  scratch: a
  * device buffer of >= 64 * n + 64 bytes for the segment tables. */

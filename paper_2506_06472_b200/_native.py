@@ -107,7 +107,11 @@ EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_devi
            "tio_plan_create", "tio_plan_create2", "tio_plan_info_get", "tio_plan_copy_out", "tio_plan_write",
            "tio_plan_destroy", "tio_plan_host", "tio_transfer_duration", "tio_simulate", "tio_simulate_layers", "tio_roofline",
            "tio_engine_replay", "tio_pack", "tio_unpack", "tio_schedule", "tio_trace_parse",
-           "tio_parsed_sizes", "tio_parsed_copy", "tio_parsed_destroy")
+           "tio_parsed_sizes", "tio_parsed_copy", "tio_parsed_destroy",
+           "tio_engine_create", "tio_engine_info", "tio_engine_bind", "tio_engine_step_begin",
+           "tio_engine_before_kernel", "tio_engine_after_kernel", "tio_engine_step_end", "tio_engine_stats_get",
+           "tio_engine_destroy", "tio_checksum",
+           "tio_engine_set_verify")
 
 
 def lib_path() -> str:

@@ -9,9 +9,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
 echo "bench rc=$?"; cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
 if [ -z "$NO_NCU" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 1 --warmup 0 --no-cpu-baseline ${BENCH_ARGS} > /dev/null 2>gpurun_out/ncu1.err
+    python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-migration ${BENCH_ARGS} > /dev/null 2>gpurun_out/ncu1.err
 echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_events} -c 1 \
-    -o gpurun_out/prof_${NCU_KERNEL:-k_events} -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline ${BENCH_ARGS} > /dev/null 2>gpurun_out/ncu2.err
+    -o gpurun_out/prof_${NCU_KERNEL:-k_events} -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-migration ${BENCH_ARGS} > /dev/null 2>gpurun_out/ncu2.err
 echo "ncu full rc=$?"
 fi
