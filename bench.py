@@ -615,6 +615,7 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
         mode.set_verify(False)
         ms, losses, apeak = run(s, steps, mode)
         st = mode.stats()
+        mode.restore()                         # globals offloaded at the step boundary come back
         dg = digest(s)
         info = mode.info
         off_gbs = st["last_offload_bytes"] / (st["last_offload_busy_ms"] * 1e6) if st["last_offload_busy_ms"] else 0.0

@@ -329,6 +329,7 @@ typedef struct tio_engine_online_stats {
     double last_offload_busy_ms, last_prefetch_busy_ms;                      /* last step, per-copy device time */
     int64_t last_offload_bytes, last_prefetch_bytes;
     int64_t verify, verify_mismatches;
+    int64_t reconcile_transfers, reconcile_bytes;   /* step-boundary fix-ups (all steps) */
 } tio_engine_online_stats;
 
 int tio_engine_create(const tio_trace_desc *trace, const tio_entry *entries, int64_t num_entries,
@@ -342,8 +343,20 @@ int tio_engine_before_kernel(tio_engine *eng, int64_t k);
 int tio_engine_after_kernel(tio_engine *eng, int64_t k, int64_t n_new, const int64_t *new_pos, void *const *new_ptr);
 /* done_stream (optional): made to wait for every transfer issued so far */
 int tio_engine_step_end(tio_engine *eng, void *done_stream);
+/* leave a step that failed (framework exception): waits for the engine's
+ * streams; restore() then brings the globals back */
+int tio_engine_step_abort(tio_engine *eng);
 int tio_engine_stats_get(tio_engine *eng, tio_engine_online_stats *stats);
 int tio_engine_destroy(tio_engine *eng);
+/* Walk the engine program of `steps` consecutive steps without a device (no
+ * CUDA calls; fake addresses): fails with the engine's own error when the
+ * program would offload a tensor that is not resident, prefetch a resident
+ * one or launch a kernel whose tensor is off the GPU.  Host-only. */
+int tio_engine_check_program(const tio_trace_desc *trace, const tio_entry *entries, int64_t num_entries,
+                             const tio_engine_config *cfg, int64_t steps, tio_engine_info_t *info);
+/* between steps: bring every global whose latest copy is off the GPU back
+ * (synchronous) and reset to the pre-steady-state (the next step sets it up) */
+int tio_engine_restore(tio_engine *eng);
 /* turn checksum verification on / off between steps */
 int tio_engine_set_verify(tio_engine *eng, int verify);
 /* the engine's verification checksum of a device buffer (order-independent

@@ -111,7 +111,8 @@ EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_devi
            "tio_engine_create", "tio_engine_info", "tio_engine_bind", "tio_engine_step_begin",
            "tio_engine_before_kernel", "tio_engine_after_kernel", "tio_engine_step_end", "tio_engine_stats_get",
            "tio_engine_destroy", "tio_checksum",
-           "tio_engine_set_verify")
+           "tio_engine_set_verify", "tio_engine_restore",
+           "tio_engine_check_program", "tio_engine_step_abort")
 
 
 def lib_path() -> str:

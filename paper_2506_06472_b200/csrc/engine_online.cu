@@ -108,6 +108,10 @@ static int launch_checksum(const void *p, int64_t bytes, unsigned long long *out
 
 using namespace tio;
 
+// CUDA calls of the engine are skipped in a dry (program-check) engine
+#define GPU(expr) do { if (!dry) TIO_CUDA(expr); } while (0)
+#define EGPU(expr) do { if (!E->dry) TIO_CUDA(expr); } while (0)
+
 struct tio_engine {
     // owned trace columns + plan (the caller's arrays need not outlive create)
     std::vector<int64_t> dur, tid, size, ptr;
@@ -146,10 +150,16 @@ struct tio_engine {
 
     int64_t step = 0, cursor = 0, next_kernel = 0;
     bool in_step = false;
+    bool dry = false;                        // program walk only: no CUDA calls, internal callbacks
     int64_t bytes_dir[2] = {0, 0}, count_dir[2] = {0, 0};
     std::vector<uint8_t> issued_this_step;
+    std::vector<int8_t> xact_rec;            // action of each reconciliation slot
+    std::vector<uint8_t> end_resident;       // per global: resident when the next step begins (program view)
+    std::vector<uint8_t> reconciled;         // per tensor: moved by the last step_end's reconciliation
+    int64_t n_reconcile = 0, bytes_reconcile = 0;
 
     ~tio_engine() {
+        if (dry) return;
         if (comp) cudaStreamSynchronize(comp);
         for (int c = 0; c < 4; ++c) if (ch[c]) { cudaStreamSynchronize(ch[c]); cudaStreamDestroy(ch[c]); }
         for (auto e : pool) cudaEventDestroy(e);
@@ -158,7 +168,7 @@ struct tio_engine {
         if (dcs) cudaFree(dcs);
     }
     int mk_event(cudaEvent_t *e, bool timing) {
-        TIO_CUDA(cudaEventCreateWithFlags(e, timing ? cudaEventDefault : cudaEventDisableTiming));
+        GPU(cudaEventCreateWithFlags(e, timing ? cudaEventDefault : cudaEventDisableTiming));
         pool.push_back(*e);
         return TIO_OK;
     }
@@ -173,53 +183,64 @@ struct tio_engine {
     }
     int channel_of(const SchedTransfer &x) const { return (x.device == LOC_SSD ? 0 : 2) + x.action; }
 
-    int offload(int64_t xi, bool wait_issue) {
-        const SchedTransfer &x = sc.transfers[xi];
-        const int64_t t = x.tensor, nb = size[t];
-        cudaStream_t s = ch[channel_of(x)];
-        if (wait_issue && x.issue_kernel >= 0) TIO_CUDA(cudaStreamWaitEvent(s, kdone[x.issue_kernel], 0));
-        if (last_x[t] >= 0) TIO_CUDA(cudaStreamWaitEvent(s, xdone[last_x[t]], 0));
-        if (last_k[t] >= 0) TIO_CUDA(cudaStreamWaitEvent(s, kdone[last_k[t]], 0));
+    // transfer slots: [0, X) the program's transfers, [X, X + T) one
+    // reconciliation slot per tensor (step_end)
+    int64_t slot_action(int64_t slot) const {
+        return slot < X ? sc.transfers[slot].action : xact_rec[slot - X];
+    }
+    int offload(int64_t t, int c, int64_t slot, int64_t wait_kernel) {
+        const int64_t nb = size[t];
+        cudaStream_t s = ch[c];
+        if (wait_kernel >= 0) GPU(cudaStreamWaitEvent(s, kdone[wait_kernel], 0));
+        if (last_x[t] >= 0) GPU(cudaStreamWaitEvent(s, xdone[last_x[t]], 0));
+        if (last_k[t] >= 0) GPU(cudaStreamWaitEvent(s, kdone[last_k[t]], 0));
         if (!dptr[t])
-            return fail(TIO_ERR_INTERNAL, "offload of tensor %lld that is not resident / not bound", (long long)tid[t]);
-        if (cfg.verify) TIO_TRY(launch_checksum(dptr[t], nb, dcs + t, s));
-        TIO_CUDA(cudaEventRecord(xt0[xi], s));
-        TIO_CUDA(cudaMemcpyAsync(host + hoff[t], dptr[t], (size_t)nb, cudaMemcpyDeviceToHost, s));
-        TIO_CUDA(cudaEventRecord(xt1[xi], s));
+            return fail(TIO_ERR_INTERNAL, "step %lld: offload of tensor %lld that is not resident / not bound",
+                        (long long)step, (long long)tid[t]);
+        if (cfg.verify && !dry) TIO_TRY(launch_checksum(dptr[t], nb, dcs + t, s));
+        GPU(cudaEventRecord(xt0[slot], s));
+        GPU(cudaMemcpyAsync(host + hoff[t], dptr[t], (size_t)nb, cudaMemcpyDeviceToHost, s));
+        GPU(cudaEventRecord(xt1[slot], s));
         if (free_cb(user, t, (void *)s) != 0)
             return fail(TIO_ERR_INVALID, "free callback failed for tensor %lld", (long long)tid[t]);
         dptr[t] = nullptr;
+        GPU(cudaEventRecord(xdone[slot], s));
+        last_x[t] = slot;
         return TIO_OK;
     }
-    int prefetch(int64_t xi) {
-        const SchedTransfer &x = sc.transfers[xi];
-        const int64_t t = x.tensor, nb = size[t];
-        cudaStream_t s = ch[channel_of(x)];
+    int prefetch(int64_t t, int c, int64_t slot, int64_t mem_time) {
+        const int64_t nb = size[t];
+        cudaStream_t s = ch[c];
         // the model reserves memory at prefetch start once the offloads it
         // counted as complete have freed theirs (simulator.py:353-354)
-        for (int dv = 0; dv < 2; ++dv) {
-            const int64_t lo = latest_off_before(dv, x.start);
-            if (lo >= 0) TIO_CUDA(cudaStreamWaitEvent(s, xdone[lo], 0));
-        }
-        if (last_x[t] >= 0) TIO_CUDA(cudaStreamWaitEvent(s, xdone[last_x[t]], 0));
-        if (dptr[t]) return fail(TIO_ERR_INTERNAL, "prefetch of resident tensor %lld", (long long)tid[t]);
+        if (mem_time >= 0)
+            for (int dv = 0; dv < 2; ++dv) {
+                const int64_t lo = latest_off_before(dv, mem_time);
+                if (lo >= 0) GPU(cudaStreamWaitEvent(s, xdone[lo], 0));
+            }
+        if (last_x[t] >= 0) GPU(cudaStreamWaitEvent(s, xdone[last_x[t]], 0));
+        if (dptr[t])
+            return fail(TIO_ERR_INTERNAL, "step %lld: prefetch of resident tensor %lld", (long long)step,
+                        (long long)tid[t]);
         void *p = nullptr;
         if (alloc_cb(user, t, nb, &p) != 0 || !p)
             return fail(TIO_ERR_NOMEM, "alloc callback failed for tensor %lld (%lld bytes)", (long long)tid[t],
                         (long long)nb);
         // the framework allocated in compute-stream order: the block is free
         // for the channel only once the compute stream reaches this point
-        TIO_CUDA(cudaEventRecord(alloc_ev, comp));
-        TIO_CUDA(cudaStreamWaitEvent(s, alloc_ev, 0));
+        GPU(cudaEventRecord(alloc_ev, comp));
+        GPU(cudaStreamWaitEvent(s, alloc_ev, 0));
         dptr[t] = p;
-        TIO_CUDA(cudaEventRecord(xt0[xi], s));
-        TIO_CUDA(cudaMemcpyAsync(p, host + hoff[t], (size_t)nb, cudaMemcpyHostToDevice, s));
-        TIO_CUDA(cudaEventRecord(xt1[xi], s));
-        if (cfg.verify) {
+        GPU(cudaEventRecord(xt0[slot], s));
+        GPU(cudaMemcpyAsync(p, host + hoff[t], (size_t)nb, cudaMemcpyHostToDevice, s));
+        GPU(cudaEventRecord(xt1[slot], s));
+        if (cfg.verify && !dry) {
             TIO_TRY(launch_checksum(p, nb, dcs + T + t, s));
             k_checksum_compare<<<1, 1, 0, s>>>(dcs + t, dcs + T + t, dcs + 2 * T);
             count_launch();
         }
+        GPU(cudaEventRecord(xdone[slot], s));
+        last_x[t] = slot;
         return TIO_OK;
     }
     int transfer(int64_t xi) {
@@ -227,20 +248,43 @@ struct tio_engine {
         const int64_t t = x.tensor;
         const int dv = x.device == LOC_SSD ? 0 : 1;
         if (x.tail && step > 0) {
-            // already running: the previous step's late transfer of this tensor
+            // already running: the previous step's late transfer of this
+            // tensor (unless step_end had to reconcile the tensor instead)
             const int64_t y = straddler[xi];
-            last_x[t] = y;
-            if (x.action == 0) offs_done[dv].push_back({x.end, y});
+            if (!reconciled[t] && y >= 0) last_x[t] = y;
+            if (x.action == 0) offs_done[dv].push_back({x.end, last_x[t]});
             return TIO_OK;
         }
-        if (x.action == 0) TIO_TRY(offload(xi, !x.tail));
-        else TIO_TRY(prefetch(xi));
-        TIO_CUDA(cudaEventRecord(xdone[xi], ch[channel_of(x)]));
-        last_x[t] = xi;
+        if (x.action == 0) TIO_TRY(offload(t, channel_of(x), xi, x.tail ? -1 : x.issue_kernel));
+        else TIO_TRY(prefetch(t, channel_of(x), xi, x.start));
         if (x.action == 0) offs_done[dv].push_back({x.end, xi});
         bytes_dir[x.action] += size[t];
         count_dir[x.action] += 1;
         issued_this_step[xi] = 1;
+        return TIO_OK;
+    }
+    // after the step's program: every movable global must be where the next
+    // step's program expects it (the one-iteration model does not carry state
+    // across iterations: e.g. a Belady emergency eviction of a global whose
+    // next use is in the next iteration, simulator.py:414-469)
+    int reconcile() {
+        std::fill(reconciled.begin(), reconciled.end(), 0);
+        for (int64_t t = 0; t < T; ++t) {
+            if (!movable[t] || kind[t] != TIO_KIND_GLOBAL) continue;
+            const bool res = dptr[t] != nullptr;
+            if (res == (bool)end_resident[t]) continue;
+            const int64_t slot = X + t;
+            if (end_resident[t]) {
+                xact_rec[t] = 1;
+                TIO_TRY(prefetch(t, 1, slot, -1));
+            } else {
+                xact_rec[t] = 0;
+                TIO_TRY(offload(t, 0, slot, -1));
+            }
+            reconciled[t] = 1;
+            n_reconcile += 1;
+            bytes_reconcile += size[t];
+        }
         return TIO_OK;
     }
     // process program ops up to (excluding) position `until`
@@ -255,14 +299,15 @@ struct tio_engine {
 
 static inline int64_t align4k(int64_t x) { return (x + 4095) & ~(int64_t)4095; }
 
-extern "C" int tio_engine_create(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries,
-                                 const tio_engine_config *cfg, void *compute_stream, tio_alloc_cb alloc_cb,
-                                 tio_free_cb free_cb, void *user, tio_engine **out) {
-    if (!d || !cfg || !out || !alloc_cb || !free_cb || (num_entries > 0 && !entries))
+static int engine_create(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries,
+                         const tio_engine_config *cfg, void *compute_stream, tio_alloc_cb alloc_cb,
+                         tio_free_cb free_cb, void *user, bool dry, tio_engine **out) {
+    if (!d || !cfg || !out || (!dry && (!alloc_cb || !free_cb)) || (num_entries > 0 && !entries))
         return fail(TIO_ERR_INVALID, "null argument");
     *out = nullptr;
     tio_engine *E = new tio_engine();
     std::unique_ptr<tio_engine> guard(E);
+    E->dry = dry;
     const int64_t N = d->num_kernels, T = d->num_tensors;
     E->N = N; E->T = T;
     E->dur.assign(d->duration_us, d->duration_us + N);
@@ -315,9 +360,8 @@ extern "C" int tio_engine_create(const tio_trace_desc *d, const tio_entry *entri
             if (y.tail || y.tensor != x.tensor || y.action != x.action || y.emergency) continue;
             if (best < 0 || y.seq > sc.transfers[best].seq) best = j;
         }
-        if (best < 0)
-            return fail(TIO_ERR_INTERNAL, "boundary transfer of tensor %lld has no issuing transfer in the step",
-                        (long long)E->tid[x.tensor]);
+        // none: the step never issues it (skipped / cancelled in the model);
+        // step_end's reconciliation then performs the boundary move
         E->straddler[i] = best;
     }
     // kernel -> tensors; per-tensor first / last access
@@ -342,29 +386,88 @@ extern "C" int tio_engine_create(const tio_trace_desc *d, const tio_entry *entri
         if (sc.initial_loc[t] == LOC_SSD || sc.initial_loc[t] == LOC_HOST) E->movable[t] = 1;
     for (int64_t t = 0; t < T; ++t)
         if (E->movable[t]) { E->hoff[t] = E->host_bytes; E->host_bytes += align4k(E->size[t]); }
+    E->dptr.assign(T, nullptr);
+    E->last_x.assign(T, -1);
+    E->last_k.assign(T, -1);
+    E->issued_this_step.assign(X, 0);
+    E->xact_rec.assign(T, 0);
+    E->reconciled.assign(T, 0);
+    // residency of each global when a step begins, as the program leaves it:
+    // a boundary transfer's direction decides, else the folded t = 0 location
+    E->end_resident.assign(T, 0);
+    for (int64_t t = 0; t < T; ++t) E->end_resident[t] = sc.initial_loc[t] == LOC_GPU;
+    for (int64_t i = 0; i < X; ++i)
+        if (sc.transfers[i].tail) E->end_resident[sc.transfers[i].tensor] = sc.transfers[i].action == 1;
+    E->alloc_cb = alloc_cb; E->free_cb = free_cb; E->user = user;
+    if (dry) {
+        *out = guard.release();
+        return TIO_OK;
+    }
     // resources
     E->comp = (cudaStream_t)compute_stream;
     for (int c = 0; c < 4; ++c) TIO_CUDA(cudaStreamCreateWithFlags(&E->ch[c], cudaStreamNonBlocking));
     if (E->host_bytes) TIO_CUDA(cudaHostAlloc((void **)&E->host, (size_t)E->host_bytes, cudaHostAllocPortable));
     TIO_CUDA(cudaMalloc((void **)&E->dcs, sizeof(unsigned long long) * (2 * T + 2)));
     TIO_CUDA(cudaMemset(E->dcs, 0, sizeof(unsigned long long) * (2 * T + 2)));
-    E->kdone.resize(N); E->xdone.resize(X); E->xt0.resize(X); E->xt1.resize(X);
+    E->kdone.resize(N); E->xdone.resize(X + T); E->xt0.resize(X + T); E->xt1.resize(X + T);
     for (int64_t k = 0; k < N; ++k) TIO_TRY(E->mk_event(&E->kdone[k], false));
-    for (int64_t i = 0; i < X; ++i) {
+    for (int64_t i = 0; i < X + T; ++i) {
+        if (i >= X && !(E->movable[i - X] && E->kind[i - X] == TIO_KIND_GLOBAL)) continue;
         TIO_TRY(E->mk_event(&E->xdone[i], false));
         TIO_TRY(E->mk_event(&E->xt0[i], true));
         TIO_TRY(E->mk_event(&E->xt1[i], true));
     }
     TIO_CUDA(cudaEventCreateWithFlags(&E->alloc_ev, cudaEventDisableTiming));
-    E->dptr.assign(T, nullptr);
-    E->last_x.assign(T, -1);
-    E->last_k.assign(T, -1);
-    E->issued_this_step.assign(X, 0);
-    E->alloc_cb = alloc_cb; E->free_cb = free_cb; E->user = user;
     *out = guard.release();
     return TIO_OK;
 }
 
+extern "C" int tio_engine_create(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries,
+                                 const tio_engine_config *cfg, void *compute_stream, tio_alloc_cb alloc_cb,
+                                 tio_free_cb free_cb, void *user, tio_engine **out) {
+    return engine_create(d, entries, num_entries, cfg, compute_stream, alloc_cb, free_cb, user, false, out);
+}
+
+// dry engine callbacks: a fake, non-null address per tensor; frees are no-ops
+static int dry_alloc(void *, int64_t t, int64_t, void **p) {
+    *p = reinterpret_cast<void *>((uintptr_t)(0x10000 + 16 * t));
+    return 0;
+}
+static int dry_free(void *, int64_t, void *) { return 0; }
+
+extern "C" int tio_engine_check_program(const tio_trace_desc *d, const tio_entry *entries, int64_t num_entries,
+                                        const tio_engine_config *cfg, int64_t steps, tio_engine_info_t *info) {
+    tio_engine *E = nullptr;
+    TIO_TRY(engine_create(d, entries, num_entries, cfg, nullptr, dry_alloc, dry_free, nullptr, true, &E));
+    std::unique_ptr<tio_engine> guard(E);
+    if (info) TIO_TRY(tio_engine_info(E, info, nullptr));
+    // globals exist before the step (bound); intermediates when created
+    for (int64_t t = 0; t < E->T; ++t)
+        if (E->kind[t] == TIO_KIND_GLOBAL && E->movable[t]) dry_alloc(nullptr, t, 0, &E->dptr[t]);
+    std::vector<int64_t> npos;
+    std::vector<void *> nptr;
+    for (int64_t st = 0; st < steps; ++st) {
+        TIO_TRY(tio_engine_step_begin(E));
+        for (int64_t k = 0; k < E->N; ++k) {
+            TIO_TRY(tio_engine_before_kernel(E, k));
+            npos.clear(); nptr.clear();
+            for (int64_t j = E->act_ptr[k]; j < E->act_ptr[k + 1]; ++j) {
+                const int64_t t = E->act[j];
+                if (E->kind[t] != TIO_KIND_GLOBAL && E->first_k[t] == k && E->movable[t]) {
+                    npos.push_back(t);
+                    void *p;
+                    dry_alloc(nullptr, t, 0, &p);
+                    nptr.push_back(p);
+                }
+            }
+            TIO_TRY(tio_engine_after_kernel(E, k, (int64_t)npos.size(), npos.data(), nptr.data()));
+        }
+        TIO_TRY(tio_engine_step_end(E, nullptr));
+    }
+    return TIO_OK;
+}
+
+extern "C" int tio_engine_info(const tio_engine *E, tio_engine_info_t *info, uint8_t *movable);
 extern "C" int tio_engine_info(const tio_engine *E, tio_engine_info_t *info, uint8_t *movable) {
     if (!E || !info) return fail(TIO_ERR_INVALID, "null argument");
     memset(info, 0, sizeof(*info));
@@ -404,10 +507,10 @@ extern "C" int tio_engine_step_begin(tio_engine *E) {
             if (!E->dptr[t])
                 return fail(TIO_ERR_INVALID, "tensor %lld starts the step off the GPU but was never bound",
                             (long long)E->tid[t]);
-            if (E->cfg.verify) TIO_TRY(launch_checksum(E->dptr[t], E->size[t], E->dcs + t, E->comp));
-            TIO_CUDA(cudaMemcpyAsync(E->host + E->hoff[t], E->dptr[t], (size_t)E->size[t], cudaMemcpyDeviceToHost,
+            if (E->cfg.verify && !E->dry) TIO_TRY(launch_checksum(E->dptr[t], E->size[t], E->dcs + t, E->comp));
+            EGPU(cudaMemcpyAsync(E->host + E->hoff[t], E->dptr[t], (size_t)E->size[t], cudaMemcpyDeviceToHost,
                                      E->comp));
-            TIO_CUDA(cudaStreamSynchronize(E->comp));
+            EGPU(cudaStreamSynchronize(E->comp));
             if (E->free_cb(E->user, t, (void *)E->comp) != 0)
                 return fail(TIO_ERR_INVALID, "free callback failed for tensor %lld", (long long)E->tid[t]);
             E->dptr[t] = nullptr;
@@ -432,7 +535,7 @@ extern "C" int tio_engine_before_kernel(tio_engine *E, int64_t k) {
     bool creates = false;
     for (int64_t j = E->act_ptr[k]; j < E->act_ptr[k + 1]; ++j) {
         const int64_t t = E->act[j], xi = E->last_x[t];
-        if (xi >= 0 && E->sc.transfers[xi].action == 1) TIO_CUDA(cudaStreamWaitEvent(E->comp, E->xdone[xi], 0));
+        if (xi >= 0 && E->slot_action(xi) == 1) EGPU(cudaStreamWaitEvent(E->comp, E->xdone[xi], 0));
         if (E->first_k[t] == k && E->kind[t] != TIO_KIND_GLOBAL) creates = true;
         else if (E->movable[t] && !E->dptr[t])
             return fail(TIO_ERR_INTERNAL, "kernel %lld needs tensor %lld that is off the GPU", (long long)k,
@@ -441,7 +544,7 @@ extern "C" int tio_engine_before_kernel(tio_engine *E, int64_t k) {
     if (creates)
         for (int dv = 0; dv < 2; ++dv) {
             const int64_t lo = E->latest_off_before(dv, E->sc.start[k]);
-            if (lo >= 0) TIO_CUDA(cudaStreamWaitEvent(E->comp, E->xdone[lo], 0));
+            if (lo >= 0) EGPU(cudaStreamWaitEvent(E->comp, E->xdone[lo], 0));
         }
     E->cursor = E->kop[k] + 1;
     return TIO_OK;
@@ -451,7 +554,7 @@ extern "C" int tio_engine_after_kernel(tio_engine *E, int64_t k, int64_t n_new, 
                                        void *const *new_ptr) {
     if (!E || !E->in_step) return fail(TIO_ERR_INVALID, "no step in progress");
     if (k != E->next_kernel) return fail(TIO_ERR_INVALID, "after_kernel(%lld) without before_kernel", (long long)k);
-    TIO_CUDA(cudaEventRecord(E->kdone[k], E->comp));
+    EGPU(cudaEventRecord(E->kdone[k], E->comp));
     for (int64_t j = E->act_ptr[k]; j < E->act_ptr[k + 1]; ++j) E->last_k[E->act[j]] = k;
     TIO_TRY(tio_engine_bind(E, n_new, new_pos, new_ptr));
     // an intermediate's storage is the framework's to free after its last use
@@ -469,12 +572,13 @@ extern "C" int tio_engine_step_end(tio_engine *E, void *done_stream) {
         return fail(TIO_ERR_INVALID, "step ended after %lld of %lld kernels: the step diverges from the profiled "
                     "trace", (long long)E->next_kernel, (long long)E->N);
     TIO_TRY(E->advance((int64_t)E->ops.size()));
+    TIO_TRY(E->reconcile());
     if (done_stream) {
         // make `done_stream` wait for every transfer of the step (end-of-step
         // fence for timing; the steady state does not need it)
         for (int c = 0; c < 4; ++c) {
-            TIO_CUDA(cudaEventRecord(E->alloc_ev, E->ch[c]));
-            TIO_CUDA(cudaStreamWaitEvent((cudaStream_t)done_stream, E->alloc_ev, 0));
+            EGPU(cudaEventRecord(E->alloc_ev, E->ch[c]));
+            EGPU(cudaStreamWaitEvent((cudaStream_t)done_stream, E->alloc_ev, 0));
         }
     }
     E->in_step = false;
@@ -482,11 +586,24 @@ extern "C" int tio_engine_step_end(tio_engine *E, void *done_stream) {
     return TIO_OK;
 }
 
+extern "C" int tio_engine_step_abort(tio_engine *E) {
+    if (!E) return fail(TIO_ERR_INVALID, "null engine");
+    if (!E->dry) {
+        for (int c = 0; c < 4; ++c) TIO_CUDA(cudaStreamSynchronize(E->ch[c]));
+        TIO_CUDA(cudaStreamSynchronize(E->comp));
+    }
+    E->in_step = false;
+    // tensors the aborted step created are gone; globals keep their state
+    for (int64_t t = 0; t < E->T; ++t)
+        if (E->kind[t] != TIO_KIND_GLOBAL) E->dptr[t] = nullptr;
+    return TIO_OK;
+}
+
 extern "C" int tio_engine_stats_get(tio_engine *E, tio_engine_online_stats *st) {
     if (!E || !st) return fail(TIO_ERR_INVALID, "null argument");
     memset(st, 0, sizeof(*st));
-    for (int c = 0; c < 4; ++c) TIO_CUDA(cudaStreamSynchronize(E->ch[c]));
-    TIO_CUDA(cudaStreamSynchronize(E->comp));
+    for (int c = 0; c < 4; ++c) EGPU(cudaStreamSynchronize(E->ch[c]));
+    EGPU(cudaStreamSynchronize(E->comp));
     st->steps = E->step;
     st->offload_bytes = E->bytes_dir[0]; st->prefetch_bytes = E->bytes_dir[1];
     st->n_offloads = E->count_dir[0]; st->n_prefetches = E->count_dir[1];
@@ -500,9 +617,32 @@ extern "C" int tio_engine_stats_get(tio_engine *E, tio_engine_online_stats *st) 
         else { st->last_prefetch_busy_ms += m; st->last_prefetch_bytes += E->size[x.tensor]; }
     }
     unsigned long long bad = 0;
-    TIO_CUDA(cudaMemcpy(&bad, E->dcs + 2 * E->T, sizeof(bad), cudaMemcpyDeviceToHost));
+    EGPU(cudaMemcpy(&bad, E->dcs + 2 * E->T, sizeof(bad), cudaMemcpyDeviceToHost));
     st->verify_mismatches = (int64_t)bad;
     st->verify = E->cfg.verify;
+    st->reconcile_transfers = E->n_reconcile;
+    st->reconcile_bytes = E->bytes_reconcile;
+    return TIO_OK;
+}
+
+extern "C" int tio_engine_restore(tio_engine *E) {
+    if (!E) return fail(TIO_ERR_INVALID, "null engine");
+    if (E->in_step) return fail(TIO_ERR_INVALID, "restore inside a step");
+    for (int c = 0; c < 4; ++c) EGPU(cudaStreamSynchronize(E->ch[c]));
+    EGPU(cudaStreamSynchronize(E->comp));
+    // every global whose latest copy is its host extent comes back
+    for (int64_t t = 0; t < E->T; ++t) {
+        if (!E->movable[t] || E->kind[t] != TIO_KIND_GLOBAL || E->dptr[t]) continue;
+        void *p = nullptr;
+        if (E->alloc_cb(E->user, t, E->size[t], &p) != 0 || !p)
+            return fail(TIO_ERR_NOMEM, "alloc callback failed for tensor %lld", (long long)E->tid[t]);
+        EGPU(cudaStreamSynchronize(E->comp));
+        EGPU(cudaMemcpy(p, E->host + E->hoff[t], (size_t)E->size[t], cudaMemcpyHostToDevice));
+        E->dptr[t] = p;
+    }
+    std::fill(E->last_x.begin(), E->last_x.end(), -1);
+    std::fill(E->last_k.begin(), E->last_k.end(), -1);
+    E->step = 0;              // the next step sets the steady state up again
     return TIO_OK;
 }
 

@@ -93,6 +93,26 @@ def replay(trace: Trace, plan, capacity: int, rates: ChannelRates, time_scale: f
     return ReplayReport(**{f: getattr(st, f) for f, _ in EngineStatsC._fields_})
 
 
+def check_program(trace: Trace, plan, capacity: int, rates: ChannelRates, steps: int = 3) -> dict:
+    """Walk the online engine's program for `steps` consecutive steps on the
+    host (tio_engine_check_program: no device, fake addresses) — every
+    offload finds its tensor resident, every prefetch finds it gone, every
+    kernel finds its tensors on the GPU.  Returns the engine info."""
+    lib = _native.load()
+    cols = _native.HostColumns(trace.arrays())
+    desc = cols.desc()
+    ents = entries_array(_entries_of(plan))
+    cfg = EngineConfigC(capacity, _rates_struct(rates), 1.0, 0, 0)
+    info = EngineInfoC()
+    rc = lib.tio_engine_check_program(ctypes.byref(desc), _native._ptr(ents), ctypes.c_int64(ents.shape[0]),
+                                      ctypes.byref(cfg), ctypes.c_int64(steps), ctypes.byref(info))
+    if rc == _native.TIO_ERR_SIMULATION:
+        from .simulator import SimulationError
+        raise SimulationError(_native.last_error())
+    _native.check(rc)
+    return {f: getattr(info, f) for f, _ in EngineInfoC._fields_}
+
+
 def checksums(tensors) -> list[int]:
     """libtio's verification checksum of each CUDA tensor's storage bytes
     (one device pass each, on the current stream)."""
@@ -208,7 +228,8 @@ class OnlineStatsC(ctypes.Structure):
                                              "n_prefetches")] + [
         ("last_offload_busy_ms", ctypes.c_double), ("last_prefetch_busy_ms", ctypes.c_double),
         ("last_offload_bytes", ctypes.c_int64), ("last_prefetch_bytes", ctypes.c_int64),
-        ("verify", ctypes.c_int64), ("verify_mismatches", ctypes.c_int64)]
+        ("verify", ctypes.c_int64), ("verify_mismatches", ctypes.c_int64),
+        ("reconcile_transfers", ctypes.c_int64), ("reconcile_bytes", ctypes.c_int64)]
 
 
 class StepDivergence(RuntimeError):
@@ -288,6 +309,7 @@ class OffloadMode:
     # -- host side of the engine's memory callbacks ---------------------------
     def _on_free(self, user, pos, stream):
         try:
+            stream = stream or 0                 # ctypes passes NULL (the legacy stream) as None
             t = self.refs[pos]
             s = self._streams.get(stream)
             if s is None:
@@ -357,8 +379,18 @@ class OffloadMode:
         _native.check(self.lib.tio_engine_stats_get(self.h, ctypes.byref(st)))
         return {f: getattr(st, f) for f, _ in OnlineStatsC._fields_}
 
-    def close(self):
+    def restore(self) -> None:
+        """Bring every global tensor whose latest copy is off the GPU back
+        (between steps; e.g. before a checkpoint or leaving the engine)."""
+        self._cb_error = None
+        self._call(self.lib.tio_engine_restore(self.h))
+
+    def close(self, restore: bool = True):
+        """Destroy the engine; by default first restore every global tensor to
+        the device so the model is whole again."""
         if self.h:
+            if restore:
+                self.restore()
             self.lib.tio_engine_destroy(self.h)
             self.h = ctypes.c_void_p()
         self.refs.clear()
@@ -397,6 +429,9 @@ class _EngineStep:
         self.mode.__exit__(et, ev, tb)
         e = self.eng
         if et is not None:
+            e.lib.tio_engine_step_abort(e.h)
+            for p in [p for p in e.refs if not e.is_global[p]]:
+                del e.refs[p]
             return False
         e._call(e.lib.tio_engine_step_end(e.h, ctypes.c_void_p(
             self.done_stream.cuda_stream if self.done_stream is not None else 0)))

@@ -62,3 +62,45 @@ def test_engine_program_consistent_on_corpus():
             _check(tr, xs, starts, kseq, loc)
             n += 1
     assert n >= 1500
+
+
+def test_online_engine_program_holds_over_consecutive_steps():
+    """The online engine (csrc/engine_online.cu) walked for 3 consecutive
+    steps without a device (tio_engine_check_program): steady-state folding,
+    boundary-straddling transfers handed from one step to the next, emergency
+    evictions — every offload finds its tensor resident, every prefetch finds
+    it gone, every kernel finds its tensors on the GPU."""
+    from paper_2506_06472_b200.engine import check_program
+    sims = load_golden("sim")
+    plans = {r["trace_sha256"]: r for r in load_golden("crit2") + load_golden("extreme")}
+    n = 0
+    for rec in sims:
+        base = plans[rec["trace_sha256"]]
+        tr = regen(rec)
+        for entries in ((parse_plan(base["plan"])[1] if "plan" in base else None), []):
+            if entries is None:
+                continue
+            key = "plan" if entries else "on_demand"
+            if "error" in rec[key]:
+                continue
+            check_program(tr, entries, base["capacity"], rates_of(base), steps=3)
+            n += 1
+    assert n >= 1500
+
+
+def test_online_engine_program_on_llama_traces_with_oracle_plans():
+    """Appendix-C Llama-3-8B traces (1 and 4 microbatches) planned by the
+    oracle at tight capacities: the plans have wrap periods of globals, folded
+    prefetches and straddling transfers; 3 steps of the online program."""
+    from oracle import oracle as O
+    from paper_2506_06472_b200 import ChannelRates, PlanEntry
+    from paper_2506_06472_b200 import tracegen as G
+    from paper_2506_06472_b200.engine import check_program
+    for mb, frac, rate in ((1, 0.5, 16_000.0), (1, 0.7, 50_000.0), (4, 0.5, 50_000.0), (4, 0.8, 50_000.0)):
+        tr = G.gen_llama_trace(G.LlamaTraceConfig(microbatches=mb))
+        a = tr.arrays()
+        cap = int(G.llama_peak_bytes(tr) * frac)
+        p = O.plan(a, cap, rate, rate)
+        entries = [PlanEntry(tid, act, trig, dl, tgt, urg) for tid, act, trig, dl, tgt, urg in p["entries"]]
+        info = check_program(tr, entries, cap, ChannelRates.symmetric(rate), steps=3)
+        assert info["num_transfers"] > 0
