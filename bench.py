@@ -573,7 +573,11 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
 
+    def log(msg):
+        print(f"[c4] {msg}  (allocated {torch.cuda.memory_allocated() / 1e9:.1f} GB)", file=sys.stderr, flush=True)
+
     # ---- ideal: plain PyTorch, capacity unconstrained
+    log("ideal run")
     s = Step(cfg, seed=0)
     for _ in range(3):
         s()
@@ -583,6 +587,7 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
     s = None
 
     # ---- profile (step 2 of a fresh model) -> trace
+    log(f"ideal {ideal_ms:.1f} ms/step, peak {ideal_peak / 1e9:.1f} GB; profiling")
     s = Step(cfg, seed=0)
     s()
     t0 = time.perf_counter()
@@ -597,8 +602,10 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
            "ideal": {"step_ms": ideal_ms, "allocator_peak_bytes": ideal_peak, "losses": ideal_losses},
            "profile_s": t_prof, "runs": []}
     first = True
+    log(f"trace: {a.num_kernels} kernels, {a.num_tensors} tensors, peak {peak / 1e9:.1f} GB ({t_prof:.1f} s)")
     for frac in fracs:
         cap = int(peak * frac)
+        log(f"capacity {frac} x peak")
         t0 = time.perf_counter()
         plan = plan_migrations(tr, cap, rates)
         t_plan = time.perf_counter() - t0
@@ -683,6 +690,10 @@ def main(argv=None):
             args.ref_rounds_total = _known_rounds(args.config)
         run_reference(args, rank, world)
         return
+    # the C4 leg's real training step: expandable segments keep the caching
+    # allocator's fragmentation out of the offloaded step's peak (must be set
+    # before the first CUDA allocation of the process)
+    os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
     if world > 1:
         import torch
         import torch.distributed as dist

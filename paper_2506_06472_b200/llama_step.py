@@ -50,6 +50,52 @@ LLAMA3_8B_MODEL = LlamaConfig()
 TINY = LlamaConfig(vocab=4096, dim=512, layers=2, heads=8, kv_heads=2, ffn=1536, seq=512)
 
 
+def _acc(t):
+    """accumulation dtype: fp32 for bf16/fp16/fp32 tensors (fp64 stays fp64)"""
+    return torch.promote_types(t.dtype, torch.float32)
+
+
+class _RMSNormFn(torch.autograd.Function):
+    """RMSNorm in fp32 that keeps only (x, weight, rstd) for backward — the
+    memory profile of a fused norm kernel."""
+
+    @staticmethod
+    def forward(ctx, x, w, eps):
+        xf = x.to(_acc(x))
+        rstd = torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)
+        ctx.save_for_backward(x, w, rstd)
+        return (xf * rstd).to(x.dtype) * w
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w, rstd = ctx.saved_tensors
+        xhat = x.to(_acc(x)) * rstd
+        g = gy.to(_acc(gy))
+        gw = (g * xhat).sum(dim=tuple(range(g.dim() - 1))).to(w.dtype)
+        gxh = g * w.to(_acc(w))
+        gx = rstd * (gxh - xhat * (gxh * xhat).mean(-1, keepdim=True))
+        return gx.to(x.dtype), gw, None
+
+
+class _SwiGLUFn(torch.autograd.Function):
+    """silu(g) * u keeping only (g, u) for backward."""
+
+    @staticmethod
+    def forward(ctx, g, u):
+        ctx.save_for_backward(g, u)
+        return F.silu(g) * u
+
+    @staticmethod
+    def backward(ctx, gm):
+        g, u = ctx.saved_tensors
+        gf = g.to(_acc(g))
+        sg = torch.sigmoid(gf)
+        gmf = gm.to(_acc(gm))
+        du = (gmf * gf * sg).to(u.dtype)
+        dg = (gmf * u.to(_acc(u)) * sg * (1 + gf * (1 - sg))).to(g.dtype)
+        return dg, du
+
+
 class RMSNorm(nn.Module):
     def __init__(self, dim: int, eps: float):
         super().__init__()
@@ -57,9 +103,7 @@ class RMSNorm(nn.Module):
         self.eps = eps
 
     def forward(self, x):
-        xf = x.float()
-        y = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + self.eps)
-        return y.to(x.dtype) * self.weight
+        return _RMSNormFn.apply(x, self.weight, self.eps)
 
 
 def _rope(x, cos, sin):
@@ -94,7 +138,7 @@ class Block(nn.Module):
         o = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
         x = x + self.wo(o.transpose(1, 2).reshape(B, S, c.dim))
         h2 = self.ffn_norm(x)
-        return x + self.w2(F.silu(self.w1(h2)) * self.w3(h2))
+        return x + self.w2(_SwiGLUFn.apply(self.w1(h2), self.w3(h2)))
 
 
 class Llama(nn.Module):
