@@ -394,6 +394,7 @@ class OffloadMode:
             self.lib.tio_engine_destroy(self.h)
             self.h = ctypes.c_void_p()
         self.refs.clear()
+        self.globals_ = {}                     # the model's tensors are no longer the engine's
 
     def __del__(self):
         try:
