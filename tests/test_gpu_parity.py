@@ -380,19 +380,21 @@ def test_lifetime_vs_reference_itself_at_scale(config):
 
 def test_c2_host_tier_plan_prefix_vs_oracle():
     """Config C2 with the host tier of SURVEY §8(d) (host 50,000 B/us both
-    ways, host_cap 256e9): the first 400 commits of the device plan against
-    the oracle's first 400 — a prefix of the same greedy sequence, with
-    SSD-infeasible candidates falling back to the host and the host-cap
-    occupancy test live (the oracle's full plan takes hours here)."""
+    ways, host_cap 256e9): the first 700 commits of the device plan against
+    the oracle's first 700 — a prefix of the same greedy sequence; from commit
+    576 on the SSD channels are saturated and candidates fall back to the host
+    with the host-cap occupancy test live (124 host commits here; the oracle's
+    host-tier rounds cost ~0.4 s each, so its full 32k-round plan is out of
+    reach)."""
     from paper_2506_06472_b200 import LLAMA3_8B, gen_llama_trace
     from paper_2506_06472_b200.tracegen import llama_peak_bytes
     tr = gen_llama_trace(LLAMA3_8B)
     a = tr.arrays()
     cap = llama_peak_bytes(tr) // 2
-    R = 400
+    R = 700
     o = O.plan(a, cap, 16000.0, 16000.0, 50000.0, 50000.0, 256 * 10**9, max_rounds=R)
     g = plan_device(tr, cap, ChannelRates.symmetric(16_000, host=50_000), 256 * 10**9, max_rounds=R)
     assert int(g["info"].num_commits) == len(o["committed"]) == R
-    assert sum(1 for c in o["committed"] if c[4] == "CPU") > 0          # the host tier is exercised
+    assert sum(1 for c in o["committed"] if c[4] == "CPU") >= 100       # the host tier is exercised
     assert g["plan_bytes"] == o["plan_bytes"]
     assert np.array_equal(g["residual"], o["residual"])
