@@ -181,7 +181,35 @@ typedef struct tio_plan_opts {
     int64_t max_rounds;
     int32_t warp_refit_max;
     int32_t pad;
+    /* Sharded planning: nranks > 1 makes this call rank `rank`
+     * of nranks.  Every rank holds the whole replicated planner state (channels,
+     * residual, critical prefix) but evaluates only the candidate tiles
+     * t % nranks == rank; each round the ranks exchange their local best
+     * (key + winner window) through the mailboxes and apply the same commit,
+     * so every rank ends with the full plan.  mailbox: this rank's
+     * tio_mailbox_bytes() of device memory (zeroed once); peer_mailboxes:
+     * [nranks] device pointers of every rank's mailbox as mapped in this
+     * process (CUDA IPC / peer access; [rank] = mailbox); epoch: strictly
+     * increasing per planning call over the mailbox's lifetime (flags are
+     * compared against epoch + round + 1, so no reset is needed).
+     * blocks > 0 overrides the planner's grid (virtual ranks on one GPU). */
+    int32_t nranks;
+    int32_t rank;
+    int32_t blocks;
+    int32_t pad2;
+    uint64_t epoch;
+    void *mailbox;
+    void *const *peer_mailboxes;
 } tio_plan_opts;
+/* device bytes of one rank's mailbox */
+size_t tio_mailbox_bytes(void);
+/* Sharded planning of one trace by `nranks` virtual ranks on THIS GPU (the
+ * check of the multi-GPU protocol on one device): rank r runs as a separate
+ * planner instance (own replicated state, own stream, its own cooperative
+ * grid of SMs / nranks blocks), all concurrently, exchanging through
+ * mailboxes in device memory.  out[r] / info[r]: each rank's plan. */
+int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap,
+                            const tio_plan_opts *opts, int32_t nranks, tio_plan **out, tio_plan_info *info);
 int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap,
                      const tio_plan_opts *opts, void *stream, tio_plan **out, tio_plan_info *info);
 int tio_plan_info_get(tio_plan *p, tio_plan_info *out);

@@ -76,7 +76,10 @@ class PlanInfo(ctypes.Structure):
 
 
 class PlanOpts(ctypes.Structure):
-    _fields_ = [("max_rounds", _i64), ("warp_refit_max", ctypes.c_int32), ("pad", ctypes.c_int32)]
+    _fields_ = [("max_rounds", _i64), ("warp_refit_max", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("blocks", ctypes.c_int32),
+                ("pad2", ctypes.c_int32), ("epoch", ctypes.c_uint64), ("mailbox", ctypes.c_void_p),
+                ("peer_mailboxes", ctypes.POINTER(ctypes.c_void_p))]
 
 
 class SimReportC(ctypes.Structure):
@@ -112,7 +115,7 @@ EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_devi
            "tio_engine_before_kernel", "tio_engine_after_kernel", "tio_engine_step_end", "tio_engine_stats_get",
            "tio_engine_destroy", "tio_checksum",
            "tio_engine_set_verify", "tio_engine_restore",
-           "tio_engine_check_program", "tio_engine_step_abort")
+           "tio_engine_check_program", "tio_engine_step_abort", "tio_plan_create_virtual")
 
 
 def lib_path() -> str:
@@ -136,6 +139,7 @@ def load(build_if_missing: bool = True):
         lib = ctypes.CDLL(path)
         for name in EXPORTS:
             getattr(lib, name).restype = ctypes.c_int
+        lib.tio_mailbox_bytes.restype = ctypes.c_size_t
         if lib.tio_abi_version() != 1:
             raise NativeUnavailable("libtio ABI mismatch")
         _lib = lib
@@ -245,10 +249,16 @@ class DeviceTrace:
         out["iteration"] = v.iteration_us
         return out
 
-    def plan(self, capacity: int, rates: Rates, host_cap: int, max_rounds: int = 0) -> "DevicePlan":
+    def plan(self, capacity: int, rates: Rates, host_cap: int, max_rounds: int = 0, shard=None) -> "DevicePlan":
         info = PlanInfo()
         h = ctypes.c_void_p()
         opts = PlanOpts(max_rounds, -1, 0)
+        if shard is not None:
+            # sharded planning: (rank, nranks, own mailbox ptr, [peer mailbox ptrs], epoch)
+            rank, nranks, mb, peers, epoch = shard
+            self._peers = (ctypes.c_void_p * nranks)(*peers)
+            opts.nranks, opts.rank, opts.epoch, opts.mailbox = nranks, rank, epoch, mb
+            opts.peer_mailboxes = ctypes.cast(self._peers, ctypes.POINTER(ctypes.c_void_p))
         rc = self._lib.tio_plan_create2(self.handle, _i64(capacity), ctypes.byref(rates), _i64(host_cap),
                                         ctypes.byref(opts), self.stream, ctypes.byref(h), ctypes.byref(info))
         if rc != TIO_OK:
@@ -256,6 +266,20 @@ class DeviceTrace:
             err.info = info
             raise err
         return DevicePlan(self._lib, h, info, self.stream, self.num_kernels)
+
+    def plan_virtual(self, capacity: int, rates: Rates, host_cap: int, nranks: int,
+                     max_rounds: int = 0) -> list:
+        """The sharded planner with `nranks` virtual ranks on this GPU
+        (tio_plan_create_virtual): one DevicePlan per rank."""
+        infos = (PlanInfo * nranks)()
+        hs = (ctypes.c_void_p * nranks)()
+        opts = PlanOpts(max_rounds, -1, 0)
+        rc = self._lib.tio_plan_create_virtual(self.handle, _i64(capacity), ctypes.byref(rates), _i64(host_cap),
+                                               ctypes.byref(opts), ctypes.c_int32(nranks), hs, infos)
+        if rc != TIO_OK:
+            raise TioError(rc, last_error())
+        return [DevicePlan(self._lib, ctypes.c_void_p(hs[r]), infos[r], None, self.num_kernels)
+                for r in range(nranks)]
 
 
 class DevicePlan:

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -488,6 +489,21 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     a.t_ka_lo = t_ka_lo; a.t_ka_hi = t_ka_hi; a.t_kb_lo = t_kb_lo; a.t_kb_hi = t_kb_hi; a.tile_best = tile_best;
     int G = 0;
     PTRY(plan_loop_grid(&G));
+    if (opts && opts->blocks > 0 && opts->blocks < G) G = opts->blocks;
+    const int nranks = opts && opts->nranks > 1 ? opts->nranks : 1;
+    if (nranks > MAX_RANKS) return bail(fail(TIO_ERR_INVALID, "at most %d ranks", MAX_RANKS));
+    if (nranks > 1) {
+        if (!opts->mailbox || !opts->peer_mailboxes || opts->rank < 0 || opts->rank >= nranks)
+            return bail(fail(TIO_ERR_INVALID, "sharded planning needs rank, mailbox and peer mailboxes"));
+        a.nranks = nranks;
+        a.rank = opts->rank;
+        a.epoch = opts->epoch;
+        a.mb_self = static_cast<Mailbox *>(opts->mailbox);
+        for (int r = 0; r < nranks; ++r) a.mb_peer[r] = static_cast<Mailbox *>(opts->peer_mailboxes[r]);
+    }
+    PTRY(A.alloc(&a.win, 1));
+    PTRY(A.alloc(&a.win_gen, 1));
+    PCUDA(cudaMemsetAsync(a.win_gen, 0, 8, s));
     int64_t *resid, *local_cp, *chunk_sum;
     PTRY(A.alloc(&resid, N)); PTRY(A.alloc(&local_cp, N + 1)); PTRY(A.alloc(&chunk_sum, G));
     if (N) PCUDA(cudaMemcpyAsync(resid, t->timeline, 8 * N, cudaMemcpyDeviceToDevice, s));
@@ -701,6 +717,65 @@ int tio_plan_destroy(tio_plan *p) {
     p->arena.release();
     cudaStreamSynchronize(p->arena.stream);
     delete p;
+    return TIO_OK;
+}
+
+size_t tio_mailbox_bytes(void) { return sizeof(Mailbox); }
+
+int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap,
+                            const tio_plan_opts *opts, int32_t nranks, tio_plan **out, tio_plan_info *info) {
+    if (!t || !rates || !out || !info) return fail(TIO_ERR_INVALID, "null argument");
+    if (nranks < 1 || nranks > MAX_RANKS) return fail(TIO_ERR_INVALID, "nranks must be in [1, %d]", MAX_RANKS);
+    TIO_TRY(lifetime_sync(t, nullptr));        // shared trace products, before the rank threads start
+    int G = 0;
+    TIO_TRY(plan_loop_grid(&G));
+    int dev = 0;
+    TIO_CUDA(cudaGetDevice(&dev));
+    Mailbox *mb = nullptr;
+    TIO_CUDA(cudaMalloc((void **)&mb, sizeof(Mailbox) * nranks));
+    TIO_CUDA(cudaMemset(mb, 0, sizeof(Mailbox) * nranks));
+    std::vector<void *> peers(nranks);
+    for (int r = 0; r < nranks; ++r) peers[r] = mb + r;
+    std::vector<int> rcs(nranks, TIO_OK);
+    std::vector<std::string> errs(nranks);
+    std::vector<std::thread> th;
+    for (int r = 0; r < nranks; ++r) {
+        out[r] = nullptr;
+        th.emplace_back([&, r]() {
+            cudaSetDevice(dev);
+            cudaStream_t s = nullptr;
+            if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+                rcs[r] = fail(TIO_ERR_CUDA, "stream creation failed");
+                errs[r] = "stream creation failed";
+                return;
+            }
+            tio_plan_opts o;
+            memset(&o, 0, sizeof(o));
+            if (opts) o.max_rounds = opts->max_rounds;
+            o.nranks = nranks;
+            o.rank = r;
+            o.blocks = G / nranks;
+            o.epoch = 0;
+            o.mailbox = mb + r;
+            o.peer_mailboxes = peers.data();
+            rcs[r] = tio_plan_create2(t, capacity, rates, host_cap, &o, s, &out[r], &info[r]);
+            if (rcs[r] != TIO_OK) {
+                char b[1024];
+                tio_last_error(b, sizeof(b));
+                errs[r] = b;
+            }
+            cudaStreamSynchronize(s);
+            if (out[r]) out[r]->arena.stream = nullptr;   // later frees on the legacy stream
+            cudaStreamDestroy(s);
+        });
+    }
+    for (auto &x : th) x.join();
+    cudaFree(mb);
+    for (int r = 0; r < nranks; ++r)
+        if (rcs[r] != TIO_OK) {
+            for (int q = 0; q < nranks; ++q) { tio_plan_destroy(out[q]); out[q] = nullptr; }
+            return fail(rcs[r], "virtual rank %d: %s", r, errs[r].c_str());
+        }
     return TIO_OK;
 }
 

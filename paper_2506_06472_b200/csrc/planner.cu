@@ -395,6 +395,116 @@ struct WinInfo {
     uint64_t blo, bhi;
 };
 
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// WinMsg copies through 16-byte volatile accesses (peer / IPC memory, never
+// cached in L1)
+__device__ __forceinline__ void msg_store(WinMsg *dst, const WinMsg &m) {
+    const ulonglong2 *s = reinterpret_cast<const ulonglong2 *>(&m);
+    ulonglong2 *d = reinterpret_cast<ulonglong2 *>(dst);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(WinMsg) / 16); ++i)
+        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(d + i), "l"(s[i].x), "l"(s[i].y) : "memory");
+}
+__device__ __forceinline__ WinMsg msg_load(const WinMsg *src) {
+    WinMsg m;
+    ulonglong2 *d = reinterpret_cast<ulonglong2 *>(&m);
+    const ulonglong2 *s = reinterpret_cast<const ulonglong2 *>(src);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(WinMsg) / 16); ++i) {
+        unsigned long long x, y;
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(s + i) : "memory");
+        d[i] = make_ulonglong2(x, y);
+    }
+    return m;
+}
+
+// The round's winner (replaces a grid barrier + a redundant per-block
+// argmax): every block arrives on the grid's arrival counter after writing
+// its block best; the last arrival's block reduces the G block bests, thread
+// 0 reads the winner's column into a WinMsg, and with R > 1 ranks puts it
+// into slot [round & 1][rank] of every rank's mailbox, raises its flag there
+// (release, system scope), waits for all R flags of its own mailbox, and
+// takes the best of the R messages (kbetter: ratio, then lowest candidate
+// index — the same winner on every rank).  It publishes the winner and bumps
+// win_gen; every block waits for win_gen and reads the winner.
+__device__ void round_winner(const PlanArgs &a, int64_t round, int G, Key *sm_key, WinMsg *out) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long *ctr = reinterpret_cast<unsigned long long *>(a.bar);
+        unsigned long long v;
+        asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], 1;" : "=l"(v) : "l"(ctr) : "memory");
+        s_last = ((v + 1) % (unsigned long long)G) == 0;
+    }
+    __syncthreads();
+    if (s_last) {
+        Key w{0, 0, 1, 0};
+        for (int j = threadIdx.x; j < G; j += blockDim.x) {
+            const Key o = kload(&a.blk_best[j]);
+            if (kbetter(o, w)) w = o;
+        }
+        w = block_best(w, sm_key);
+        if (threadIdx.x == 0) {
+            WinMsg m;
+            memset(&m, 0, sizeof(m));
+            m.k = w;
+            if ((w.blo | w.bhi) != 0) {
+                const int64_t c = (int64_t)(((uint64_t)w.meta >> 2) & 0x7fffffffu);
+                const int q0 = (w.meta & 3) == TIO_DEST_SSD ? 0 : 2;
+                m.size = __ldg(&a.c_size[c]);
+                m.off_s = ld_cg(&a.place[4 * c + q0]);
+                m.off_e = m.off_s + __ldg(&a.c_d[4 * c + q0]);
+                m.pre_s = ld_cg(&a.place[4 * c + q0 + 1]);
+                m.pre_e = m.pre_s + __ldg(&a.c_d[4 * c + q0 + 1]);
+                for (int q = 0; q < 4; ++q) m.r[q] = ld_cg(&a.rng[4 * c + q]);
+            }
+            if (a.nranks > 1) {
+                const int slot = (int)(round & 1);
+                const unsigned long long tag = a.epoch + (unsigned long long)round + 1;
+                for (int p = 0; p < a.nranks; ++p) {
+                    Mailbox *mb = a.mb_peer[p];
+                    msg_store(&mb->msg[slot][a.rank], m);
+                    st_release_sys(&mb->flag[a.rank], tag);
+                }
+                Mailbox *me = a.mb_self;
+                for (int p = 0; p < a.nranks; ++p)
+                    while (ld_acquire_sys(&me->flag[p]) < tag) {
+                    }
+                WinMsg best = msg_load(&me->msg[slot][0]);
+                for (int p = 1; p < a.nranks; ++p) {
+                    const WinMsg o = msg_load(&me->msg[slot][p]);
+                    if (kbetter(o.k, best.k)) best = o;
+                }
+                m = best;
+            }
+            msg_store(a.win, m);
+            st_release_gpu(a.win_gen, (unsigned long long)round + 1);
+        }
+    }
+    if (threadIdx.x == 0) {
+        while (ld_acquire_gpu(a.win_gen) < (unsigned long long)round + 1) {
+        }
+        *out = msg_load(a.win);
+    }
+    __syncthreads();
+}
+
 constexpr int DIRTY_MAX = 2048;  // own tiles tested / listed per pass
 constexpr size_t PLAN_DYN_SMEM = 0;
 
@@ -402,7 +512,7 @@ __global__ void __launch_bounds__(PLAN_THREADS)
 plan_loop_kernel(PlanArgs a) {
     __shared__ int64_t cp_prefix[MAXG + 1];
     __shared__ Key sm_key[33];
-    __shared__ WinInfo s_win;
+    __shared__ WinMsg s_win;
     __shared__ LastCommit last;
     __shared__ int64_t sm_scan[40];
     __shared__ int64_t ch_n[4];
@@ -427,7 +537,12 @@ plan_loop_kernel(PlanArgs a) {
     const int64_t period = I > 0 ? I : 0;
     const int64_t nb = period > 0 ? 3 : 1;
     const int64_t NT = a.ntiles;
-    const int64_t my_tiles = NT > b ? (NT - 1 - b) / G + 1 : 0;   // tiles b, b+G, ...
+    // tile ownership: rank `rank` of R owns tiles t = rank + R u; its block b
+    // owns u = b, b + G, ... (R = 1: tiles b, b + G, ...)
+    const int64_t R = a.nranks > 1 ? a.nranks : 1, rk = a.nranks > 1 ? a.rank : 0;
+    const int64_t NTr = NT > rk ? (NT - rk + R - 1) / R : 0;
+    const int64_t my_tiles = NTr > b ? (NTr - 1 - b) / G + 1 : 0;
+    auto own_tile = [&](int64_t j) -> int64_t { return rk + R * (b + j * G); };
     int64_t *flip = &a.scalars[PS_FLIP];                       // [3 slots][cnt, lo, hi]
     const Key none{0, 0, 1, 0};
 
@@ -737,7 +852,7 @@ plan_loop_kernel(PlanArgs a) {
             if (threadIdx.x == 0) s_ndirty = 0;
             __syncthreads();
             for (int64_t j = j0 + threadIdx.x; j < my_tiles && j < j0 + DIRTY_MAX; j += blockDim.x) {
-                const int64_t t = b + j * G;
+                const int64_t t = own_tile(j);
                 // tiles whose candidates phase R handled last round take them back
                 bool d = round == 0 || t == s_win_tile || (round > 1 && ld_cg(&a.t_refit[t]) == (int32_t)(round - 2));
                 if (!d && last.dest == TIO_DEST_SSD) {
@@ -825,7 +940,7 @@ plan_loop_kernel(PlanArgs a) {
             // keys change the block best
             Key mine = none;
             for (int64_t j = threadIdx.x; j < my_tiles; j += blockDim.x) {
-                const Key o = a.tile_best[b + j * G];
+                const Key o = a.tile_best[own_tile(j)];
                 if (kbetter(o, mine)) mine = o;
             }
             const Key tm = block_best(mine, sm_key);
@@ -849,7 +964,12 @@ plan_loop_kernel(PlanArgs a) {
         PROF(if (threadIdx.x == 0) atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 15]),
                                              (long long)(gtime() - te0)));
         TICK(2);
-        grid_barrier(a.bar);
+        // ---- the round's winner: the last block to arrive reduces the block
+        // bests (one block instead of every block re-reading all of them),
+        // exchanges its rank's best with the other ranks' (sharded planning),
+        // and publishes the winner; the others wait for it.  This replaces
+        // the first grid barrier.
+        round_winner(a, round, G, sm_key, &s_win);
         TICK(3);
         PROF(if (tb) {
             a.scalars[PS_DBG + 10] += ld_cg(&a.scalars[PS_DBG + 15]);
@@ -857,36 +977,17 @@ plan_loop_kernel(PlanArgs a) {
             a.scalars[PS_DBG + 13] += ld_cg(&a.scalars[PS_DBG + 14]);
             a.scalars[PS_DBG + 14] = 0;
         })
-
-        // ---- phase C: global argmax (redundant per block) and commit
+        if (b == 0 && threadIdx.x == 0) a.scalars[PS_ROUNDS] = round + 1;
+        WinInfo w;
         {
-            Key w = none;
-            for (int j = threadIdx.x; j < G; j += blockDim.x) {
-                const Key o = kload(&a.blk_best[j]);
-                if (kbetter(o, w)) w = o;
-            }
-            w = block_best(w, sm_key);
-            if (threadIdx.x == 0) {
-                WinInfo wi;
-                wi.blo = w.blo; wi.bhi = w.bhi; wi.cost = w.cost;
-                wi.idx = (w.blo | w.bhi) != 0 ? (int64_t)(((uint64_t)w.meta >> 2) & 0x7fffffffu) : 0;   // column position
-                wi.dest = w.meta & 3;
-                if ((w.blo | w.bhi) != 0) {
-                    const int64_t c = wi.idx;
-                    const int q0 = wi.dest == TIO_DEST_SSD ? 0 : 2;
-                    wi.size = __ldg(&a.c_size[c]);
-                    wi.off_s = ld_cg(&a.place[4 * c + q0]);
-                    wi.off_e = wi.off_s + __ldg(&a.c_d[4 * c + q0]);
-                    wi.pre_s = ld_cg(&a.place[4 * c + q0 + 1]);
-                    wi.pre_e = wi.pre_s + __ldg(&a.c_d[4 * c + q0 + 1]);
-                    for (int q = 0; q < 4; ++q) wi.r[q] = ld_cg(&a.rng[4 * c + q]);
-                }
-                s_win = wi;
-                if (b == 0) a.scalars[PS_ROUNDS] = round + 1;
-            }
-            __syncthreads();
+            const WinMsg wm = s_win;
+            w.blo = wm.k.blo; w.bhi = wm.k.bhi; w.cost = wm.k.cost;
+            w.idx = (w.blo | w.bhi) != 0 ? (int64_t)(((uint64_t)wm.k.meta >> 2) & 0x7fffffffu) : 0;   // column
+            w.dest = wm.k.meta & 3;
+            w.size = wm.size;
+            w.off_s = wm.off_s; w.off_e = wm.off_e; w.pre_s = wm.pre_s; w.pre_e = wm.pre_e;
+            for (int q = 0; q < 4; ++q) w.r[q] = wm.r[q];
         }
-        const WinInfo w = s_win;
         TICK(4);
         if ((w.blo | w.bhi) == 0) break;  // planner.py:311-312 no viable candidate
         const int q0 = w.dest == TIO_DEST_SSD ? 0 : 2;
@@ -910,7 +1011,7 @@ plan_loop_kernel(PlanArgs a) {
                 if (threadIdx.x == 0) s_ndirty = 0;
                 __syncthreads();
                 for (int64_t j = j0 + threadIdx.x; j < my_tiles && j < j0 + DIRTY_MAX; j += blockDim.x) {
-                    const int64_t t = b + j * G;
+                    const int64_t t = own_tile(j);
                     const longlong2 h01 = __ldcg(reinterpret_cast<const longlong2 *>(a.t_hull + 4 * t));
                     const longlong2 h23 = __ldcg(reinterpret_cast<const longlong2 *>(a.t_hull + 4 * t + 2));
                     if (spans_hit(h01.x, h01.y, ns[0], ne[0], nb) || spans_hit(h23.x, h23.y, ns[1], ne[1], nb))

@@ -32,6 +32,28 @@ struct Key {
     int64_t meta;
 };
 
+// A round's winner as one rank publishes it: the key plus everything the
+// commit needs from the winner's column (a rank only evaluates the
+// candidates of its own tiles, so the others do not have it).
+struct WinMsg {
+    Key k;
+    int64_t size, off_s, off_e, pre_s, pre_e;
+    int32_t r[4];
+    int64_t pad[3];
+};
+static_assert(sizeof(WinMsg) == 112, "WinMsg layout");
+
+// Sharded planner (candidate tiles split over ranks, state replicated):
+// every rank's mailbox in device memory (its own; peers reach it through
+// P2P / IPC mappings, or it is another instance's on the same GPU):
+//   flag[r]          = epoch + round + 1 once rank r's round-`round` message is in
+//   msg[round & 1][r] the message
+constexpr int MAX_RANKS = 8;
+struct Mailbox {
+    unsigned long long flag[MAX_RANKS];
+    WinMsg msg[2][MAX_RANKS];
+};
+
 struct PlanArgs {
     int64_t N, P, iteration, capacity, host_cap;
     int32_t has_host;
@@ -82,6 +104,15 @@ struct PlanArgs {
     int64_t *scalars;              // [PS_COUNT]
     const int64_t *c_tid;          // [P] tensor id per candidate (for commit records)
     const int32_t *c_tpos;         // [P]
+    // the round's winner (the last block to arrive reduces the block bests,
+    // exchanges with the other ranks, publishes it here and bumps win_gen)
+    WinMsg *win;                   // [1]
+    unsigned long long *win_gen;   // [1] zeroed
+    // sharding: rank `rank` of `nranks` owns tiles t with t % nranks == rank
+    int32_t nranks, rank;
+    unsigned long long epoch;      // added to every mailbox flag (one per planning call)
+    Mailbox *mb_self;              // this rank's mailbox
+    Mailbox *mb_peer[MAX_RANKS];   // every rank's mailbox as mapped here (mb_peer[rank] == mb_self)
 };
 
 int plan_loop_grid(int *blocks);

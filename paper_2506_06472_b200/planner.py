@@ -282,6 +282,30 @@ def plan_device(trace: Trace, capacity: int, rates: ChannelRates, host_cap: int 
     return out
 
 
+def plan_device_virtual(trace: Trace, capacity: int, rates: ChannelRates, host_cap: int = 0, nranks: int = 2,
+                        max_rounds: int = 0) -> list[dict]:
+    """The sharded planner run by `nranks` virtual ranks on this
+    GPU (tio_plan_create_virtual): each rank evaluates only its candidate
+    tiles, the ranks exchange their round's best through device mailboxes and
+    apply the same commit.  Returns every rank's raw output (plan_device
+    format); all must equal the single-rank plan."""
+    dt = _device_trace(trace)
+    try:
+        plans = dt.plan_virtual(capacity, _rates_struct(rates), host_cap, nranks, max_rounds)
+    except _native.TioError as err:
+        _raise_for(err, capacity, rates)
+    outs = []
+    for p in plans:
+        try:
+            o = p.copy_out()
+            o["info"] = p.info
+            o["plan_bytes"] = p.write()
+            outs.append(o)
+        finally:
+            p.close()
+    return outs
+
+
 def plan_migrations(trace: Trace, capacity: int, rates: ChannelRates, host_cap: int = 0) -> MigrationPlan:
     """Greedy Algorithm-1 plan computed on the GPU (planner.py:267-370).
 
