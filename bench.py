@@ -27,9 +27,15 @@ key.  Both plans are bit-exact with the oracle fingerprints in tests/golden.
 --impl reference times that CPU path (the reference's algorithm; the Python
 reference itself cannot run here: ~8 h per planner round at C2)
 over one FULL lifetime + plan of the trace (measured, with its plan sha256)
-and prints its own JSON line.  Multi-GPU (torchrun): each rank plans its own
-replica of the trace ("replicas only" for this config), timing is
-the max over ranks.
+and prints its own JSON line.
+
+Multi-GPU (torchrun, one process per GPU): strong scaling of the SAME trace —
+every rank runs the lifetime stage and the sharded planner
+(distributed.PlanGroup: candidate tiles split over the ranks, replicated
+planner state, each round's local bests exchanged through CUDA-IPC mailboxes
+over NVLink), so value = E / (max over ranks of the device time), and the
+line reports whether every rank's plan sha256 is the same.  The C4 leg runs
+at N = 1 only.
 """
 
 from __future__ import annotations
@@ -243,6 +249,15 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
     dt = _native.DeviceTrace(a, stream=sh)
     r = _rates_struct(rates)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    group = None
+    if world > 1:
+        # strong scaling: ONE trace planned by all ranks, candidate tiles
+        # sharded, per-round winner exchange over NVLink (distributed.PlanGroup)
+        from paper_2506_06472_b200.distributed import PlanGroup
+        group = PlanGroup(rank, world)
+
+    def plan_call():
+        return group.plan(dt, cap, r, hc) if group is not None else dt.plan(cap, r, hc)
 
     def step(evs=None):
         if evs:
@@ -250,7 +265,7 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
         _native.check(lib.tio_lifetime(dt.handle, ctypes.c_void_p(sh)))
         if evs:
             evs[1].record(stream)
-        p = dt.plan(cap, r, hc)
+        p = plan_call()
         if evs:
             evs[2].record(stream)
         return p
@@ -268,6 +283,9 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
         with Clocks(dev.index) as clk:
             for i in range(steps):
                 flush.fill_(1)          # L2 flush, outside the timed region
+                torch.cuda.synchronize()
+                if world > 1:
+                    torch.distributed.barrier()
                 evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 p = step(evs)
                 torch.cuda.synchronize()
@@ -281,10 +299,12 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
                 p.close()
         launches = _native.kernel_launches() - launches0
         torch.cuda.synchronize()
-    t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([tot_ms, loop_ms], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    tot_ms_max = float(t.item())
+    tot_ms_max = float(t[0].item())
+    loop_ms = float(t[1].item())
+    agree = group.plans_agree(plan_bytes) if group is not None else True
 
     # ---- e2e: C-ABI one-shot call, pinned host columns, host entries out
     cols = _native.HostColumns(a)
@@ -303,15 +323,34 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
     d2h = ne * _native.ENTRY_DTYPE.itemsize
 
     def one_shot():
-        _native.check(lib.tio_plan_host(ctypes.byref(desc_c), ctypes.c_int64(cap), ctypes.byref(r),
-                                        ctypes.c_int64(hc), ctypes.c_void_p(sh), ctypes.byref(pinfo),
-                                        ctypes.c_void_p(ent.data_ptr()), ctypes.c_int64(ne)))
+        if group is None:
+            _native.check(lib.tio_plan_host(ctypes.byref(desc_c), ctypes.c_int64(cap), ctypes.byref(r),
+                                            ctypes.c_int64(hc), ctypes.c_void_p(sh), ctypes.byref(pinfo),
+                                            ctypes.c_void_p(ent.data_ptr()), ctypes.c_int64(ne)))
+            return
+        # N > 1: the same C-ABI calls composed — trace upload from the pinned
+        # host columns, lifetime, sharded plan, entries back to pinned host
+        th = ctypes.c_void_p()
+        _native.check(lib.tio_trace_create(ctypes.byref(desc_c), _native.TIO_MEM_HOST, ctypes.c_void_p(sh),
+                                           ctypes.byref(th)))
+        try:
+            pdt = _native.DeviceTrace.__new__(_native.DeviceTrace)
+            pdt._lib, pdt.handle, pdt.stream = lib, th, ctypes.c_void_p(sh)
+            pdt.num_kernels, pdt.num_tensors = N, T
+            p = group.plan(pdt, cap, r, hc)
+            _native.check(lib.tio_plan_copy_out(p.handle, ctypes.c_void_p(sh), None,
+                                                ctypes.c_void_p(ent.data_ptr()), None, None))
+            p.close()
+        finally:
+            lib.tio_trace_destroy(th)
     for _ in range(2):
         one_shot()
     e2e_ms = 0.0
     for _ in range(steps):
         flush.fill_(1)
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -349,13 +388,18 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
         except Exception:
             ptraffic = None
     loop_s = loop_ms / K / 1e3
+    if group is not None:
+        group.close()
     return {
-        "value": world * E * K / (tot_ms_max / 1e3), "ms_per_step": tot_ms_max / K,
+        "value": E * K / (tot_ms_max / 1e3), "ms_per_step": tot_ms_max / K,
         "config": {"workload": desc, "events": E, "kernels": N, "tensors": T, "periods": P,
                    "capacity": cap, "rates": "ssd 16000 B/us symmetric", "host_cap": hc,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": (f"sharded{world}: one trace, candidate tiles split over ranks, per-round "
+                                   f"winner exchange through CUDA-IPC mailboxes over NVLink") if world > 1
+                   else "single",
                    "l2": "flushed (256 MiB write) before every step, outside the timed region",
-                   "plan_sha256": hashlib.sha256(plan_bytes).hexdigest()},
+                   "plan_sha256": hashlib.sha256(plan_bytes).hexdigest(),
+                   "plan_sha256_equal_on_all_ranks": bool(agree)},
         "breakdown_ms": {"lifetime": life_ms / K, "plan": plan_ms / K, "plan_round_loop": loop_ms / K,
                          "plan_setup_epilogue_host": (plan_ms - loop_ms) / K},
         "roofline": {"kernel": "lifetime (k_tile_owners + k_events + k_kernels)", "bound": "hbm",
@@ -384,8 +428,11 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
                         "refits_per_round": info.dbg[9] / max(1, rounds),
                         "max_block_phase_E_us_per_round": info.dbg[10] / 1e3 / max(1, rounds)}}
                        if any(info.dbg[q] for q in range(12)) else {})},
-        "e2e": {"value": world * E * K / (e2e_ms / 1e3), "unit": "events/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "api": "tio_plan_host (C ABI), pinned host buffers"},
+        "e2e": {"value": E * K / (e2e_ms / 1e3), "unit": "events/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "api": "tio_plan_host (C ABI), pinned host buffers" if world == 1 else
+                       "tio_trace_create (pinned host) + tio_lifetime + sharded tio_plan_create2 + "
+                       "tio_plan_copy_out (C ABI), per rank"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "rounds": rounds,
@@ -418,14 +465,16 @@ def sharded_lifetime_leg(config: str, dev, rank: int, world: int) -> dict:
         dt = time.perf_counter() - t0
         t = torch.tensor([dt], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        same = all(np.array_equal(np.asarray(out[k]), np.asarray(ref[k]))
+        same = all(np.array_equal(out[k].cpu().numpy() if hasattr(out[k], "cpu") else np.asarray(out[k]),
+                                  np.asarray(ref[k]))
                    for k in ("timeline", "active", "period_tensor", "period_start", "period_end", "period_wraps"))
         ok = torch.tensor([1 if same else 0], dtype=torch.int64, device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         return {"workload": desc, "ranks": world, "ms_wall_max_over_ranks": float(t.item()) * 1e3,
                 "bit_exact_vs_unsharded": bool(ok.item()), "shard_events": int(a.access_ptr[out["shard"][1]] -
                                                                                a.access_ptr[out["shard"][0]]),
-                "collectives": f"{dist.get_backend()} all_reduce(int64[2N]) + all_gather(counts, padded period columns)"}
+                "collectives": f"{dist.get_backend()} all_reduce(int64[2N]) + all_gather(counts, padded period "
+                               f"columns), device-resident"}
     except Exception as exc:  # reported, not fatal: the headline line must still print
         return {"error": f"{type(exc).__name__}: {exc}"}
 
@@ -446,7 +495,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     line = {
         "metric": "trace events/s (lifetime+plan)", "value": m.pop("value"), "unit": "events/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": m.pop("ms_per_step"), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic", **m,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        **m,
     }
     if extra is not None:
         extra.pop("clocks", None)

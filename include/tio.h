@@ -189,9 +189,12 @@ typedef struct tio_plan_opts {
      * so every rank ends with the full plan.  mailbox: this rank's
      * tio_mailbox_bytes() of device memory (zeroed once); peer_mailboxes:
      * [nranks] device pointers of every rank's mailbox as mapped in this
-     * process (CUDA IPC / peer access; [rank] = mailbox); epoch: strictly
-     * increasing per planning call over the mailbox's lifetime (flags are
-     * compared against epoch + round + 1, so no reset is needed).
+     * process (CUDA IPC / peer access; [rank] = mailbox); epoch: 0 for the
+     * first planning call over a mailbox, then previous epoch + previous
+     * rounds + 2 (flags are compared against epoch + round + 1 and the message
+     * slot is that tag's parity, so no reset is needed between calls).  A
+     * peer that does not publish within 30 s ends the call with TIO_ERR_CUDA
+     * ("rank exchange timed out").
      * blocks > 0 overrides the planner's grid (virtual ranks on one GPU). */
     int32_t nranks;
     int32_t rank;
@@ -203,6 +206,18 @@ typedef struct tio_plan_opts {
 } tio_plan_opts;
 /* device bytes of one rank's mailbox */
 size_t tio_mailbox_bytes(void);
+/* One rank's mailbox for sharded planning across processes (one process per
+ * GPU: the per-round `allgather` of local bests): allocated and
+ * zeroed on the current device; ipc_handle receives its CUDA IPC handle
+ * (TIO_IPC_HANDLE_BYTES) for the other ranks, which map it with
+ * tio_mailbox_open (peer access over NVLink enabled lazily).  Replaces no
+ * reference function: the reference plans on one CPU thread
+ * (planner.py:293-351). */
+#define TIO_IPC_HANDLE_BYTES 64
+int tio_mailbox_create(void **mailbox, unsigned char *ipc_handle);
+int tio_mailbox_destroy(void *mailbox);
+int tio_mailbox_open(const unsigned char *ipc_handle, void **mapped);
+int tio_mailbox_close(void *mapped);
 /* Sharded planning of one trace by `nranks` virtual ranks on THIS GPU (the
  * check of the multi-GPU protocol on one device): rank r runs as a separate
  * planner instance (own replicated state, own stream, its own cooperative

@@ -115,11 +115,13 @@ EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_devi
            "tio_engine_before_kernel", "tio_engine_after_kernel", "tio_engine_step_end", "tio_engine_stats_get",
            "tio_engine_destroy", "tio_checksum",
            "tio_engine_set_verify", "tio_engine_restore",
-           "tio_engine_check_program", "tio_engine_step_abort", "tio_plan_create_virtual")
+           "tio_engine_check_program", "tio_engine_step_abort", "tio_plan_create_virtual",
+           "tio_mailbox_create", "tio_mailbox_destroy", "tio_mailbox_open", "tio_mailbox_close")
 
 
 def lib_path() -> str:
-    return _build.LIB
+    # TIO_LIB_PATH: a variant build (tools/build_variant.sh) for experiments
+    return os.environ.get("TIO_LIB_PATH") or _build.LIB
 
 
 def load(build_if_missing: bool = True):
@@ -317,6 +319,46 @@ class DevicePlan:
             self.close()
         except Exception:
             pass
+
+
+IPC_HANDLE_BYTES = 64
+
+
+class Mailbox:
+    """One rank's sharded-planning mailbox in device memory (tio_mailbox_create)
+    and its CUDA IPC handle for the other ranks."""
+
+    def __init__(self):
+        require_device()
+        self._lib = load()
+        self.ptr = ctypes.c_void_p()
+        buf = (ctypes.c_ubyte * IPC_HANDLE_BYTES)()
+        check(self._lib.tio_mailbox_create(ctypes.byref(self.ptr), buf))
+        self.handle = bytes(buf)
+
+    def close(self) -> None:
+        if self.ptr:
+            self._lib.tio_mailbox_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mailbox_open(handle: bytes) -> int:
+    """Map another process's mailbox (CUDA IPC, peer access over NVLink)."""
+    lib = load()
+    buf = (ctypes.c_ubyte * IPC_HANDLE_BYTES).from_buffer_copy(handle)
+    out = ctypes.c_void_p()
+    check(lib.tio_mailbox_open(buf, ctypes.byref(out)))
+    return int(out.value)
+
+
+def mailbox_close(ptr: int) -> None:
+    check(load().tio_mailbox_close(ctypes.c_void_p(ptr)))
 
 
 def kernel_launches() -> int:

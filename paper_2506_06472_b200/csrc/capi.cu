@@ -571,6 +571,9 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
                          (long long)pi.unsat_bytes, (long long)capacity));
     }
     if (hs[PS_STATUS] == 2) return bail(fail(TIO_ERR_INVALID, "trace violates model invariants"));
+    if (hs[PS_STATUS] == 3)
+        return bail(fail(TIO_ERR_CUDA, "sharded planning: rank exchange timed out in round %lld (a peer rank never "
+                         "published its round message)", (long long)hs[PS_ROUNDS]));
     if (hs[PS_INVARIANT]) return bail(fail(TIO_ERR_INTERNAL, "channel bookings overlapped (disjointness invariant)"));
     const int64_t nc = hs[PS_COMMITS];
     pi.num_commits = nc;
@@ -721,6 +724,42 @@ int tio_plan_destroy(tio_plan *p) {
 }
 
 size_t tio_mailbox_bytes(void) { return sizeof(Mailbox); }
+
+static_assert(sizeof(cudaIpcMemHandle_t) == TIO_IPC_HANDLE_BYTES, "IPC handle size");
+
+int tio_mailbox_create(void **mailbox, unsigned char *ipc_handle) {
+    if (!mailbox || !ipc_handle) return fail(TIO_ERR_INVALID, "null argument");
+    *mailbox = nullptr;
+    void *p = nullptr;
+    TIO_CUDA(cudaMalloc(&p, sizeof(Mailbox)));
+    cudaIpcMemHandle_t h;
+    if (cudaMemset(p, 0, sizeof(Mailbox)) != cudaSuccess || cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+        cudaFree(p);
+        return fail(TIO_ERR_CUDA, "mailbox: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    memcpy(ipc_handle, &h, sizeof(h));
+    *mailbox = p;
+    return TIO_OK;
+}
+
+int tio_mailbox_destroy(void *mailbox) {
+    if (mailbox) TIO_CUDA(cudaFree(mailbox));
+    return TIO_OK;
+}
+
+int tio_mailbox_open(const unsigned char *ipc_handle, void **mapped) {
+    if (!ipc_handle || !mapped) return fail(TIO_ERR_INVALID, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    *mapped = nullptr;
+    TIO_CUDA(cudaIpcOpenMemHandle(mapped, h, cudaIpcMemLazyEnablePeerAccess));
+    return TIO_OK;
+}
+
+int tio_mailbox_close(void *mapped) {
+    if (mapped) TIO_CUDA(cudaIpcCloseMemHandle(mapped));
+    return TIO_OK;
+}
 
 int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rates, int64_t host_cap,
                             const tio_plan_opts *opts, int32_t nranks, tio_plan **out, tio_plan_info *info) {

@@ -48,13 +48,45 @@ constexpr int KT_TILE = KT_THREADS * KT_EPT;
 __host__ __device__ int64_t lifetime_event_tiles(int64_t E) { return (E + LT_TILE - 1) / LT_TILE; }
 __host__ __device__ int64_t lifetime_kernel_tiles(int64_t N) { return (N + KT_TILE - 1) / KT_TILE; }
 
+// Tile prefixes without a look-back chain: every tile publishes its
+// aggregate {value, flag} and adds it into its group of LB_GROUP tiles
+// ({sum, count}); a tile's exclusive prefix is the sum of the complete groups
+// before its own plus the aggregates of the earlier tiles of its group, all
+// loaded in parallel by one warp.  Tiles are claimed in order from an atomic
+// ticket, so every earlier tile is resident or finished and publishes without
+// waiting on anything: the wait is for the slowest predecessor's publish, not
+// for a chain of inclusive prefixes (a decoupled look-back's inclusive
+// frontier advances ~64 tiles per L2 round trip — at C3's 4,851 event tiles
+// that chain was the k_events time).
+constexpr int LB_GROUP = 32;
+__host__ __device__ __forceinline__ int64_t lb_groups(int64_t ntiles) { return (ntiles + LB_GROUP - 1) / LB_GROUP; }
+
 // workspace layout (int64 words): [0,2) tile counters | owners [NTe+1],
-// padded to an even length | event look-back status [2 NTe] | dur / diff
-// look-back status [2 NTk] each (status words 16-byte aligned)
+// padded to an even length | event tile status [2 NTe] | dur / diff tile
+// status [2 NTk] each | event groups [2 NGe] | dur / diff groups [2 NGk]
+// each (16-byte words, 16-byte aligned; everything after the owners is
+// zeroed by k_tile_owners)
 __host__ __device__ __forceinline__ int64_t owners_len(int64_t nte) { return (nte + 3) & ~(int64_t)1; }
 int64_t lifetime_workspace_elems(int64_t N, int64_t E) {
     const int64_t nte = lifetime_event_tiles(E), ntk = lifetime_kernel_tiles(N);
-    return 2 + owners_len(nte) + 2 * nte + 4 * ntk + 8;
+    return 2 + owners_len(nte) + 2 * nte + 4 * ntk + 2 * lb_groups(nte) + 4 * lb_groups(ntk) + 8;
+}
+struct LtWork {
+    int64_t *owner;          // [NTe + 1]
+    int64_t *est, *kst;      // event tile status [2 NTe]; dur / diff tile status [2 NTk] each
+    int64_t *egrp, *kgrp;    // event groups [2 NGe]; dur / diff groups [2 NGk] each
+    int64_t nzero;           // words from est to the end of the groups
+};
+__host__ __device__ __forceinline__ LtWork lt_work(int64_t *work, int64_t N, int64_t E) {
+    const int64_t nte = lifetime_event_tiles(E), ntk = lifetime_kernel_tiles(N);
+    LtWork w;
+    w.owner = work + 2;
+    w.est = w.owner + owners_len(nte);
+    w.kst = w.est + 2 * nte;
+    w.egrp = w.kst + 4 * ntk;
+    w.kgrp = w.egrp + 2 * lb_groups(nte);
+    w.nzero = 2 * nte + 4 * ntk + 2 * lb_groups(nte) + 4 * lb_groups(ntk);
+    return w;
 }
 
 // ---------------------------------------------------------------- look-back
@@ -74,44 +106,52 @@ __device__ __forceinline__ void status_load(const int64_t *st, int64_t tile, int
     *flag = f;
 }
 
-// Decoupled look-back, split so a tile can publish its aggregate as soon as
-// it is known and do independent work before it needs its prefix.
-__device__ __forceinline__ void lookback_publish(int64_t *st, int64_t tile, int64_t agg) {
-    if ((threadIdx.x & 31) == 0) status_store(st, tile, agg, tile == 0 ? 2 : 1);
+// Publish a tile's aggregate (lane 0 of the calling warp): the tile status,
+// then the group sum and, with release semantics, the group count.
+__device__ __forceinline__ void agg_publish(int64_t *st, int64_t *grp, int64_t tile, int64_t agg) {
+    if ((threadIdx.x & 31) == 0) {
+        status_store(st, tile, agg, 1);
+        int64_t *g = grp + 2 * (tile / LB_GROUP);
+        if (agg) atomic_add_i64(g, agg);
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(g + 1) : "memory");
+    }
 }
 
 // Exclusive prefix of tile `tile` (one warp, all lanes; the result in every
-// lane); publishes the inclusive prefix.  nch independent chains (stride
-// cstride words) resolved in the same loop.
+// lane) over NCH independent chains (status / group arrays at strides sst /
+// sgrp words).  Complete groups first, then the own group's earlier tiles.
 template <int NCH>
-__device__ void lookback_resolve(int64_t *st, int64_t cstride, int64_t tile, const int64_t *agg, int64_t *prefix) {
+__device__ void agg_prefix(const int64_t *st, int64_t sst, const int64_t *grp, int64_t sgrp, int64_t tile,
+                           int64_t *prefix) {
     const int lane = threadIdx.x & 31;
-    for (int c = 0; c < NCH; ++c) prefix[c] = 0;
-    if (tile == 0) return;
-    bool done[NCH];
-    for (int c = 0; c < NCH; ++c) done[c] = false;
-    int64_t base = tile - 1;                 // lanes read base - lane
-    while (true) {
-        const int64_t idx = base - lane;
-        bool all = true;
+    const int64_t g = tile / LB_GROUP;
+    int64_t acc[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) acc[c] = 0;
+    for (int64_t q = lane; q < g; q += 32) {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-            if (done[c]) continue;
-            int64_t v = 0, f = 2;            // before tile 0: an inclusive 0
-            if (idx >= 0) {
-                do { status_load(st + c * cstride, idx, &v, &f); } while (f == 0);
-            }
-            const unsigned inc = __ballot_sync(0xffffffffu, f == 2);
-            const int stop = inc ? __ffs(inc) - 1 : 32;      // nearest inclusive prefix
-            prefix[c] += warp_sum<int64_t>(lane <= stop ? v : 0);
-            done[c] = inc != 0;
-            all = all && done[c];
+            const int64_t *gp = grp + c * sgrp + 2 * q;
+            long long n;
+            do {
+                asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(n) : "l"(gp + 1) : "memory");
+            } while (n < LB_GROUP);
+            long long v;
+            asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(gp) : "memory");
+            acc[c] += v;
         }
-        if (all) break;
-        base -= 32;
     }
-    if (lane == 0)
-        for (int c = 0; c < NCH; ++c) status_store(st + c * cstride, tile, prefix[c] + agg[c], 2);
+    const int64_t j = g * LB_GROUP + lane;
+    if (j < tile) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            int64_t v, f;
+            do { status_load(st + c * sst, j, &v, &f); } while (f == 0);
+            acc[c] += v;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) prefix[c] = warp_sum<int64_t>(acc[c]);
 }
 
 // ---------------------------------------------------------------- owners
@@ -184,7 +224,8 @@ __device__ __forceinline__ int32_t block_exclusive_max(int32_t v, int32_t *sm) {
 // in shared memory at tile-local offsets.  The tile prefix comes from a
 // decoupled look-back; records are then stored coalesced.
 __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, EvSmem &sm, int64_t tile,
-                                                         int64_t NTe, int64_t *est, const int64_t *owner) {
+                                                         int64_t NTe, int64_t *est, int64_t *egrp,
+                                                         const int64_t *owner) {
     const int64_t T = a.T, E = a.E;
     const int32_t N = (int32_t)a.N;
     unsigned long long flags = 0;
@@ -271,7 +312,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     // successors' look-backs only wait for this counting walk
     int64_t tot;
     const int64_t loc = block_exclusive_sum<int64_t>(cnt, sm.scan, &tot);
-    if (threadIdx.x < 32) lookback_publish(est, tile, tot);
+    if (threadIdx.x < 32) agg_publish(est, egrp, tile, tot);
 
     // ---- walk 2: per-kernel active bytes and the timeline difference array
     if (!(flags & (LF_ACCESS_RANGE | LF_BAD_PTR))) {
@@ -302,7 +343,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     // ---- tile prefix
     if (threadIdx.x < 32) {
         int64_t pre;
-        lookback_resolve<1>(est, 0, tile, &tot, &pre);
+        agg_prefix<1>(est, 0, egrp, 0, tile, &pre);
         if (threadIdx.x == 0) sm.prefix = pre;
     }
     __syncthreads();
@@ -353,7 +394,8 @@ k_events(LifetimeArgs a) {
     __syncthreads();
     const int64_t tile = sm.tile;
     unsigned long long flags = 0;
-    if (tile < NTe) flags = event_tile(a, sm, tile, NTe, a.work + 2 + owners_len(NTe), a.work + 2);
+    const LtWork w = lt_work(a.work, a.N, E);
+    if (tile < NTe) flags = event_tile(a, sm, tile, NTe, w.est, w.egrp, w.owner);
 
     // ---- a slice of the tensor table: CSR / size / kind / id order, global bytes
     {
@@ -385,7 +427,7 @@ k_kernels(LifetimeArgs a) {
     __shared__ int64_t s_tile;
     const int64_t N = a.N, E = a.E;
     const int64_t NTe = lifetime_event_tiles(E), NTk = lifetime_kernel_tiles(N);
-    int64_t *dst = a.work + 2 + owners_len(NTe) + 2 * NTe;     // dur chain, then diff chain (+2 NTk)
+    const LtWork w = lt_work(a.work, N, E);                     // dur chain, then diff chain
     if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(a.work + 1), 1ull);
     __syncthreads();
     const int64_t tile = s_tile;
@@ -421,10 +463,10 @@ k_kernels(LifetimeArgs a) {
     int64_t xd = block_exclusive_sum<int64_t>(sd, scan, &agg[0]);
     int64_t xf = block_exclusive_sum<int64_t>(sf, scan, &agg[1]);
     if (threadIdx.x < 32) {
-        lookback_publish(dst, tile, agg[0]);
-        lookback_publish(dst + 2 * NTk, tile, agg[1]);
+        agg_publish(w.kst, w.kgrp, tile, agg[0]);
+        agg_publish(w.kst + 2 * NTk, w.kgrp + 2 * lb_groups(NTk), tile, agg[1]);
         int64_t pre[2];
-        lookback_resolve<2>(dst, 2 * NTk, tile, agg, pre);
+        agg_prefix<2>(w.kst, 2 * NTk, w.kgrp, 2 * lb_groups(NTk), tile, pre);
         if (threadIdx.x == 0) { s_pre[0] = pre[0]; s_pre[1] = pre[1]; }
     }
     __syncthreads();
@@ -466,9 +508,10 @@ int launch_lifetime(const LifetimeArgs &args, cudaStream_t stream) {
         attr = true;
     }
     const int64_t NTe = lifetime_event_tiles(args.E), NTk = lifetime_kernel_tiles(args.N);
-    // counters + event / kernel look-back status: zeroed by k_tile_owners
-    int64_t *status = args.work + 2 + owners_len(NTe);
-    const int64_t nstatus = 2 * NTe + 4 * NTk;
+    // counters + tile status + group sums: zeroed by k_tile_owners
+    const LtWork w = lt_work(args.work, args.N, args.E);
+    int64_t *status = w.est;
+    const int64_t nstatus = w.nzero;
     if (NTe > 0) {
         const int64_t thr = 32 * (NTe + 1);
         k_tile_owners<<<(unsigned)((thr + 255) / 256), 256, 0, stream>>>(args.ptr, args.T, args.E, NTe, args.work + 2,

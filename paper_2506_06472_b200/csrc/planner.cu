@@ -35,6 +35,9 @@ namespace cg = cooperative_groups;
 namespace tio {
 
 constexpr int MAXG = 1024;
+// longest wait for the other ranks' round message before a sharded planning
+// call gives up (status 3, TIO_ERR_CUDA "rank exchange timed out")
+constexpr int64_t EXCHANGE_TIMEOUT_NS = 30000000000ll;
 
 struct LastCommit {
     int64_t dest;                 // 0 none (first round), 1 SSD, 2 CPU
@@ -475,23 +478,36 @@ __device__ void round_winner(const PlanArgs &a, int64_t round, int G, Key *sm_ke
                 for (int q = 0; q < 4; ++q) m.r[q] = ld_cg(&a.rng[4 * c + q]);
             }
             if (a.nranks > 1) {
-                const int slot = (int)(round & 1);
+                // slot parity follows the tag, so it keeps alternating across
+                // consecutive planning calls (epoch += rounds + 2 between calls)
                 const unsigned long long tag = a.epoch + (unsigned long long)round + 1;
+                const int slot = (int)(tag & 1);
                 for (int p = 0; p < a.nranks; ++p) {
                     Mailbox *mb = a.mb_peer[p];
                     msg_store(&mb->msg[slot][a.rank], m);
                     st_release_sys(&mb->flag[a.rank], tag);
                 }
                 Mailbox *me = a.mb_self;
-                for (int p = 0; p < a.nranks; ++p)
-                    while (ld_acquire_sys(&me->flag[p]) < tag) {
+                // bounded wait: a rank that never arrives (died, or was never
+                // launched) ends this planning call with status 3 instead of
+                // hanging the GPU; the round then has no winner on this rank
+                const int64_t t0 = gtime();
+                bool lost = false;
+                unsigned spins = 0;
+                for (int p = 0; p < a.nranks && !lost; ++p)
+                    while (ld_acquire_sys(&me->flag[p]) < tag)
+                        if ((++spins & 1023u) == 0 && gtime() - t0 > EXCHANGE_TIMEOUT_NS) { lost = true; break; }
+                if (lost) {
+                    a.scalars[PS_STATUS] = 3;
+                    memset(&m, 0, sizeof(m));
+                } else {
+                    WinMsg best = msg_load(&me->msg[slot][0]);
+                    for (int p = 1; p < a.nranks; ++p) {
+                        const WinMsg o = msg_load(&me->msg[slot][p]);
+                        if (kbetter(o.k, best.k)) best = o;
                     }
-                WinMsg best = msg_load(&me->msg[slot][0]);
-                for (int p = 1; p < a.nranks; ++p) {
-                    const WinMsg o = msg_load(&me->msg[slot][p]);
-                    if (kbetter(o.k, best.k)) best = o;
+                    m = best;
                 }
-                m = best;
             }
             msg_store(a.win, m);
             st_release_gpu(a.win_gen, (unsigned long long)round + 1);

@@ -102,3 +102,74 @@ def test_virtual_ranks_c2_full_plan(nranks):
     for o in outs:
         assert hashlib.sha256(o["plan_bytes"]).hexdigest() == rec["plan_sha256"]
         assert hashlib.sha256(o["residual"].tobytes()).hexdigest() == rec["residual_sha256"]
+
+
+# ---------------------------------------------------------------- processes
+def _proc_worker(rank, world, port, q):
+    """One rank in its own process: gloo for the IPC-handle exchange (two
+    ranks cannot share a GPU under NCCL), mailboxes mapped over CUDA IPC,
+    libtio's sharded planner on cuda:0 (the ranks time-share the device)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    from paper_2506_06472_b200 import _native
+    from paper_2506_06472_b200.distributed import PlanGroup
+    from paper_2506_06472_b200.planner import _rates_struct
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = PlanGroup(rank, world)
+        out = []
+        for tr, rec in _golden_traces():
+            dt = _native.DeviceTrace(tr.arrays())
+            # two consecutive calls over the same mailboxes (epochs advance)
+            for _ in range(2):
+                p = g.plan(dt, rec["capacity"], _rates_struct(rates_of(rec)), rec["host_cap"])
+                b = p.write()
+                resid = p.copy_out()["residual"]
+                out.append((hashlib.sha256(b).hexdigest(), resid.tolist(), g.plans_agree(b)))
+                p.close()
+            dt.close()
+        dist.barrier()
+        g.close()
+        q.put((rank, out, None))
+    except Exception as exc:  # reported to the parent
+        q.put((rank, None, f"{type(exc).__name__}: {exc}"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_two_processes_ipc_mailboxes_match_reference_goldens():
+    """The multi-process path of the sharded planner (PlanGroup: device
+    mailboxes exchanged as CUDA IPC handles, one process per rank) on one
+    B200: both ranks' plans equal the reference goldens, twice in a row."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_proc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, out, err = q.get(timeout=540)
+        assert err is None, f"rank {r}: {err}"
+        res[r] = out
+    for p in procs:
+        p.join(timeout=60)
+    recs = [rec for _, rec in _golden_traces() for _ in range(2)]
+    for r in (0, 1):
+        assert len(res[r]) == len(recs)
+        for (sha, resid, agree), rec in zip(res[r], recs):
+            assert sha == rec["plan_sha256"]
+            assert resid == rec["residual"]
+            assert agree
