@@ -435,6 +435,43 @@ int tio_parsed_destroy(tio_parsed_trace *p);
 /* ceil(nbytes / rate) exactly; TIO_ERR_CHANNEL_CONFIG for rate <= 0. */
 int tio_transfer_duration(double rate, int64_t nbytes, int64_t *out);
 
+/* ---- host channels and per-candidate helpers ---------------------------------
+ * One serial migration channel with its bookings (BandwidthChannel,
+ * bandwidth.py:47-164): bookings sorted by start (equal starts in insertion
+ * order), periodic images at +-period (period <= 0: none) released with their
+ * booking.  Host memory only; the planner's own channels live on the device.
+ * Booking ids are > 0; images carry their booking's id as `owner`. */
+typedef struct tio_channel tio_channel;
+int tio_channel_create(double rate, int64_t period, tio_channel **out);          /* :47-73, ChannelConfigError */
+int tio_channel_destroy(tio_channel *c);
+int tio_channel_reserve_earliest(tio_channel *c, int64_t ready, int64_t nbytes, int64_t tensor_id,
+                                 int64_t *id, int64_t *start, int64_t *end);    /* :88-100  */
+int tio_channel_reserve_latest(tio_channel *c, int64_t deadline, int64_t not_before, int64_t nbytes,
+                               int64_t tensor_id, int32_t *found, int64_t *id, int64_t *start,
+                               int64_t *end);                                    /* :102-120 */
+int tio_channel_record(tio_channel *c, int64_t start, int64_t end, int64_t tensor_id, int32_t shadow,
+                       int64_t *id);                                             /* :129-137 */
+int tio_channel_release(tio_channel *c, int64_t id);                             /* :122-127 */
+int tio_channel_size(const tio_channel *c, int64_t *n);
+int tio_channel_copy(const tio_channel *c, int64_t *start, int64_t *end, int64_t *tensor, int64_t *id,
+                     int64_t *owner, int8_t *shadow);                            /* .reservations */
+int tio_channel_busy(const tio_channel *c, int64_t w0, int64_t w1, int64_t *busy); /* :153-164 */
+/* candidate_window (planner.py:147-176) on one channel pair; *ok = 0: None
+ * (nothing stays booked), 1: both bookings live. */
+int tio_candidate_window(tio_channel *off, tio_channel *pre, int64_t ready, int64_t deadline, int64_t nbytes,
+                         int64_t iteration, int64_t tensor_id, int32_t *ok, int64_t *off_id, int64_t *off_end,
+                         int64_t *pre_id, int64_t *pre_start);
+/* _host_peak_occupancy (planner.py:179-186) */
+int tio_host_peak_occupancy(const int64_t *s, const int64_t *e, const int64_t *sz, int64_t n, int64_t lo,
+                            int64_t hi, int64_t *out);
+/* candidate_benefit (planner.py:232-262): benefit = (hi << 64) | lo;
+ * critical: optional [N] mask of the over-capacity covered kernels.
+ * starts: [N+1] kernel start times (starts[N] = iteration). */
+int tio_candidate_benefit(const int64_t *starts, const int64_t *dur, const int64_t *residual, int64_t N,
+                          int64_t capacity, int32_t wraps, int64_t start_kernel, int64_t end_kernel, int64_t first,
+                          int64_t last, int64_t lo, int64_t hi, int64_t size, uint64_t *benefit_lo,
+                          uint64_t *benefit_hi, int8_t *critical);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,7 +116,10 @@ EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_devi
            "tio_engine_destroy", "tio_checksum",
            "tio_engine_set_verify", "tio_engine_restore",
            "tio_engine_check_program", "tio_engine_step_abort", "tio_plan_create_virtual",
-           "tio_mailbox_create", "tio_mailbox_destroy", "tio_mailbox_open", "tio_mailbox_close")
+           "tio_mailbox_create", "tio_mailbox_destroy", "tio_mailbox_open", "tio_mailbox_close",
+           "tio_channel_create", "tio_channel_destroy", "tio_channel_reserve_earliest", "tio_channel_reserve_latest",
+           "tio_channel_record", "tio_channel_release", "tio_channel_size", "tio_channel_copy", "tio_channel_busy",
+           "tio_candidate_window", "tio_host_peak_occupancy", "tio_candidate_benefit")
 
 
 def lib_path() -> str:

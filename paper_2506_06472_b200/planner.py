@@ -15,6 +15,8 @@ planner does not use.
 
 from __future__ import annotations
 
+import ctypes
+
 import json
 import logging
 from collections.abc import Sequence
@@ -162,28 +164,36 @@ def _starts_full(trace: Trace) -> list[int]:
 
 def candidate_window(period: InactivePeriod, trace: Trace, offload_channel: BandwidthChannel,
                      prefetch_channel: BandwidthChannel, destination: str) -> CandidateWindow | None:
-    """Book a trial offload/prefetch pair (planner.py:147-176); on success the
-    bookings stay live in the channels, on failure everything is rolled back."""
+    """Book a trial offload/prefetch pair (planner.py:147-176, libtio
+    `tio_candidate_window`); on success the bookings stay live in the
+    channels, on failure nothing stays booked."""
     starts = _starts_full(trace)
     iteration = starts[-1]
     ready, deadline = _period_times(period, trace, starts, iteration)
-    size = period.size_bytes
-    if (offload_channel.transfer_duration(size) > iteration
-            or prefetch_channel.transfer_duration(size) > iteration):
+    ok, oid, oend, pid, pstart = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), \
+        ctypes.c_int64()
+    _native.check(_native.load().tio_candidate_window(
+        offload_channel._h, prefetch_channel._h, ctypes.c_int64(ready), ctypes.c_int64(deadline),
+        ctypes.c_int64(period.size_bytes), ctypes.c_int64(iteration), ctypes.c_int64(period.tensor_id),
+        ctypes.byref(ok), ctypes.byref(oid), ctypes.byref(oend), ctypes.byref(pid), ctypes.byref(pstart)))
+    if not ok.value:
         return None
-    off = offload_channel.reserve_earliest(ready, size, period.tensor_id)
-    pre = prefetch_channel.reserve_latest(deadline, off.end, size, period.tensor_id)
-    if pre is None or not off.end < pre.start:
-        if pre is not None:
-            prefetch_channel.release(pre)
-        offload_channel.release(off)
-        return None
+    d_off = offload_channel.transfer_duration(period.size_bytes)
+    d_pre = prefetch_channel.transfer_duration(period.size_bytes)
+    off = offload_channel._booked(oid.value, oend.value - d_off, oend.value, period.tensor_id)
+    pre = prefetch_channel._booked(pid.value, pstart.value, pstart.value + d_pre, period.tensor_id)
     return CandidateWindow(off.end, pre.start, off, pre, destination)
 
 
 def _host_peak_occupancy(intervals, lo: int, hi: int) -> int:
-    points = {lo} | {s for s, _, _ in intervals if lo <= s <= hi}
-    return max((sum(sz for s, e, sz in intervals if s <= p < e) for p in points), default=0)
+    """planner.py:179-186 (libtio `tio_host_peak_occupancy`)."""
+    iv = np.asarray([(s, e, z) for s, e, z in intervals], np.int64).reshape(-1, 3)
+    cols = [np.ascontiguousarray(iv[:, j]) for j in range(3)]
+    out = ctypes.c_int64()
+    _native.check(_native.load().tio_host_peak_occupancy(
+        *(c.ctypes.data_as(ctypes.c_void_p) for c in cols), ctypes.c_int64(iv.shape[0]), ctypes.c_int64(lo),
+        ctypes.c_int64(hi), ctypes.byref(out)))
+    return out.value
 
 
 def _release(window: CandidateWindow, ssd: ChannelPair, host: ChannelPair | None) -> None:
@@ -217,24 +227,30 @@ def select_destination(period: InactivePeriod, trace: Trace, ssd_channels: Chann
 
 def candidate_benefit(window: CandidateWindow, period: InactivePeriod, residual: MemoryTimeline,
                       capacity: int, trace: Trace) -> Benefit:
-    """size x duration of over-capacity kernels fully inside the window."""
-    starts = _starts_full(trace)
-    iteration = starts[-1]
-    lo, hi = window.t_offloaded, window.t_prefetch
-    if not period.wraps:
-        spans = [(period.start_kernel, period.end_kernel + 1, 0)]
-    else:
-        a = trace.arrays()
+    """size x duration of over-capacity kernels fully inside the window
+    (planner.py:232-262, libtio `tio_candidate_benefit`)."""
+    a = trace.arrays()
+    N = a.num_kernels
+    starts = np.zeros(N + 1, np.int64)
+    np.cumsum(a.duration_us, out=starts[1:])
+    dur = np.ascontiguousarray(a.duration_us, np.int64)
+    resid = np.ascontiguousarray(np.asarray(residual.per_kernel_bytes, np.int64))
+    first = last = 0
+    if period.wraps:
         pos = int(np.flatnonzero(a.tensor_id == period.tensor_id)[0])
         first = int(a.accesses[a.access_ptr[pos]])
         last = int(a.accesses[a.access_ptr[pos + 1] - 1])
-        spans = [(last + 1, trace.num_kernels, 0), (0, first, iteration)]
-    covered = [k for a0, b0, sh in spans for k in range(a0, b0)
-               if starts[k] + sh >= lo and starts[k + 1] + sh <= hi]
-    critical = [k for k in covered if residual.per_kernel_bytes[k] > capacity]
-    d = trace.arrays().duration_us
-    return Benefit(value=period.size_bytes * int(sum(int(d[k]) for k in critical)),
-                   critical_kernels=frozenset(critical))
+    crit = np.zeros(max(N, 1), np.int8)
+    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+    vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _native.check(_native.load().tio_candidate_benefit(
+        vp(starts), vp(dur), vp(resid), ctypes.c_int64(N), ctypes.c_int64(capacity),
+        ctypes.c_int32(1 if period.wraps else 0), ctypes.c_int64(period.start_kernel),
+        ctypes.c_int64(period.end_kernel), ctypes.c_int64(first), ctypes.c_int64(last),
+        ctypes.c_int64(window.t_offloaded), ctypes.c_int64(window.t_prefetch), ctypes.c_int64(period.size_bytes),
+        ctypes.byref(lo), ctypes.byref(hi), vp(crit)))
+    return Benefit(value=(hi.value << 64) | lo.value,
+                   critical_kernels=frozenset(np.flatnonzero(crit[:N]).tolist()))
 
 
 # --- the device planner --------------------------------------------------------------
