@@ -160,6 +160,9 @@ int tio_trace_destroy(tio_trace *t);
  * destroy). */
 int tio_lifetime(tio_trace *t, void *stream);
 int tio_lifetime_view_get(tio_trace *t, void *stream, tio_lifetime_view *out);
+/* period_interior_duration (analysis.py:86-94) of every period, in period
+ * order, computed on the device from the start times: out = host [P]. */
+int tio_period_interior(tio_trace *t, void *stream, int64_t *out);
 /* Copy lifetime products to host buffers (any may be NULL). */
 int tio_lifetime_copy_out(tio_trace *t, void *stream, int64_t *starts, int64_t *timeline,
                           int64_t *active, int64_t *period_tensor, int32_t *period_start,

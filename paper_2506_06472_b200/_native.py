@@ -119,7 +119,8 @@ EXPORTS = ("tio_abi_version", "tio_kernel_launches", "tio_last_error", "tio_devi
            "tio_mailbox_create", "tio_mailbox_destroy", "tio_mailbox_open", "tio_mailbox_close",
            "tio_channel_create", "tio_channel_destroy", "tio_channel_reserve_earliest", "tio_channel_reserve_latest",
            "tio_channel_record", "tio_channel_release", "tio_channel_size", "tio_channel_copy", "tio_channel_busy",
-           "tio_candidate_window", "tio_host_peak_occupancy", "tio_candidate_benefit")
+           "tio_candidate_window", "tio_host_peak_occupancy", "tio_candidate_benefit",
+           "tio_period_interior")
 
 
 def lib_path() -> str:

@@ -7,9 +7,11 @@ device results into the reference's dataclasses.  `lifetime_arrays` returns
 the raw columns without building per-period Python objects (what large-trace
 callers should use).
 
-`period_interior_duration`, `characterize` and the CSV helpers are the
-reference's Fig-1/Fig-2 reporting (out of the hot-path scope, SURVEY §2 S2);
-they are restated on the host over the device-computed lifetime columns.
+`period_interior_durations` (every period's interior duration, the
+reference's only analogue of a "longest inactive gap") runs on the device;
+`period_interior_duration` (one period), `characterize` and the CSV helpers
+are the reference's Fig-1/Fig-2 reporting on the host over
+the device-computed columns.
 """
 
 from __future__ import annotations
@@ -116,6 +118,19 @@ def period_interior_duration(period: InactivePeriod, trace: Trace) -> int:
     return int(d[int(acc[-1]) + 1:].sum() + d[:int(acc[0])].sum())
 
 
+def period_interior_durations(trace: Trace) -> np.ndarray:
+    """period_interior_duration (analysis.py:86-94) of every inactive period,
+    in compute_inactive_periods order, computed on the device from the
+    kernel start times (libtio `tio_period_interior`)."""
+    import ctypes
+    dt = _device_trace(trace)
+    P = lifetime_arrays(trace).period_tensor.shape[0]
+    out = np.zeros(P, np.int64)
+    if P:
+        _native.check(dt._lib.tio_period_interior(dt.handle, dt.stream, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
 # --- characterization (reporting; reference analysis.py:120-188) -------------
 
 def bucket_label(bounds: tuple[int, ...], value: int) -> str:
@@ -152,15 +167,8 @@ def characterize(trace: Trace, capacity: int,
     if trace.num_tensors:
         la = lifetime_arrays(trace)
         a = trace.arrays()
-        cum = np.zeros(a.num_kernels + 1, np.int64)
-        np.cumsum(a.duration_us, out=cum[1:])
         tp = la.period_tensor
-        first = a.accesses[a.access_ptr[tp]]
-        last = a.accesses[a.access_ptr[tp + 1] - 1]
-        w = la.period_wraps.astype(bool)
-        inner = cum[np.minimum(la.period_end + 1, a.num_kernels)] - cum[la.period_start]
-        wrap = (cum[-1] - cum[np.minimum(last + 1, a.num_kernels)]) + cum[first]
-        interior = np.where(w, wrap, inner)
+        interior = period_interior_durations(trace)
         sizes = a.size_bytes[tp]
         for s, dur in zip(sizes.tolist(), interior.tolist()):
             cell = (bucket_label(size_buckets, s), bucket_label(duration_buckets, dur))

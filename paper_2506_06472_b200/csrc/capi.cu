@@ -93,9 +93,79 @@ int decode_rate(double rate, RateCode *rc) {
     return TIO_OK;
 }
 
+// period_interior_duration (analysis.py:86-94) of every period: durations
+// strictly inside it, from the start times — non-wrap: starts[end + 1] -
+// starts[start]; wrap: the tail after the last access plus the head before
+// the first (start = (last + 1) mod N, end = (first - 1) mod N, so a start of
+// 0 means an empty tail and an end of N - 1 an empty head).
+__global__ void k_period_interior(const int64_t *starts, const int32_t *p_start, const int32_t *p_end,
+                                  const int8_t *p_wraps, int64_t P, int64_t N, int64_t *out) {
+    const int64_t I = starts[N];
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = p_start[p], b = p_end[p];
+        if (!p_wraps[p]) {
+            out[p] = starts[b + 1] - starts[a];
+        } else {
+            const int64_t tail = a == 0 ? 0 : I - starts[a];
+            const int64_t first = b == N - 1 ? 0 : b + 1;
+            out[p] = tail + starts[first];
+        }
+    }
+}
+
 }  // namespace tio
 
 using namespace tio;
+
+// Virtual ranks (tio_plan_create_virtual): every rank thread prepares its
+// planner instance with tio_plan_create2 up to the round loop, then hands its
+// PlanArgs to this rendezvous; the last to arrive launches ONE cooperative
+// grid running every instance (launch_plan_loop_multi) after the other ranks'
+// setup work (their streams' ready events), and every rank's stream waits
+// for that grid before its epilogue.
+#include <condition_variable>
+#include <mutex>
+struct VGroup {
+    int nranks = 0, blocks_per_rank = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    bool launched = false;
+    int rc = TIO_OK;
+    std::vector<PlanArgs> args;
+    std::vector<cudaEvent_t> ready;
+    cudaEvent_t done = nullptr;
+    PlanArgs *dev_args = nullptr;
+};
+static thread_local VGroup *t_vgroup = nullptr;
+static thread_local int t_vrank = 0;
+
+static int vgroup_launch(VGroup *g, int rank, const PlanArgs &a, cudaStream_t s) {
+    std::unique_lock<std::mutex> lk(g->m);
+    g->args[rank] = a;
+    cudaEventRecord(g->ready[rank], s);
+    if (++g->arrived == g->nranks) {
+        int rc = TIO_OK;
+        for (int r = 0; r < g->nranks && rc == TIO_OK; ++r)
+            if (cudaStreamWaitEvent(s, g->ready[r], 0) != cudaSuccess) rc = fail(TIO_ERR_CUDA, "virtual ranks: wait");
+        if (rc == TIO_OK &&
+            cudaMemcpyAsync(g->dev_args, g->args.data(), sizeof(PlanArgs) * g->nranks, cudaMemcpyHostToDevice, s) !=
+                cudaSuccess)
+            rc = fail(TIO_ERR_CUDA, "virtual ranks: argument upload");
+        if (rc == TIO_OK) rc = launch_plan_loop_multi(g->dev_args, g->nranks, g->blocks_per_rank, s);
+        if (rc == TIO_OK && cudaEventRecord(g->done, s) != cudaSuccess) rc = fail(TIO_ERR_CUDA, "virtual ranks: record");
+        // the upload reads g->args (pageable): done before the host may reuse it
+        cudaStreamSynchronize(s);
+        g->rc = rc;
+        g->launched = true;
+        g->cv.notify_all();
+    } else {
+        g->cv.wait(lk, [g] { return g->launched; });
+    }
+    if (g->rc != TIO_OK) return g->rc;
+    TIO_CUDA(cudaStreamWaitEvent(s, g->done, 0));
+    return TIO_OK;
+}
 
 struct tio_trace {
     int64_t N = 0, T = 0, E = 0;
@@ -287,6 +357,26 @@ int tio_lifetime_view_get(tio_trace *t, void *stream, tio_lifetime_view *v) {
     v->starts = t->starts; v->timeline = t->timeline; v->active = t->active;
     v->period_tensor = t->p_tensor; v->period_start = t->p_start; v->period_end = t->p_end;
     v->period_wraps = t->p_wraps; v->tensor_period_ptr = t->tpp;
+    return TIO_OK;
+}
+
+int tio_period_interior(tio_trace *t, void *stream, int64_t *out) {
+    if (!t || !out) return fail(TIO_ERR_INVALID, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    TIO_TRY(lifetime_sync(t, s));
+    const int64_t P = t->num_periods;
+    if (P == 0) return TIO_OK;
+    int64_t *d = nullptr;
+    TIO_CUDA(cudaMallocAsync(&d, 8 * P, s));
+    int64_t b = (P + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    k_period_interior<<<(unsigned)b, 256, 0, s>>>(t->starts, t->p_start, t->p_end, t->p_wraps, P, t->N, d);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, 8 * P, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(TIO_ERR_CUDA, "period interior: %s", cudaGetErrorString(e));
     return TIO_OK;
 }
 
@@ -547,7 +637,7 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     PCUDA(cudaEventCreate(&ev0));
     PCUDA(cudaEventCreate(&ev1));
     PCUDA(cudaEventRecord(ev0, s));
-    int loop_rc = launch_plan_loop(a, G, s);
+    int loop_rc = t_vgroup ? vgroup_launch(t_vgroup, t_vrank, a, s) : launch_plan_loop(a, G, s);
     PCUDA(cudaEventRecord(ev1, s));
     if (loop_rc != TIO_OK) { cudaEventDestroy(ev0); cudaEventDestroy(ev1); return bail(loop_rc); }
 
@@ -733,7 +823,9 @@ int tio_mailbox_create(void **mailbox, unsigned char *ipc_handle) {
     void *p = nullptr;
     TIO_CUDA(cudaMalloc(&p, sizeof(Mailbox)));
     cudaIpcMemHandle_t h;
-    if (cudaMemset(p, 0, sizeof(Mailbox)) != cudaSuccess || cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+    // zeroed (legacy stream, then waited for) before any planner stream can use it
+    if (cudaMemset(p, 0, sizeof(Mailbox)) != cudaSuccess || cudaStreamSynchronize(nullptr) != cudaSuccess ||
+        cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
         cudaFree(p);
         return fail(TIO_ERR_CUDA, "mailbox: %s", cudaGetErrorString(cudaGetLastError()));
     }
@@ -767,12 +859,21 @@ int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rat
     if (nranks < 1 || nranks > MAX_RANKS) return fail(TIO_ERR_INVALID, "nranks must be in [1, %d]", MAX_RANKS);
     TIO_TRY(lifetime_sync(t, nullptr));        // shared trace products, before the rank threads start
     int G = 0;
-    TIO_TRY(plan_loop_grid(&G));
+    TIO_TRY(plan_loop_multi_grid(&G));
     int dev = 0;
     TIO_CUDA(cudaGetDevice(&dev));
     Mailbox *mb = nullptr;
     TIO_CUDA(cudaMalloc((void **)&mb, sizeof(Mailbox) * nranks));
     TIO_CUDA(cudaMemset(mb, 0, sizeof(Mailbox) * nranks));
+    TIO_CUDA(cudaDeviceSynchronize());          // zeroed before any rank's stream (non-blocking) runs
+    VGroup grp;
+    grp.nranks = nranks;
+    grp.blocks_per_rank = G / nranks;
+    grp.args.resize(nranks);
+    grp.ready.resize(nranks);
+    for (int r = 0; r < nranks; ++r) TIO_CUDA(cudaEventCreateWithFlags(&grp.ready[r], cudaEventDisableTiming));
+    TIO_CUDA(cudaEventCreateWithFlags(&grp.done, cudaEventDisableTiming));
+    TIO_CUDA(cudaMalloc((void **)&grp.dev_args, sizeof(PlanArgs) * nranks));
     std::vector<void *> peers(nranks);
     for (int r = 0; r < nranks; ++r) peers[r] = mb + r;
     std::vector<int> rcs(nranks, TIO_OK);
@@ -782,6 +883,8 @@ int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rat
         out[r] = nullptr;
         th.emplace_back([&, r]() {
             cudaSetDevice(dev);
+            t_vgroup = &grp;
+            t_vrank = r;
             cudaStream_t s = nullptr;
             if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
                 rcs[r] = fail(TIO_ERR_CUDA, "stream creation failed");
@@ -793,7 +896,7 @@ int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rat
             if (opts) o.max_rounds = opts->max_rounds;
             o.nranks = nranks;
             o.rank = r;
-            o.blocks = G / nranks;
+            o.blocks = grp.blocks_per_rank;
             o.epoch = 0;
             o.mailbox = mb + r;
             o.peer_mailboxes = peers.data();
@@ -810,6 +913,9 @@ int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rat
     }
     for (auto &x : th) x.join();
     cudaFree(mb);
+    cudaFree(grp.dev_args);
+    for (auto e : grp.ready) cudaEventDestroy(e);
+    cudaEventDestroy(grp.done);
     for (int r = 0; r < nranks; ++r)
         if (rcs[r] != TIO_OK) {
             for (int q = 0; q < nranks; ++q) { tio_plan_destroy(out[q]); out[q] = nullptr; }

@@ -50,19 +50,22 @@ __device__ __forceinline__ uint8_t ld_cg(const uint8_t *p) { return (uint8_t)__l
 // the B200: 1.18 us per barrier at 296 blocks (a counter + generation
 // barrier with __threadfence: 2.44 us; tools/micro/barrier_bench.cu).
 // bar[0..1] = the counter (zeroed before the launch).
-__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+// G: the blocks taking part (gridDim.x, or one rank's share of a grid that
+// runs several planner instances).
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned G) {
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long *ctr = reinterpret_cast<unsigned long long *>(bar);
         unsigned long long v;
         asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(v) : "l"(ctr) : "memory");
-        const unsigned long long target = (v / gridDim.x + 1) * gridDim.x;
+        const unsigned long long target = (v / G + 1) * G;
         while (v < target) {
             asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
         }
     }
     __syncthreads();
 }
+__device__ __forceinline__ void grid_barrier(unsigned *bar) { grid_barrier(bar, gridDim.x); }
 
 __device__ __forceinline__ void atomic_add_i64(int64_t *p, int64_t v) {
     atomicAdd(reinterpret_cast<unsigned long long *>(p), (unsigned long long)v);

@@ -37,7 +37,10 @@ namespace tio {
 constexpr int MAXG = 1024;
 // longest wait for the other ranks' round message before a sharded planning
 // call gives up (status 3, TIO_ERR_CUDA "rank exchange timed out")
-constexpr int64_t EXCHANGE_TIMEOUT_NS = 30000000000ll;
+#ifndef TIO_EXCHANGE_TIMEOUT_NS
+#define TIO_EXCHANGE_TIMEOUT_NS 30000000000ll
+#endif
+constexpr int64_t EXCHANGE_TIMEOUT_NS = TIO_EXCHANGE_TIMEOUT_NS;
 
 struct LastCommit {
     int64_t dest;                 // 0 none (first round), 1 SSD, 2 CPU
@@ -509,6 +512,10 @@ __device__ void round_winner(const PlanArgs &a, int64_t round, int G, Key *sm_ke
                     m = best;
                 }
             }
+#ifdef TIO_VDEBUG
+            printf("[vdbg] rank %d/%d round %lld blk %d: winner meta %llx blo %llx\n", a.rank, a.nranks,
+                   (long long)round, (int)blockIdx.x, (unsigned long long)m.k.meta, (unsigned long long)m.k.blo);
+#endif
             msg_store(a.win, m);
             st_release_gpu(a.win_gen, (unsigned long long)round + 1);
         }
@@ -524,8 +531,10 @@ __device__ void round_winner(const PlanArgs &a, int64_t round, int G, Key *sm_ke
 constexpr int DIRTY_MAX = 2048;  // own tiles tested / listed per pass
 constexpr size_t PLAN_DYN_SMEM = 0;
 
-__global__ void __launch_bounds__(PLAN_THREADS)
-plan_loop_kernel(PlanArgs a) {
+// The round loop of one planner instance on G blocks; b = this block's index
+// among them.  plan_loop_kernel runs one instance on the whole grid;
+// plan_loop_kernel_multi runs one instance per virtual rank on its share.
+__device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, const int b) {
     __shared__ int64_t cp_prefix[MAXG + 1];
     __shared__ Key sm_key[33];
     __shared__ WinMsg s_win;
@@ -544,8 +553,6 @@ plan_loop_kernel(PlanArgs a) {
     __shared__ int32_t s_ndirty;
 
     const int64_t N = a.N, I = a.iteration, cap = a.capacity;
-    const int G = gridDim.x;
-    const int b = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int64_t KC = a.chunk;
     const int64_t x0 = (int64_t)b * KC;                       // chunk over x in [0, N]
@@ -609,7 +616,7 @@ plan_loop_kernel(PlanArgs a) {
 #endif
         }
     }
-    grid_barrier(a.bar);
+    grid_barrier(a.bar, G);
 
 #ifdef TIO_PLAN_PROFILE
     // phase profile (block 0, %globaltimer): a debug build only, the timer
@@ -660,6 +667,10 @@ plan_loop_kernel(PlanArgs a) {
             if (threadIdx.x == 0) cp_prefix[nchunks] = v;
         }
         __syncthreads();
+#ifdef TIO_VDEBUG
+        if (threadIdx.x == 0 && (b == 0 || b == G - 1))
+            printf("[vdbg] rank %d blk %d round %lld start: crit %lld\n", a.rank, b, (long long)round, (long long)s_crit);
+#endif
         if (s_crit <= 0 || N == 0) break;   // planner.py:293 peak <= capacity
         if (a.max_rounds > 0 && round >= a.max_rounds) break;
         TICK(0);
@@ -1162,7 +1173,7 @@ plan_loop_kernel(PlanArgs a) {
             ch_par[q0] ^= 1; ch_par[q0 + 1] ^= 1;
             s_win_tile = w.idx / TILE;
         }
-        grid_barrier(a.bar);
+        grid_barrier(a.bar, G);
         TICK(7);
     }
     PROF(if (tb) for (int q = 0; q < 8; ++q) a.scalars[PS_DBG + q] = dbg[q]);
@@ -1171,6 +1182,29 @@ plan_loop_kernel(PlanArgs a) {
 #undef TICK
 #undef PROF
 #undef SUB
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS)
+plan_loop_kernel(PlanArgs a) {
+    plan_loop_body(a, (int)gridDim.x, (int)blockIdx.x);
+}
+
+// Virtual ranks on one GPU (the sharded protocol's check): R planner
+// instances in ONE cooperative grid, blocks [r Gr, (r + 1) Gr) run rank r
+// with its own arguments (staged in shared memory).  Separate cooperative
+// launches are not co-scheduled by the driver — a rank's grid would wait for
+// the other's to finish while that one waits for its messages.
+__global__ void __launch_bounds__(PLAN_THREADS)
+plan_loop_kernel_multi(const PlanArgs *args, int Gr) {
+    __shared__ __align__(16) PlanArgs sa;
+    const int r = (int)blockIdx.x / Gr;
+    {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(args + r);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(&sa);
+        for (int i = threadIdx.x; i < (int)(sizeof(PlanArgs) / 4); i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    plan_loop_body(sa, Gr, (int)blockIdx.x % Gr);
 }
 
 int plan_loop_grid(int *blocks) {
@@ -1186,6 +1220,31 @@ int plan_loop_grid(int *blocks) {
         if (cached > MAXG) cached = MAXG;
     }
     *blocks = cached;
+    return TIO_OK;
+}
+
+int plan_loop_multi_grid(int *blocks) {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0, sms = 0, per_sm = 0;
+        TIO_CUDA(cudaGetDevice(&dev));
+        TIO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        TIO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_loop_kernel_multi, PLAN_THREADS,
+                                                               PLAN_DYN_SMEM));
+        if (per_sm < 1) return fail(TIO_ERR_CUDA, "multi-rank planner kernel cannot be resident");
+        cached = sms * (per_sm < 2 ? per_sm : 2);
+        if (cached > MAXG) cached = MAXG;
+    }
+    *blocks = cached;
+    return TIO_OK;
+}
+
+int launch_plan_loop_multi(const PlanArgs *dev_args, int nranks, int blocks_per_rank, cudaStream_t stream) {
+    int Gr = blocks_per_rank;
+    void *params[] = {const_cast<PlanArgs **>(&dev_args), &Gr};
+    TIO_CUDA(cudaLaunchCooperativeKernel((const void *)plan_loop_kernel_multi, dim3(nranks * blocks_per_rank),
+                                         dim3(PLAN_THREADS), params, PLAN_DYN_SMEM, stream));
+    count_launch();
     return TIO_OK;
 }
 

@@ -117,5 +117,9 @@ struct PlanArgs {
 
 int plan_loop_grid(int *blocks);
 int launch_plan_loop(const PlanArgs &args, int blocks, cudaStream_t stream);
+// one cooperative grid of nranks x blocks_per_rank blocks, rank r running the
+// planner on dev_args[r] (device memory)
+int plan_loop_multi_grid(int *blocks);
+int launch_plan_loop_multi(const PlanArgs *dev_args, int nranks, int blocks_per_rank, cudaStream_t stream);
 
 }  // namespace tio

@@ -350,6 +350,28 @@ def test_characterization_known_answers(ex1):
     assert histogram_csv(rep).splitlines()[0] == "size_class_bytes,duration_class_us,count"
 
 
+def test_period_interior_durations_on_device():
+    """period_interior_duration (reference analysis.py:86-94) of every period
+    from the device kernel (tio_period_interior) equals the one-period host
+    restatement on wrap edge cases (last access in the last kernel, first in
+    kernel 0, single-access globals), random traces and the C1 trace."""
+    import numpy as np
+    from paper_2506_06472_b200 import TransformerGenConfig, gen_random_trace, gen_transformer_trace
+    from paper_2506_06472_b200.analysis import period_interior_duration, period_interior_durations
+    cases = [mk_trace([10, 20, 30, 40, 50], [(0, 7, "global", [1, 2])]),
+             mk_trace([10, 20, 30, 40, 50], [(0, 7, "global", [0, 4]), (1, 5, "global", [4]),
+                                             (2, 6, "global", [0]), (3, 9, "intermediate", [0, 3])]),
+             gen_transformer_trace(TransformerGenConfig(num_layers=2))]
+    cases += [gen_random_trace(s, 20 + s, 15 + s % 9) for s in range(20)]
+    n = 0
+    for tr in cases:
+        dev = period_interior_durations(tr)
+        per = compute_inactive_periods(tr)
+        assert dev.tolist() == [period_interior_duration(p, tr) for p in per]
+        n += len(per)
+    assert n > 500
+
+
 @pytest.mark.parametrize("config", ["c2", "c3"])
 def test_lifetime_vs_reference_itself_at_scale(config):
     """C2 (1.0M events) and C3 (9.9M events) lifetime products against the
