@@ -315,7 +315,11 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     if (threadIdx.x < 32) agg_publish(est, egrp, tile, tot);
 
     // ---- walk 2: per-kernel active bytes and the timeline difference array
+#ifndef LT_NO_REDS          // (timing experiments only: tools/build_variant.sh -DLT_NO_REDS)
     if (!(flags & (LF_ACCESS_RANGE | LF_BAD_PTR))) {
+#else
+    if (false) {
+#endif
 #pragma unroll
         for (int j = 0; j < LT_EPT; ++j) {
             if (j >= nv) break;
@@ -365,6 +369,9 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     }
     // period records, stored coalesced: the staged event and the staged
     // accesses / owner map give the record back
+#ifdef LT_NO_RECORDS
+    return flags;
+#endif
     for (int64_t i = threadIdx.x; i < tot; i += blockDim.x) {
         const int32_t e = sm.rec[i], o = sm.own[e], kk = sm.acc[e];
         const int64_t g = prefix + i;
@@ -535,7 +542,11 @@ int launch_lifetime(const LifetimeArgs &args, cudaStream_t stream) {
     cfg.dynamicSmemBytes = sizeof(EvSmem);
     TIO_CUDA(cudaLaunchKernelEx(&cfg, k_events, args));
     count_launch();
+#ifdef LT_NO_KERNELS
+    if (false) {
+#else
     if (NTk > 0) {
+#endif
         cfg.gridDim = dim3((unsigned)NTk);
         cfg.blockDim = dim3(KT_THREADS);
         cfg.dynamicSmemBytes = 0;

@@ -3,7 +3,9 @@ step of a randomly initialised Llama-3-8B on one B200 — the step the
 migration engine offloads.
 
   * model: Llama-3 architecture (RMSNorm, RoPE theta 5e5, GQA attention with
-    8 KV heads via scaled_dot_product_attention, SwiGLU FFN, untied LM head);
+    8 KV heads — FlashAttention-2 with its deterministic backward, so a rerun
+    of the same steps is bit-identical; SDPA when flash_attn is absent —
+    SwiGLU FFN, untied LM head);
     Llama-3-8B = 32 layers, hidden 4096, FFN 14336, vocab 128,256;
   * weights bf16, `torch.manual_seed(seed)` random init (no checkpoint: no
     network), gradients bf16, AdamW moments fp32 (allocated up front, as in
@@ -27,6 +29,11 @@ import torch
 import torch.nn.functional as F
 from torch import nn
 
+try:                                     # FlashAttention-2 (library kernels: plumbing of the workload)
+    from flash_attn import flash_attn_func as _flash_attn_func
+except Exception:                        # pragma: no cover - absent in some images
+    _flash_attn_func = None
+
 
 @dataclass(frozen=True)
 class LlamaConfig:
@@ -39,6 +46,7 @@ class LlamaConfig:
     rope_theta: float = 500_000.0
     eps: float = 1e-5
     seq: int = 8192
+    deterministic: bool = True     # run-to-run identical kernels (deterministic attention backward)
 
     @property
     def head_dim(self) -> int:
@@ -135,8 +143,16 @@ class Block(nn.Module):
         k = self.wk(h).view(B, S, c.kv_heads, c.head_dim).transpose(1, 2)
         v = self.wv(h).view(B, S, c.kv_heads, c.head_dim).transpose(1, 2)
         q, k = _rope(q, cos, sin), _rope(k, cos, sin)
-        o = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
-        x = x + self.wo(o.transpose(1, 2).reshape(B, S, c.dim))
+        if c.deterministic and _flash_attn_func is not None and q.is_cuda:
+            # FlashAttention-2 with its deterministic backward (no atomic dq
+            # accumulation): the no-offload and offloaded steps are then
+            # bit-comparable; layout (B, S, H, D), GQA native
+            o = _flash_attn_func(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), causal=True,
+                                 deterministic=True)
+            x = x + self.wo(o.reshape(B, S, c.dim))
+        else:
+            o = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+            x = x + self.wo(o.transpose(1, 2).reshape(B, S, c.dim))
         h2 = self.ffn_norm(x)
         return x + self.w2(_SwiGLUFn.apply(self.w1(h2), self.w3(h2)))
 

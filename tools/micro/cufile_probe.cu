@@ -38,7 +38,9 @@ int main(int argc, char **argv) {
     const size_t SZ = (argc > 2) ? (size_t)atoll(argv[2]) << 20 : (size_t)1 << 30;
     const char *path = argc > 1 ? argv[1] : "/tmp/tio_cufile_probe.bin";
     std::string out = "{\"path\": \"" + std::string(path) + "\", \"bytes\": " + std::to_string(SZ);
+    fprintf(stderr, "[cufile_probe] driver open...\n");
     CUfileError_t st = cuFileDriverOpen();
+    fprintf(stderr, "[cufile_probe] driver open rc %d\n", (int)st.err);
     out += ", \"driver_open\": " + std::to_string((int)st.err);
     CUfileDrvProps_t props;
     memset(&props, 0, sizeof(props));
@@ -64,7 +66,9 @@ int main(int argc, char **argv) {
     d.handle.fd = fd;
     d.type = CU_FILE_HANDLE_TYPE_OPAQUE_FD;
     CUfileHandle_t fh;
+    fprintf(stderr, "[cufile_probe] handle register (o_direct %d)...\n", (int)direct);
     st = cuFileHandleRegister(&fh, &d);
+    fprintf(stderr, "[cufile_probe] handle register rc %d\n", (int)st.err);
     out += ", \"handle_register\": " + std::to_string((int)st.err);
     if (st.err != CU_FILE_SUCCESS) {
         printf("%s}\n", out.c_str());
@@ -88,6 +92,7 @@ int main(int argc, char **argv) {
     double bw = 1e30, br = 1e30;
     ssize_t wr = 0, rd = 0;
     for (int r = 0; r < 3; ++r) {
+        fprintf(stderr, "[cufile_probe] sync write/read %d...\n", r);
         double t0 = now();
         wr = cuFileWrite(fh, a, SZ, 0, 0);
         fsync(fd);
@@ -107,6 +112,7 @@ int main(int argc, char **argv) {
     // stream-ordered API
     cudaStream_t s;
     cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    fprintf(stderr, "[cufile_probe] stream API...\n");
     const CUfileError_t rs = cuFileStreamRegister((CUstream)s, 15);
     size_t size = SZ;
     off_t foff = 0, boff = 0;

@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import ncu_lines  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SO = os.path.join(ROOT, "paper_2506_06472_b200", "_lib", "libtio.so")
+SO = os.environ.get("TIO_LIB_PATH") or os.path.join(ROOT, "paper_2506_06472_b200", "_lib", "libtio.so")
 DETAILS = ["Memory Throughput", "DRAM Throughput", "Duration", "L1/TEX Cache Throughput", "L2 Cache Throughput",
            "Compute (SM) Throughput", "Executed Ipc Active", "L2 Hit Rate", "Warp Cycles Per Issued Instruction",
            "Executed Instructions", "Block Size", "Grid Size", "Registers Per Thread",
