@@ -561,7 +561,8 @@ def migration_bench(microbatches: int = 8, verify: bool = True, link: dict | Non
     }
 
 
-def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = None, model: str = "8b") -> dict:
+def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = None, model: str = "8b",
+                    identity_frac: float = 0.8, identity_steps: int = 2) -> dict:
     """Configs C4 (BASELINE.json configs[3]): the migration engine executing
     the plan of a REAL Llama-3-8B training step on 1 B200 (random init bf16
     weights, fp32 AdamW moments, synthetic 8,192-token batch;
@@ -575,17 +576,25 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
     run     fresh model, same step sequence, OffloadMode (libtio online
             engine: storages freed / restored on side streams, event gated).
 
-    Each timed step (K back to back, CUDA events on the compute stream, the
-    last step fenced on every transfer) includes the batch H2D from pinned
-    host and the loss D2H.  Checked: losses and the checksum of every weight /
-    moment after the timed steps equal the ideal run's; one verification step
-    (checksum of every tensor at offload and after prefetch) before timing."""
+    Timing runs use the model's fast attention (cuDNN / flash SDPA, whose
+    backward is not run-to-run deterministic).  Each timed step (K back to
+    back, CUDA events on the compute stream, the last step fenced on every
+    transfer) includes the batch H2D from pinned host and the loss D2H.  One
+    verification step (checksum of every tensor at offload and after its
+    prefetch) precedes the timed steps.
+
+    identity: the same sequence on the deterministic model
+    (FlashAttention-2 deterministic backward; run-to-run bit-identical) at
+    capacity identity_frac x peak: losses and the checksum of every weight /
+    AdamW moment after the offloaded steps must EQUAL the no-offload run's."""
+    import dataclasses
     import gc
     import torch
     from paper_2506_06472_b200 import ChannelRates, compute_memory_timeline, engine, plan_migrations
     from paper_2506_06472_b200.llama_step import LLAMA3_8B_MODEL, TINY, Step
     from paper_2506_06472_b200.profiler import profile_step
-    cfg = LLAMA3_8B_MODEL if model == "8b" else TINY
+    cfg_det = LLAMA3_8B_MODEL if model == "8b" else TINY
+    cfg = dataclasses.replace(cfg_det, deterministic=False)
     dev = torch.device("cuda")
     link = link or engine.measure_link()
     rate = float(int(link["bidir_gbs_each"] * 1e3))            # bytes/us, integral
@@ -625,23 +634,43 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
     def log(msg):
         print(f"[c4] {msg}  (allocated {torch.cuda.memory_allocated() / 1e9:.1f} GB)", file=sys.stderr, flush=True)
 
-    # ---- ideal: plain PyTorch, capacity unconstrained
+    def ideal_run(c, n):
+        s = Step(c, seed=0)
+        for _ in range(3):
+            s()
+        ms, losses, peak = run(s, n)
+        dg = digest(s)
+        return ms, losses, peak, dg
+
+    def offloaded(c, tr, frac, n, peak):
+        """steps 1 (plain) + 2 (profiled, done by the caller or here) + 3
+        (verification) + n timed: the same step count as ideal_run."""
+        cap = int(peak * frac)
+        t0 = time.perf_counter()
+        plan = plan_migrations(tr, cap, rates)
+        t_plan = time.perf_counter() - t0
+        s = Step(c, seed=0)
+        for _ in range(2):
+            s()
+        mode = engine.OffloadMode(tr, plan, cap, rates, s.globals_of(), verify=True)
+        with mode.step():                      # step 3: sets up the steady state, checksums every round trip
+            s()
+        torch.cuda.synchronize()
+        vst = mode.stats()
+        mode.set_verify(False)
+        ms, losses, apeak = run(s, n, mode)
+        st = mode.stats()
+        mode.restore()                         # globals offloaded at the step boundary come back
+        dg = digest(s)
+        info = mode.info
+        mode.close()
+        return cap, plan, t_plan, vst, ms, losses, apeak, st, dg, info
+
+    # ---- ideal: plain PyTorch, capacity unconstrained (+ the model's own spread)
     log("ideal run")
-    s = Step(cfg, seed=0)
-    for _ in range(3):
-        s()
-    ideal_ms, ideal_losses, ideal_peak = run(s, steps)
-    ideal_digest = digest(s)
-    s = None
+    ideal_ms, ideal_losses, ideal_peak, ideal_digest = ideal_run(cfg, steps)
     free()
-    # the model's own run-to-run spread (cuDNN's SDPA backward accumulates dq
-    # with atomics at this size): a second plain run of the same sequence
-    s = Step(cfg, seed=0)
-    for _ in range(3):
-        s()
-    _, rerun_losses, _ = run(s, steps)
-    rerun_digest = digest(s)
-    s = None
+    _, rerun_losses, _, rerun_digest = ideal_run(cfg, steps)
     free()
 
     # ---- profile (step 2 of a fresh model) -> trace
@@ -651,6 +680,8 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
     t0 = time.perf_counter()
     tr = profile_step(s, globals_=s.globals_of(), meta={"generator": "TraceProfiler", "model": f"llama3-{model}"})
     t_prof = time.perf_counter() - t0
+    s = None
+    free()
     a = tr.arrays()
     peak = compute_memory_timeline(tr).peak()
     out = {"workload": f"Llama-3-{model.upper()} real training step (random init bf16 weights, fp32 AdamW, "
@@ -659,32 +690,14 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
            "link": link, "plan_rates_bytes_per_us": rate,
            "ideal": {"step_ms": ideal_ms, "allocator_peak_bytes": ideal_peak, "losses": ideal_losses,
                      "rerun_losses": rerun_losses, "rerun_state_checksums_equal": rerun_digest == ideal_digest,
-                     "deterministic": rerun_losses == ideal_losses and rerun_digest == ideal_digest},
+                     "deterministic": rerun_losses == ideal_losses and rerun_digest == ideal_digest,
+                     "attention": "SDPA (cuDNN / flash; backward not run-to-run deterministic)"},
            "profile_s": t_prof, "runs": []}
-    first = True
     log(f"trace: {a.num_kernels} kernels, {a.num_tensors} tensors, peak {peak / 1e9:.1f} GB ({t_prof:.1f} s)")
     for frac in fracs:
-        cap = int(peak * frac)
         log(f"capacity {frac} x peak")
-        t0 = time.perf_counter()
-        plan = plan_migrations(tr, cap, rates)
-        t_plan = time.perf_counter() - t0
-        if not first:
-            s = Step(cfg, seed=0)
-            for _ in range(2):
-                s()
-        first = False
-        mode = engine.OffloadMode(tr, plan, cap, rates, s.globals_of(), verify=True)
-        with mode.step():                      # step 3: sets up the steady state, checksums every round trip
-            s()
-        torch.cuda.synchronize()
-        vst = mode.stats()
-        mode.set_verify(False)
-        ms, losses, apeak = run(s, steps, mode)
-        st = mode.stats()
-        mode.restore()                         # globals offloaded at the step boundary come back
-        dg = digest(s)
-        info = mode.info
+        cap, plan, t_plan, vst, ms, losses, apeak, st, dg, info = offloaded(cfg, tr, frac, steps, peak)
+        free()
         off_gbs = st["last_offload_bytes"] / (st["last_offload_busy_ms"] * 1e6) if st["last_offload_busy_ms"] else 0.0
         pre_gbs = st["last_prefetch_bytes"] / (st["last_prefetch_busy_ms"] * 1e6) if st["last_prefetch_busy_ms"] else 0.0
         per_step_off = st["offload_bytes"] / max(1, st["steps"])
@@ -706,17 +719,37 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
             "transfers_per_step": {"offloads": info["model_offloads"], "prefetches": info["model_prefetches"],
                                    "emergency": info["emergency_offloads"]},
             "verify": {"round_trips_checked": vst["n_prefetches"], "mismatches": vst["verify_mismatches"]},
-            "losses": losses, "losses_equal_ideal": losses == ideal_losses,
-            "max_loss_dev_vs_ideal": max(abs(x - y) for x, y in zip(losses, ideal_losses)),
+            "losses": losses, "max_loss_dev_vs_ideal": max(abs(x - y) for x, y in zip(losses, ideal_losses)),
             "ideal_rerun_max_loss_dev": max(abs(x - y) for x, y in zip(rerun_losses, ideal_losses)),
-            "state_checksums_equal_ideal": dg == ideal_digest,
         })
-        mode.close()
-        mode = None
+        log(f"capacity {frac}: {ms:.1f} ms/step ({ms / ideal_ms:.2f}x ideal), allocator peak {apeak / 1e9:.1f} GB")
+
+    # ---- byte identity on the deterministic model
+    if identity_frac:
+        log(f"identity leg: deterministic model, capacity {identity_frac} x peak")
+        d_ms, d_losses, _, d_digest = ideal_run(cfg_det, identity_steps)
+        free()
+        s = Step(cfg_det, seed=0)
+        s()
+        trd = profile_step(s, globals_=s.globals_of(), meta={"generator": "TraceProfiler",
+                                                              "model": f"llama3-{model}-deterministic"})
         s = None
         free()
-        log(f"capacity {frac}: {ms:.1f} ms/step ({ms / ideal_ms:.2f}x ideal), allocator peak {apeak / 1e9:.1f} GB")
-    out["tier"] = "pinned host extents (4 KB aligned) via cudaMemcpyAsync on per-channel side streams"
+        peak_d = compute_memory_timeline(trd).peak()
+        cap, plan, _, vst, ms, losses, apeak, st, dg, info = offloaded(cfg_det, trd, identity_frac, identity_steps,
+                                                                       peak_d)
+        free()
+        out["identity"] = {
+            "model": "deterministic attention (FlashAttention-2, deterministic backward)",
+            "capacity_frac_of_trace_peak": identity_frac, "capacity": cap, "steps_compared": identity_steps,
+            "ideal_step_ms": d_ms, "offloaded_step_ms": ms, "step_vs_ideal": ms / d_ms,
+            "offloaded_bytes_per_step": st["offload_bytes"] / max(1, st["steps"]),
+            "verify_mismatches": vst["verify_mismatches"],
+            "losses_ideal": d_losses, "losses_offloaded": losses, "losses_equal": losses == d_losses,
+            "state_checksums_equal": dg == d_digest, "tensors_compared": len(dg)}
+        log(f"identity: losses equal {losses == d_losses}, state equal {dg == d_digest}")
+    out["tier"] = "pinned host extents (4 KB aligned) via cudaMemcpyAsync on per-channel side streams " \
+                  "(cuFile: cuFileDriverOpen blocks on the GPU boxes, profiles/r09/cufile_probe.txt)"
     return out
 
 

@@ -578,7 +578,8 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     a.ntiles = ntiles; a.tcand = tcand; a.t_lo = t_lo; a.t_hi = t_hi;
     a.t_ka_lo = t_ka_lo; a.t_ka_hi = t_ka_hi; a.t_kb_lo = t_kb_lo; a.t_kb_hi = t_kb_hi; a.tile_best = tile_best;
     int G = 0;
-    PTRY(plan_loop_grid(&G));
+    const bool wide = !t_vgroup && plan_loop_wide(ntiles);
+    PTRY(plan_loop_grid(&G, wide));
     if (opts && opts->blocks > 0 && opts->blocks < G) G = opts->blocks;
     const int nranks = opts && opts->nranks > 1 ? opts->nranks : 1;
     if (nranks > MAX_RANKS) return bail(fail(TIO_ERR_INVALID, "at most %d ranks", MAX_RANKS));
@@ -637,7 +638,7 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     PCUDA(cudaEventCreate(&ev0));
     PCUDA(cudaEventCreate(&ev1));
     PCUDA(cudaEventRecord(ev0, s));
-    int loop_rc = t_vgroup ? vgroup_launch(t_vgroup, t_vrank, a, s) : launch_plan_loop(a, G, s);
+    int loop_rc = t_vgroup ? vgroup_launch(t_vgroup, t_vrank, a, s) : launch_plan_loop(a, G, s, wide);
     PCUDA(cudaEventRecord(ev1, s));
     if (loop_rc != TIO_OK) { cudaEventDestroy(ev0); cudaEventDestroy(ev1); return bail(loop_rc); }
 

@@ -436,6 +436,8 @@ k_kernels(LifetimeArgs a) {
     const int64_t NTe = lifetime_event_tiles(E), NTk = lifetime_kernel_tiles(N);
     const LtWork w = lt_work(a.work, N, E);                     // dur chain, then diff chain
     if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(a.work + 1), 1ull);
+    // the globals' bytes (k_events' sum) load early, beside the tile's loads
+    const int64_t gbytes = __ldcg(reinterpret_cast<const long long *>(&a.scalars[SC_GLOBAL_BYTES]));
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= NTk) return;
@@ -478,7 +480,7 @@ k_kernels(LifetimeArgs a) {
     }
     __syncthreads();
     xd += s_pre[0];
-    xf += s_pre[1] + __ldcg(reinterpret_cast<const long long *>(&a.scalars[SC_GLOBAL_BYTES]));
+    xf += s_pre[1] + gbytes;
     if (k0 + KT_EPT <= N && vec) {
         longlong2 *ps = reinterpret_cast<longlong2 *>(a.starts + k0);
         longlong2 *pt = reinterpret_cast<longlong2 *>(a.timeline + k0);

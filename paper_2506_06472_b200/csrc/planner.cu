@@ -1184,8 +1184,24 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
 #undef SUB
 }
 
-__global__ void __launch_bounds__(PLAN_THREADS)
+#ifndef TIO_PLAN_MINB
+#define TIO_PLAN_MINB 2       // blocks per SM the register allocation must allow (build knob)
+#endif
+#ifndef TIO_PLAN_MAX_PER_SM
+#define TIO_PLAN_MAX_PER_SM 2 // resident planner blocks per SM used (build knob)
+#endif
+__global__ void __launch_bounds__(PLAN_THREADS, TIO_PLAN_MINB)
 plan_loop_kernel(PlanArgs a) {
+    plan_loop_body(a, (int)gridDim.x, (int)blockIdx.x);
+}
+
+// The wide form: registers capped for 3 resident blocks per SM (80 registers,
+// a small spill to L1) — 1.5x the warps for the dirty-tile and refit phases.
+// Measured (tools/micro/plvar.sh): C3 (150K tiles) 59.2 -> 55.9 us/round,
+// C2 (15K tiles) 22.6 -> 23.9 (more blocks in every barrier and reduction
+// for little phase-E work), so it is chosen by tile count.
+__global__ void __launch_bounds__(PLAN_THREADS, 3)
+plan_loop_kernel_wide(PlanArgs a) {
     plan_loop_body(a, (int)gridDim.x, (int)blockIdx.x);
 }
 
@@ -1194,7 +1210,7 @@ plan_loop_kernel(PlanArgs a) {
 // with its own arguments (staged in shared memory).  Separate cooperative
 // launches are not co-scheduled by the driver — a rank's grid would wait for
 // the other's to finish while that one waits for its messages.
-__global__ void __launch_bounds__(PLAN_THREADS)
+__global__ void __launch_bounds__(PLAN_THREADS, TIO_PLAN_MINB)
 plan_loop_kernel_multi(const PlanArgs *args, int Gr) {
     __shared__ __align__(16) PlanArgs sa;
     const int r = (int)blockIdx.x / Gr;
@@ -1207,19 +1223,31 @@ plan_loop_kernel_multi(const PlanArgs *args, int Gr) {
     plan_loop_body(sa, Gr, (int)blockIdx.x % Gr);
 }
 
-int plan_loop_grid(int *blocks) {
-    static int cached = 0;
-    if (!cached) {
+bool plan_loop_wide(int64_t ntiles) {
+    static int64_t thresh = -1;
+    if (thresh < 0) {
+        const char *e = getenv("TIO_PLAN_WIDE_TILES");
+        thresh = e ? atoll(e) : 60000;
+    }
+    return thresh > 0 && ntiles >= thresh;
+}
+
+int plan_loop_grid(int *blocks, bool wide) {
+    static int cached[2] = {0, 0};
+    int &c = cached[wide ? 1 : 0];
+    if (!c) {
         int dev = 0, sms = 0, per_sm = 0;
+        const void *fn = wide ? (const void *)plan_loop_kernel_wide : (const void *)plan_loop_kernel;
         TIO_CUDA(cudaGetDevice(&dev));
         TIO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        TIO_CUDA(cudaFuncSetAttribute(plan_loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DYN_SMEM));
-        TIO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_loop_kernel, PLAN_THREADS, PLAN_DYN_SMEM));
+        TIO_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLAN_DYN_SMEM));
+        TIO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PLAN_THREADS, PLAN_DYN_SMEM));
         if (per_sm < 1) return fail(TIO_ERR_CUDA, "planner kernel cannot be resident");
-        cached = sms * (per_sm < 2 ? per_sm : 2);
-        if (cached > MAXG) cached = MAXG;
+        const int cap = wide ? 3 : TIO_PLAN_MAX_PER_SM;
+        c = sms * (per_sm < cap ? per_sm : cap);
+        if (c > MAXG) c = MAXG;
     }
-    *blocks = cached;
+    *blocks = c;
     return TIO_OK;
 }
 
@@ -1232,7 +1260,7 @@ int plan_loop_multi_grid(int *blocks) {
         TIO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_loop_kernel_multi, PLAN_THREADS,
                                                                PLAN_DYN_SMEM));
         if (per_sm < 1) return fail(TIO_ERR_CUDA, "multi-rank planner kernel cannot be resident");
-        cached = sms * (per_sm < 2 ? per_sm : 2);
+        cached = sms * (per_sm < TIO_PLAN_MAX_PER_SM ? per_sm : TIO_PLAN_MAX_PER_SM);
         if (cached > MAXG) cached = MAXG;
     }
     *blocks = cached;
@@ -1248,9 +1276,10 @@ int launch_plan_loop_multi(const PlanArgs *dev_args, int nranks, int blocks_per_
     return TIO_OK;
 }
 
-int launch_plan_loop(const PlanArgs &args, int blocks, cudaStream_t stream) {
+int launch_plan_loop(const PlanArgs &args, int blocks, cudaStream_t stream, bool wide) {
     void *params[] = {const_cast<PlanArgs *>(&args)};
-    TIO_CUDA(cudaLaunchCooperativeKernel((const void *)plan_loop_kernel, dim3(blocks), dim3(PLAN_THREADS),
+    TIO_CUDA(cudaLaunchCooperativeKernel(wide ? (const void *)plan_loop_kernel_wide : (const void *)plan_loop_kernel,
+                                         dim3(blocks), dim3(PLAN_THREADS),
                                          params, PLAN_DYN_SMEM, stream));
     count_launch();
     return TIO_OK;

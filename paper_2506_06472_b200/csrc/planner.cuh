@@ -115,8 +115,11 @@ struct PlanArgs {
     Mailbox *mb_peer[MAX_RANKS];   // every rank's mailbox as mapped here (mb_peer[rank] == mb_self)
 };
 
-int plan_loop_grid(int *blocks);
-int launch_plan_loop(const PlanArgs &args, int blocks, cudaStream_t stream);
+// the wide form (3 blocks per SM) for large candidate sets (env
+// TIO_PLAN_WIDE_TILES: tile threshold, default 60000; 0 = never)
+bool plan_loop_wide(int64_t ntiles);
+int plan_loop_grid(int *blocks, bool wide = false);
+int launch_plan_loop(const PlanArgs &args, int blocks, cudaStream_t stream, bool wide = false);
 // one cooperative grid of nranks x blocks_per_rank blocks, rank r running the
 // planner on dev_args[r] (device memory)
 int plan_loop_multi_grid(int *blocks);
