@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -206,6 +207,48 @@ __global__ void k_copy_rest(const PackSeg *segs, int nseg) {
     }
 }
 
+// Segment tables go to the device through a ring of pinned host slots: a
+// slot is reused only once the copy that read it has completed (its event,
+// normally long done), so a pack call never waits for its stream.
+struct PinnedRing {
+    static constexpr int SLOTS = 8;
+    std::mutex m;
+    uint8_t *buf[SLOTS] = {};
+    size_t cap[SLOTS] = {};
+    cudaEvent_t ev[SLOTS] = {};
+    int next = 0;
+};
+static PinnedRing g_ring;
+
+static int ring_upload(const void *data, size_t n, void *dst, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_ring.m);
+    const int k = g_ring.next;
+    g_ring.next = (k + 1) % PinnedRing::SLOTS;
+    if (g_ring.ev[k]) TIO_CUDA(cudaEventSynchronize(g_ring.ev[k]));
+    else TIO_CUDA(cudaEventCreateWithFlags(&g_ring.ev[k], cudaEventDisableTiming));
+    if (g_ring.cap[k] < n) {
+        if (g_ring.buf[k]) TIO_CUDA(cudaFreeHost(g_ring.buf[k]));
+        const size_t c = n > (64u << 10) ? n : (64u << 10);
+        TIO_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&g_ring.buf[k]), c, cudaHostAllocDefault));
+        g_ring.cap[k] = c;
+    }
+    memcpy(g_ring.buf[k], data, n);
+    TIO_CUDA(cudaMemcpyAsync(dst, g_ring.buf[k], n, cudaMemcpyHostToDevice, s));
+    TIO_CUDA(cudaEventRecord(g_ring.ev[k], s));
+    return TIO_OK;
+}
+
+static int pack_attr() {
+    static std::once_flag once;
+    static int rc = TIO_OK;
+    std::call_once(once, [] {
+        if (cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, PACK_STAGES * PACK_CHUNK) !=
+            cudaSuccess)
+            rc = fail(TIO_ERR_CUDA, "k_pack: shared memory attribute");
+    });
+    return rc;
+}
+
 static int launch_pack(const std::vector<PackSeg> &segs, cudaStream_t s, void *scratch, size_t scratch_bytes) {
     if (segs.empty()) return TIO_OK;
     const int nseg = (int)segs.size();
@@ -226,14 +269,9 @@ static int launch_pack(const std::vector<PackSeg> &segs, cudaStream_t s, void *s
     memcpy(blob.data(), segs.data(), sizeof(PackSeg) * nseg);
     if (ntma) memcpy(blob.data() + sizeof(PackSeg) * nseg, tma.data(), sizeof(PackSeg) * ntma);
     memcpy(blob.data() + sizeof(PackSeg) * (nseg + ntma), cp.data(), sizeof(int64_t) * (ntma + 1));
-    TIO_CUDA(cudaMemcpyAsync(scratch, blob.data(), need, cudaMemcpyHostToDevice, s));
-    TIO_CUDA(cudaStreamSynchronize(s));     // blob is pageable host memory
-    static bool attr = false;
+    TIO_TRY(ring_upload(blob.data(), need, scratch, s));
+    TIO_TRY(pack_attr());
     const int smem = PACK_STAGES * PACK_CHUNK;
-    if (!attr) {
-        TIO_CUDA(cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
