@@ -333,16 +333,16 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
         th = ctypes.c_void_p()
         _native.check(lib.tio_trace_create(ctypes.byref(desc_c), _native.TIO_MEM_HOST, ctypes.c_void_p(sh),
                                            ctypes.byref(th)))
+        pdt = _native.DeviceTrace.__new__(_native.DeviceTrace)      # owns th from here on
+        pdt._lib, pdt.handle, pdt.stream = lib, th, ctypes.c_void_p(sh)
+        pdt.num_kernels, pdt.num_tensors = N, T
         try:
-            pdt = _native.DeviceTrace.__new__(_native.DeviceTrace)
-            pdt._lib, pdt.handle, pdt.stream = lib, th, ctypes.c_void_p(sh)
-            pdt.num_kernels, pdt.num_tensors = N, T
             p = group.plan(pdt, cap, r, hc)
             _native.check(lib.tio_plan_copy_out(p.handle, ctypes.c_void_p(sh), None,
                                                 ctypes.c_void_p(ent.data_ptr()), None, None))
             p.close()
         finally:
-            lib.tio_trace_destroy(th)
+            pdt.close()
     for _ in range(2):
         one_shot()
     e2e_ms = 0.0
@@ -782,6 +782,11 @@ def main(argv=None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # testing the multi-process path on ONE GPU: TIO_BENCH_ONE_GPU=1 puts every
+    # rank on cuda:0 and uses gloo (NCCL refuses two ranks on one device)
+    one_gpu = os.environ.get("TIO_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local_rank = 0
     if args.impl == "reference":
         if args.ref_rounds_total is None:
             args.ref_rounds_total = _known_rounds(args.config)
@@ -795,7 +800,10 @@ def main(argv=None):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -1,7 +1,9 @@
 """k_pack (the engine's TMA gather into 4 KB-aligned staging extents,
 csrc/engine.cu) against the HBM roofline: 2 x bytes (read + write) over the
-CUDA-event time, best of 10, vs MEASURED_PEAKS.json hbm_gbs; beside it one
-cudaMemcpyAsync D2D per tensor (the alternative).  One JSON line per case."""
+CUDA-event time (device work only: a spin kernel ahead of the timed region
+covers the host's enqueue), best of 10, vs MEASURED_PEAKS.json hbm_gbs;
+beside it one cudaMemcpyAsync D2D per tensor (the alternative).  One JSON
+line per case."""
 import json
 import os
 import sys
@@ -23,6 +25,9 @@ def main():
         for _ in range(10):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
+            # a ~2 ms spin first, so the host finishes enqueueing the pack
+            # before the GPU reaches it: the events then time the device work
+            torch.cuda._sleep(4_000_000)
             e0.record(s)
             offs = engine.pack(ts, staging, stream=s.cuda_stream)
             e1.record(s)
@@ -33,6 +38,7 @@ def main():
         for _ in range(5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
+            torch.cuda._sleep(40_000_000)
             e0.record(s)
             for o, t in zip(offs, ts):
                 staging[o:o + size].copy_(t)
