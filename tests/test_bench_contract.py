@@ -52,3 +52,33 @@ def test_our_arm_line_on_gpu():
         rec = json.load(f)[0]
     if rec.get("capacity") == d["config"]["capacity"]:
         assert d["config"]["plan_sha256"] == hashlib.sha256(rec["plan"].encode()).hexdigest()
+
+
+@pytest.mark.gpu
+def test_two_rank_line_on_one_gpu():
+    """The N > 1 path (torchrun, one process per rank, sharded planner over
+    CUDA-IPC mailboxes, device-resident sharded lifetime) with both ranks on
+    cuda:0 (TIO_BENCH_ONE_GPU: gloo instead of NCCL): strong scaling of ONE
+    trace, every rank's plan equal to the reference's llama1 plan."""
+    import gzip
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ, TIO_BENCH_ONE_GPU="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "llama1", "--secondary", "c1",
+                          "--no-migration"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert BASE_KEYS <= set(d) and d["n_gpus"] == 2 and d["scaling"] == "strong"
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "llama1.json.gz"), "rt") as f:
+        rec = json.load(f)
+    rec = rec[0] if isinstance(rec, list) else rec
+    assert d["config"]["plan_sha256"] == rec["plan_sha256"]
+    assert d["config"]["plan_sha256_equal_on_all_ranks"] is True
+    assert d["sharded_lifetime"]["bit_exact_vs_unsharded"] is True
