@@ -426,7 +426,8 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
                             [round(info.dbg[q] / 1e3 / max(1, rounds), 3) for q in range(8)])),
                         "dirty_tiles_per_round": info.dbg[8] / max(1, rounds),
                         "refits_per_round": info.dbg[9] / max(1, rounds),
-                        "max_block_phase_E_us_per_round": info.dbg[10] / 1e3 / max(1, rounds)}}
+                        "max_block_phase_E_us_per_round": info.dbg[10] / 1e3 / max(1, rounds),
+                        "max_block_dirty_tiles_per_round": info.dbg[13] / max(1, rounds)}}
                        if any(info.dbg[q] for q in range(12)) else {})},
         "e2e": {"value": E * K / (e2e_ms / 1e3), "unit": "events/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,

@@ -903,6 +903,8 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
             const int nd = s_ndirty;
             if (nd) any_dirty = true;
             PROF(if (nd && threadIdx.x == 0) atomic_add_i64(&a.scalars[PS_DBG + 8], nd));
+            PROF(if (nd && threadIdx.x == 0)       // the most dirty tiles any block had this round
+                     atomicMax(reinterpret_cast<long long *>(&a.scalars[PS_DBG + 14]), (long long)nd));
             // one warp per dirty tile, one lane per candidate
             for (int di = warp; di < nd; di += nwarps) {
                 if (di + nwarps < nd) {
