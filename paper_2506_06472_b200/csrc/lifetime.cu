@@ -42,7 +42,13 @@ constexpr int LT_MAXO = LT_TILE + 2;                // staged tensors per tile
 #ifndef KT_THREADS
 #define KT_THREADS 256
 #endif
-constexpr int KT_EPT = 8;                           // kernels per thread
+#ifndef KT_EPT_
+#define KT_EPT_ 8
+#endif
+#ifndef KT_MINB
+#define KT_MINB (1024 / KT_THREADS)
+#endif
+constexpr int KT_EPT = KT_EPT_;                     // kernels per thread
 constexpr int KT_TILE = KT_THREADS * KT_EPT;
 
 __host__ __device__ int64_t lifetime_event_tiles(int64_t E) { return (E + LT_TILE - 1) / LT_TILE; }
@@ -426,7 +432,7 @@ k_events(LifetimeArgs a) {
 }
 
 // ---------------------------------------------------------------- kernels
-__global__ void __launch_bounds__(KT_THREADS, 1024 / KT_THREADS)
+__global__ void __launch_bounds__(KT_THREADS, KT_MINB)
 k_kernels(LifetimeArgs a) {
     asm volatile("griddepcontrol.wait;" ::: "memory");      // k_events complete (programmatic launch)
     __shared__ int64_t scan[40];

@@ -52,7 +52,9 @@ def main(config: str = "c2"):
         "planned_host_bytes": int(p["planned_host_bytes"]),
         "oracle_seconds": round(time.time() - t0, 1), "oracle_threads": int(O.lib().tio_oracle_threads()),
     }
-    with gzip.open(os.path.join(HERE, f"{config}.json.gz"), "wt") as f:
+    out_dir = os.environ.get("TIO_GOLDEN_OUT", HERE)       # e.g. gpurun_out/ when run on the GPU box's host
+    os.makedirs(out_dir, exist_ok=True)
+    with gzip.open(os.path.join(out_dir, f"{config}.json.gz"), "wt") as f:
         json.dump(rec, f)
     print(rec)
 
