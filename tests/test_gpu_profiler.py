@@ -50,3 +50,52 @@ def test_profiled_llama_step_is_a_valid_trace_and_plans():
     plan = plan_migrations(tr, int(peak * 0.7), rates)
     rep = simulate(tr, plan, int(peak * 0.7), rates)
     assert rep.total_time >= rep.ideal_time > 0
+
+
+def test_collective_tensors_are_active_in_the_trace():
+    """tensors used by inter-GPU communication must be
+    active while the collective runs.  A data-parallel step (NCCL process
+    group of one rank) all-reduces its gradients: the profiler records the
+    collective as a trace kernel touching the gradient, so the planner never
+    offloads a gradient across its all-reduce."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2506_06472_b200.profiler import profile_step
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        torch.manual_seed(0)
+        w = torch.randn(256, 256, device="cuda", requires_grad=True)
+        x = torch.randn(64, 256, device="cuda")
+
+        def step():
+            loss = (x @ w).square().mean()
+            loss.backward()
+            dist.all_reduce(w.grad)                    # the DP gradient exchange
+            with torch.no_grad():
+                w.sub_(1e-3 * w.grad)
+            w.grad = None
+
+        step()
+        tr = profile_step(step, globals_={"w": w})
+        a = tr.arrays()
+        names = [a.name_table[c] for c in a.kernel_name_code.tolist()]
+        ks = [k for k, n in enumerate(names) if "allreduce" in n]
+        assert ks, names
+        k = ks[0]
+        # the collective touches exactly the gradient: an intermediate of the
+        # step produced by the backward and consumed by the update
+        touched = [t for t in range(a.num_tensors) if k in a.accesses[a.access_ptr[t]:a.access_ptr[t + 1]]]
+        assert len(touched) == 1
+        t = touched[0]
+        assert a.size_bytes[t] == 256 * 256 * 4 and a.kind[t] == 0
+        acc = a.accesses[a.access_ptr[t]:a.access_ptr[t + 1]].tolist()
+        assert acc[0] < k < acc[-1]                    # produced before, consumed after the collective
+    finally:
+        dist.destroy_process_group()
