@@ -13,6 +13,11 @@
 #include <cstdint>
 #include "common.cuh"
 
+// walk-length statistics hook (the planner's debug build defines it)
+#ifndef WWALK_COUNT
+#define WWALK_COUNT(n) do { } while (0)
+#endif
+
 namespace tio {
 
 // first index i in [lo, hi) with pred(i) true, for a monotone (false..true)
@@ -47,7 +52,9 @@ __device__ __forceinline__ int64_t warp_earliest(const int64_t *cs, const int64_
     const int lane = threadIdx.x & 31;
     int64_t i = warp_lower_bound(lo_idx, hi_idx, [&](int64_t j) { return ld_cg(ce + j) > ready; });
     int64_t t = ready;
+    int64_t iters = 0;
     while (i < n) {
+        ++iters;
         const int64_t j = i + lane;
         const bool in = j < n;
         const int64_t s = in ? ld_cg(cs + j) : INT64_MAX;
@@ -60,6 +67,7 @@ __device__ __forceinline__ int64_t warp_earliest(const int64_t *cs, const int64_
         if (m) {
             const int f = __ffs(m) - 1;
             *p = i + f;
+            WWALK_COUNT(iters);
             return __shfl_sync(0xffffffffu, tj, f);
         }
         const int64_t last_e = __shfl_sync(0xffffffffu, e, 31);
@@ -80,10 +88,12 @@ __device__ __forceinline__ bool warp_latest(const int64_t *cs, const int64_t *ce
     // last index with s < deadline = (first index with s >= deadline) - 1
     int64_t i = warp_lower_bound(lo_idx, hi_idx, [&](int64_t j) { return ld_cg(cs + j) >= deadline; }) - 1;
     int64_t start = deadline - d;
+    int64_t iters = 0;
     // Walking down from i: every visited booking starts before start + d
     // (sorted, disjoint), so the reference's `continue` branch never fires;
     // a booking either ends at or before `start` (fit) or pushes start to s - d.
     while (i >= 0) {
+        ++iters;
         const int64_t j = i - lane;
         const bool in = j >= 0;
         const int64_t s = in ? ld_cg(cs + j) : INT64_MIN;
@@ -94,6 +104,7 @@ __device__ __forceinline__ bool warp_latest(const int64_t *cs, const int64_t *ce
         const unsigned m = __ballot_sync(0xffffffffu, stop);
         if (m) {
             const int f = __ffs(m) - 1;
+            WWALK_COUNT(iters);
             const int64_t st = __shfl_sync(0xffffffffu, sj, f);
             if (st < not_before) return false;
             *out = st;
