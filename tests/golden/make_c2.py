@@ -26,7 +26,7 @@ ROOT = os.path.abspath(os.path.join(HERE, "..", ".."))
 sys.path.insert(0, ROOT)
 
 
-def main(config: str = "c2"):
+def main(config: str = "c2", max_rounds: int = 0):
     from oracle import oracle as O
     from paper_2506_06472_b200 import LLAMA3_8B, LLAMA3_70B, gen_llama_trace, write_trace
     from paper_2506_06472_b200.tracegen import llama_peak_bytes
@@ -38,9 +38,9 @@ def main(config: str = "c2"):
     host_cap = 256 * 10**9 if host else 0
     t0 = time.time()
     if host:
-        p = O.plan(a, cap, 16000.0, 16000.0, 50000.0, 50000.0, host_cap, verbose=True)
+        p = O.plan(a, cap, 16000.0, 16000.0, 50000.0, 50000.0, host_cap, verbose=True, max_rounds=max_rounds)
     else:
-        p = O.plan(a, cap, 16000.0, 16000.0, verbose=True)
+        p = O.plan(a, cap, 16000.0, 16000.0, verbose=True, max_rounds=max_rounds)
     rec = {
         "trace_sha256": hashlib.sha256(write_trace(tr)).hexdigest(),
         "num_events": a.num_events, "capacity": cap, "rates": rates, "host_cap": host_cap,
@@ -54,10 +54,13 @@ def main(config: str = "c2"):
     }
     out_dir = os.environ.get("TIO_GOLDEN_OUT", HERE)       # e.g. gpurun_out/ when run on the GPU box's host
     os.makedirs(out_dir, exist_ok=True)
-    with gzip.open(os.path.join(out_dir, f"{config}.json.gz"), "wt") as f:
+    if max_rounds:
+        rec["max_rounds"] = max_rounds          # a prefix of the greedy sequence (planner.py:293-351)
+    name = f"{config}_prefix{max_rounds}" if max_rounds else config
+    with gzip.open(os.path.join(out_dir, f"{name}.json.gz"), "wt") as f:
         json.dump(rec, f)
     print(rec)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "c2")
+    main(sys.argv[1] if len(sys.argv) > 1 else "c2", int(sys.argv[2]) if len(sys.argv) > 2 else 0)
