@@ -490,6 +490,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     extra = None
     if args.secondary and args.secondary != args.config:
         extra = measure(args.secondary, args.steps, warm, dev, rank, world)
+    c5 = c5_leg(args, rank, world) if args.c5 and world > 1 else None
     if rank != 0:
         return
     rounds = m.pop("rounds")
@@ -510,17 +511,60 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                             if args.config == "c3" else args.ref_rounds)
     if world > 1 and m_sh is not None:
         line["sharded_lifetime"] = m_sh
+    if c5 is not None:
+        line["migration_dp"] = c5
     if not args.no_migration and world == 1:
         # C4 on one GPU; at N > 1 the per-rank pinned host extents (24-78 GB
         # each) would exceed the box's host memory, so the leg runs at N = 1 only
         from paper_2506_06472_b200 import engine
         link = engine.measure_link()
-        line["migration"] = real_step_bench(link=link, model=args.offload_model)
+        line["migration"] = real_step_bench(link=link, model=args.offload_model, rate_scale=args.c4_rate_scale,
+                                            fracs=tuple(args.c4_fracs),
+                                            identity_frac=0 if args.no_identity else 0.8)
         if args.replay_leg:
             # the synthetic Appendix-C replay against placeholder kernels (round 1's leg)
             line["migration_replay"] = [migration_bench(mb, link=link, cap_frac=f)
                                         for mb, f in ((4, 0.5), (8, 0.8), (8, 0.9))]
     print(json.dumps(line), flush=True)
+
+
+def c5_leg(args, rank: int, world: int) -> dict:
+    """Configs C5 (BASELINE.json configs[4]): data-parallel Llama-3-8B, one
+    rank per GPU, every rank profiling its own step (gradients all-reduced
+    between backward and the optimizer — the collective is a trace kernel
+    touching the gradients, so they stay resident across it), planning it
+    and running its own online engine over its own link, all at once.
+    Reported: per capacity, the slowest rank's offloaded step vs the slowest
+    rank's no-offload step, and every rank's link rates and byte checks."""
+    import torch.distributed as dist
+    from paper_2506_06472_b200 import engine
+    own_link = engine.measure_link()
+    box = [own_link]
+    dist.broadcast_object_list(box, src=0)      # every rank plans with rank 0's link rate: identical plans
+    r = real_step_bench(fracs=tuple(args.c5_fracs), link=box[0], model=args.offload_model, identity_frac=0,
+                        dp=True)
+    r["own_link"] = own_link
+    allr = [None] * world
+    dist.all_gather_object(allr, r)
+    if rank != 0:
+        return None
+    out = {"workload": allr[0]["workload"] + f"; data parallel over {world} ranks (gradient all-reduce)",
+           "ranks": world, "ideal_step_ms_max": max(x["ideal"]["step_ms"] for x in allr),
+           "plans_identical": len({json.dumps([run["plan"]["sha256"] for run in x["runs"]]) for x in allr}) == 1,
+           "links_gbs": [{"h2d": x["own_link"]["h2d_gbs"], "d2h": x["own_link"]["d2h_gbs"]} for x in allr],
+           "plan_link": "rank 0's measured bidirectional rate (broadcast), rank 0's profiled durations", "runs": []}
+    for i, frac in enumerate(args.c5_fracs):
+        runs = [x["runs"][i] for x in allr]
+        out["runs"].append({
+            "capacity_frac_of_trace_peak": frac,
+            "step_ms_max": max(q["step_ms"] for q in runs),
+            "step_vs_ideal": max(q["step_ms"] for q in runs) / out["ideal_step_ms_max"],
+            "model_step_vs_ideal": max(q["model_step_vs_ideal"] for q in runs),
+            "offload_gbs_min": min(q["offload_gbs"] for q in runs),
+            "prefetch_gbs_min": min(q["prefetch_gbs"] for q in runs),
+            "verify_mismatches": sum(q["verify"]["mismatches"] for q in runs),
+            "allocator_peak_vs_capacity_max": max(q["allocator_peak_vs_capacity"] for q in runs)})
+    return out
 
 
 def migration_bench(microbatches: int = 8, verify: bool = True, link: dict | None = None,
@@ -563,7 +607,8 @@ def migration_bench(microbatches: int = 8, verify: bool = True, link: dict | Non
 
 
 def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = None, model: str = "8b",
-                    identity_frac: float = 0.8, identity_steps: int = 2) -> dict:
+                    identity_frac: float = 0.8, identity_steps: int = 2, dp: bool = False,
+                    rate_scale: float = 1.0) -> dict:
     """Configs C4 (BASELINE.json configs[3]): the migration engine executing
     the plan of a REAL Llama-3-8B training step on 1 B200 (random init bf16
     weights, fp32 AdamW moments, synthetic 8,192-token batch;
@@ -591,14 +636,47 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
     import dataclasses
     import gc
     import torch
-    from paper_2506_06472_b200 import ChannelRates, compute_memory_timeline, engine, plan_migrations
+    import hashlib
+    from paper_2506_06472_b200 import ChannelRates, compute_memory_timeline, engine, plan_migrations, write_plan
     from paper_2506_06472_b200.llama_step import LLAMA3_8B_MODEL, TINY, Step
     from paper_2506_06472_b200.profiler import profile_step
     cfg_det = LLAMA3_8B_MODEL if model == "8b" else TINY
     cfg = dataclasses.replace(cfg_det, deterministic=False)
-    dev = torch.device("cuda")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    group = None
+    if dp:                                     # configs C5: every rank runs this leg at once
+        import torch.distributed as dist
+        group = dist.group.WORLD
+
+        def Step(c, seed=0, _S=Step):          # noqa: N802 - the DP form of the step
+            return _S(c, seed=seed, dp_group=group)
+
+    def sync():
+        if group is not None:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def common_trace(tr):
+        """DP: the ranks' traces have the same operators and tensors; their
+        profiled durations differ by timing noise.  Every rank takes rank 0's
+        durations (one int64[N] broadcast), so every rank plans the same trace
+        and holds the same plan (identical per-rank plans)."""
+        if group is None:
+            return tr
+        import dataclasses as dc
+        import numpy as np
+        import torch.distributed as dist
+        from paper_2506_06472_b200.trace import Trace
+        a = tr.arrays()
+        d = torch.from_numpy(np.ascontiguousarray(a.duration_us, dtype=np.int64))
+        d = d.to(dev) if dist.get_backend(group) == "nccl" else d
+        dist.broadcast(d, src=0, group=group)
+        return Trace.from_arrays(dc.replace(a, duration_us=d.cpu().numpy().astype(np.int64)), dict(tr.meta))
     link = link or engine.measure_link()
-    rate = float(int(link["bidir_gbs_each"] * 1e3))            # bytes/us, integral
+    # the plan's channel rate: the measured link with both directions busy,
+    # optionally scaled (rate_scale < 1 plans with headroom for the copies'
+    # achieved per-transfer rate)
+    rate = float(int(link["bidir_gbs_each"] * 1e3 * rate_scale))   # bytes/us, integral
     rates = ChannelRates.symmetric(rate)
     stream = torch.cuda.current_stream()
     loss_host = torch.empty((), dtype=torch.float32, pin_memory=True)
@@ -606,6 +684,7 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
     def run(s, n, mode=None):
         losses = []
         torch.cuda.synchronize()
+        sync()                                 # DP: every rank starts the timed steps together
         torch.cuda.reset_peak_memory_stats()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -679,7 +758,8 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
     s = Step(cfg, seed=0)
     s()
     t0 = time.perf_counter()
-    tr = profile_step(s, globals_=s.globals_of(), meta={"generator": "TraceProfiler", "model": f"llama3-{model}"})
+    tr = common_trace(profile_step(s, globals_=s.globals_of(), meta={"generator": "TraceProfiler",
+                                                                       "model": f"llama3-{model}"}))
     t_prof = time.perf_counter() - t0
     s = None
     free()
@@ -688,7 +768,7 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
     out = {"workload": f"Llama-3-{model.upper()} real training step (random init bf16 weights, fp32 AdamW, "
                        f"1 x {cfg.seq} synthetic tokens); trace of the profiled step: {a.num_kernels} kernels "
                        f"(aten operators), {a.num_tensors} tensors, {a.num_events} events, peak {peak} B",
-           "link": link, "plan_rates_bytes_per_us": rate,
+           "link": link, "plan_rates_bytes_per_us": rate, "plan_rate_scale": rate_scale,
            "ideal": {"step_ms": ideal_ms, "allocator_peak_bytes": ideal_peak, "losses": ideal_losses,
                      "rerun_losses": rerun_losses, "rerun_state_checksums_equal": rerun_digest == ideal_digest,
                      "deterministic": rerun_losses == ideal_losses and rerun_digest == ideal_digest,
@@ -707,7 +787,8 @@ def real_step_bench(fracs=(0.5, 0.8, 0.9), steps: int = 3, link: dict | None = N
         out["runs"].append({
             "capacity_frac_of_trace_peak": frac, "capacity": cap,
             "plan": {"entries": len(plan.entries), "warning": plan.warning,
-                     "over_capacity_kernels": len(plan.over_capacity_kernels), "seconds": t_plan},
+                     "over_capacity_kernels": len(plan.over_capacity_kernels), "seconds": t_plan,
+                     "sha256": hashlib.sha256(write_plan(plan)).hexdigest()},
             "step_ms": ms, "step_vs_ideal": ms / ideal_ms,
             "model_step_vs_ideal": info["model_total_us"] / max(1, info["model_ideal_us"]),
             "link_lower_bound_ms": lb_ms, "link_lower_bound_vs_ideal": max(1.0, lb_ms / ideal_ms),
@@ -768,6 +849,15 @@ def main(argv=None):
     ap.add_argument("--no-migration", action="store_true", help="skip the C4 offloaded-step leg")
     ap.add_argument("--offload-model", default="8b", choices=["8b", "tiny"],
                     help="model of the C4 leg (8b = Llama-3-8B; tiny for quick checks)")
+    ap.add_argument("--c4-rate-scale", type=float, default=1.0,
+                    help="C4: plan with this fraction of the measured bidirectional link rate")
+    ap.add_argument("--c4-fracs", type=float, nargs="+", default=[0.5, 0.8, 0.9],
+                    help="C4: capacities (x trace peak)")
+    ap.add_argument("--no-identity", action="store_true", help="C4: skip the byte-identity sub-leg")
+    ap.add_argument("--c5", action="store_true",
+                    help="N > 1: also run the data-parallel offloaded step on every rank (configs C5)")
+    ap.add_argument("--c5-fracs", type=float, nargs="+", default=[0.9],
+                    help="capacities (x trace peak) of the C5 leg")
     ap.add_argument("--replay-leg", action="store_true",
                     help="also run the Appendix-C replay against placeholder kernels")
     ap.add_argument("--ref-rounds", type=int, default=40, help="planner rounds in the CPU sample (C2)")

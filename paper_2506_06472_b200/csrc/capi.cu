@@ -131,6 +131,8 @@ struct VGroup {
     std::condition_variable cv;
     int arrived = 0;
     bool launched = false;
+    bool failed = false;                 // a rank failed before its launch point: nobody launches
+    std::vector<char> here;              // rank r reached the rendezvous (or gave up)
     int rc = TIO_OK;
     std::vector<PlanArgs> args;
     std::vector<cudaEvent_t> ready;
@@ -140,11 +142,30 @@ struct VGroup {
 static thread_local VGroup *t_vgroup = nullptr;
 static thread_local int t_vrank = 0;
 
+// a rank that ends (error) without reaching the launch still counts as
+// arrived, so the others are released instead of waiting forever
+static void vgroup_leave(VGroup *g, int rank) {
+    std::unique_lock<std::mutex> lk(g->m);
+    if (g->here[rank]) return;
+    g->here[rank] = 1;
+    g->failed = true;
+    if (++g->arrived == g->nranks) {
+        g->rc = fail(TIO_ERR_INTERNAL, "virtual ranks: a rank failed before the round loop");
+        g->launched = true;
+        g->cv.notify_all();
+    }
+}
+
 static int vgroup_launch(VGroup *g, int rank, const PlanArgs &a, cudaStream_t s) {
     std::unique_lock<std::mutex> lk(g->m);
+    g->here[rank] = 1;
     g->args[rank] = a;
     cudaEventRecord(g->ready[rank], s);
-    if (++g->arrived == g->nranks) {
+    if (++g->arrived == g->nranks && g->failed) {
+        g->rc = fail(TIO_ERR_INTERNAL, "virtual ranks: a rank failed before the round loop");
+        g->launched = true;
+        g->cv.notify_all();
+    } else if (g->arrived == g->nranks) {
         int rc = TIO_OK;
         for (int r = 0; r < g->nranks && rc == TIO_OK; ++r)
             if (cudaStreamWaitEvent(s, g->ready[r], 0) != cudaSuccess) rc = fail(TIO_ERR_CUDA, "virtual ranks: wait");
@@ -578,10 +599,11 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     a.ntiles = ntiles; a.tcand = tcand; a.t_lo = t_lo; a.t_hi = t_hi;
     a.t_ka_lo = t_ka_lo; a.t_ka_hi = t_ka_hi; a.t_kb_lo = t_kb_lo; a.t_kb_hi = t_kb_hi; a.tile_best = tile_best;
     int G = 0;
-    const bool wide = !t_vgroup && plan_loop_wide(ntiles);
+    const int nranks = opts && opts->nranks > 1 ? opts->nranks : 1;
+    // the wide form pays off with many tiles per rank (sharded: this rank's share)
+    const bool wide = !t_vgroup && plan_loop_wide(ntiles / nranks);
     PTRY(plan_loop_grid(&G, wide));
     if (opts && opts->blocks > 0 && opts->blocks < G) G = opts->blocks;
-    const int nranks = opts && opts->nranks > 1 ? opts->nranks : 1;
     if (nranks > MAX_RANKS) return bail(fail(TIO_ERR_INVALID, "at most %d ranks", MAX_RANKS));
     if (nranks > 1) {
         if (!opts->mailbox || !opts->peer_mailboxes || opts->rank < 0 || opts->rank >= nranks)
@@ -872,6 +894,7 @@ int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rat
     grp.blocks_per_rank = G / nranks;
     grp.args.resize(nranks);
     grp.ready.resize(nranks);
+    grp.here.assign(nranks, 0);
     for (int r = 0; r < nranks; ++r) TIO_CUDA(cudaEventCreateWithFlags(&grp.ready[r], cudaEventDisableTiming));
     TIO_CUDA(cudaEventCreateWithFlags(&grp.done, cudaEventDisableTiming));
     TIO_CUDA(cudaMalloc((void **)&grp.dev_args, sizeof(PlanArgs) * nranks));
@@ -890,6 +913,7 @@ int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rat
             if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
                 rcs[r] = fail(TIO_ERR_CUDA, "stream creation failed");
                 errs[r] = "stream creation failed";
+                vgroup_leave(&grp, r);
                 return;
             }
             tio_plan_opts o;
@@ -902,6 +926,7 @@ int tio_plan_create_virtual(tio_trace *t, int64_t capacity, const tio_rates *rat
             o.mailbox = mb + r;
             o.peer_mailboxes = peers.data();
             rcs[r] = tio_plan_create2(t, capacity, rates, host_cap, &o, s, &out[r], &info[r]);
+            vgroup_leave(&grp, r);           // no-op when the rank reached the launch
             if (rcs[r] != TIO_OK) {
                 char b[1024];
                 tio_last_error(b, sizeof(b));

@@ -1,12 +1,13 @@
 // lifetime.cu — the lifetime stage on sm_100a (reference analysis.py:58-117,
 // trace.py:97-107) as three streaming kernels, each a single pass over its
-// input with decoupled look-back scans between tiles (no grid barrier, no
-// second read of the events):
+// input with chain-free tile prefixes (agg_prefix: no grid barrier, no second
+// read of the events):
 //
 //   k_tile_owners  owner tensor of every event-tile boundary (32-ary warp
 //                  searches over the CSR offsets).
-//   k_events       one tile of LT_EPT consecutive events per thread (LT_TILE
-//                  per block, tiles claimed in order from an atomic counter):
+//   k_events       one tile of LT_TILE events per block (tiles claimed in
+//                  order from an atomic counter), walked warp-contiguously
+//                  (lane = event) with owners from a tensor-head bitmask:
 //                    active[k] += size                (per_kernel_active_bytes, :111-117)
 //                    diff[first] += size, diff[last+1] -= size for intermediates
 //                                                     (compute_memory_timeline, :97-108)
@@ -179,243 +180,66 @@ __global__ void k_tile_owners(const int64_t *ptr, int64_t T, int64_t E, int64_t 
 }
 
 // ---------------------------------------------------------------- events
+// Warp-contiguous form: warp w of a tile walks events [256 w, 256 w + 256) in
+// 8 steps of 32 (lane = event).  A tensor-head bitmask over the tile (one bit
+// per event where a staged tensor starts) gives every event its owner with
+// one broadcast load and a popcount; a step's periods are a ballot, so the
+// tile-local record offsets need one block exchange (warp totals) and the
+// records are stored straight to their final positions.
 struct EvSmem {
-    alignas(16) int32_t acc[LT_TILE + 4];   // the tile's accesses (+ the next tile's first); first: 16-byte aligned
-    int32_t ptr[LT_MAXO + 1];   // staged CSR offsets relative to the tile's first event
-    int16_t own[LT_TILE];       // staged owner index of every event of the tile
-    union {
-        uint64_t sk[LT_MAXO];   // during the walks: size | kind << 63 of the staged tensors
-        int16_t rec[LT_TILE];   // afterwards: the event opening each period, tile-local order
-    };
-    int32_t scan32[40];
-    int64_t scan[40];
+    alignas(16) int32_t acc[LT_TILE + 4];
+    int32_t ptr[LT_MAXO + 1];
+    uint64_t sk[LT_MAXO];
+    uint32_t head[LT_TILE / 32];
+    int32_t wcnt[LIFETIME_THREADS / 32];
+    int64_t wglob[LIFETIME_THREADS / 32];
+    unsigned long long wflags[LIFETIME_THREADS / 32];
     int64_t prefix;
     int64_t tile;
 };
 
-// exclusive block max-scan of int32 (-1 identity), all threads
-__device__ __forceinline__ int32_t block_exclusive_max(int32_t v, int32_t *sm) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int32_t inc = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t n = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o && n > inc) inc = n;
-    }
-    if (lane == 31) sm[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        int32_t w = lane < nw ? sm[lane] : -1;
-        int32_t wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t n = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o && n > wi) wi = n;
-        }
-        const int32_t ex = __shfl_up_sync(0xffffffffu, wi, 1);
-        if (lane < nw) sm[lane] = lane == 0 ? -1 : ex;
-    }
-    __syncthreads();
-    int32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (lane == 0) ex = -1;
-    const int32_t r = sm[warp] > ex ? sm[warp] : ex;
-    __syncthreads();
-    return r;
-}
-
-// One event tile.  Staging: the tile's tensors (CSR offsets, sizes, kinds)
-// and accesses in shared memory, and an owner map (tensor heads, then a
-// block max-scan).  Walks over each thread's LT_EPT consecutive events:
-// (1) validation, period count, masks; (2) the atomics; (3) period records
-// in shared memory at tile-local offsets.  The tile prefix comes from a
-// decoupled look-back; records are then stored coalesced.
 __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, EvSmem &sm, int64_t tile,
-                                                         int64_t NTe, int64_t *est, int64_t *egrp,
-                                                         const int64_t *owner) {
+                                                          int64_t NTe, int64_t *est, int64_t *egrp,
+                                                          const int64_t *owner) {
+    constexpr int STEPS = LT_TILE / LIFETIME_THREADS;        // 8 steps of 32 events per warp
     const int64_t T = a.T, E = a.E;
     const int32_t N = (int32_t)a.N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long flags = 0;
     const int64_t e0 = tile * LT_TILE, e1 = (e0 + LT_TILE < E) ? e0 + LT_TILE : E;
     const int32_t ne = (int32_t)(e1 - e0);
     const int64_t o0 = __ldcg(reinterpret_cast<const long long *>(owner + tile));
     int64_t o1 = __ldcg(reinterpret_cast<const long long *>(owner + tile + 1));
     if (o1 < o0) o1 = o0;
-    const int64_t no = o1 - o0 + 1;
-    // more staged tensors than events can only come from empty tensors (an
-    // invalid trace, flagged by the tensor-table checks): skip the tile
+    const int32_t no = (int32_t)(o1 - o0 + 1);
     const bool staged = no <= LT_MAXO;
-    for (int i = threadIdx.x; i < LT_TILE; i += blockDim.x) sm.own[i] = i == 0 ? 0 : -1;   // o0 starts at or before the tile
-    if (staged) {
-        for (int64_t i = threadIdx.x; i <= no; i += blockDim.x) {
-            const int64_t p = (o0 + i <= T) ? __ldg(a.ptr + o0 + i) : E;
-            sm.ptr[i] = (int32_t)(p - e0 < INT32_MIN ? INT32_MIN : (p - e0 > INT32_MAX ? INT32_MAX : p - e0));
-        }
-        for (int64_t i = threadIdx.x; i < no; i += blockDim.x) {
-            sm.sk[i] = (uint64_t)__ldg(a.size + o0 + i) | ((uint64_t)(__ldg(a.kind + o0 + i) == 1) << 63);
-        }
-    }
+
+    // ---- staging; the head mask (zeroed before the ticket barrier)
     if (((uintptr_t)a.acc & 15) == 0 && ne == LT_TILE) {
         const int4 *q = reinterpret_cast<const int4 *>(a.acc + e0);
-        for (int i = threadIdx.x; i < LT_TILE / 4; i += blockDim.x)
+        for (int i = threadIdx.x; i < LT_TILE / 4; i += LIFETIME_THREADS)
             reinterpret_cast<int4 *>(sm.acc)[i] = __ldg(q + i);
     } else {
-        for (int i = threadIdx.x; i < ne; i += blockDim.x) sm.acc[i] = __ldg(a.acc + e0 + i);
+        for (int i = threadIdx.x; i < ne; i += LIFETIME_THREADS) sm.acc[i] = __ldg(a.acc + e0 + i);
     }
     if (threadIdx.x == 0) sm.acc[ne] = e1 < E ? __ldg(a.acc + e1) : 0;
-    __syncthreads();
-    // owner map: tensor heads inside the tile, then a running max
-    if (staged)
-        for (int64_t i = threadIdx.x; i < no; i += blockDim.x) {
-            const int32_t r = sm.ptr[i];
-            if (r >= 0 && r < ne) sm.own[r] = (int16_t)i;
-        }
-    __syncthreads();
-    const int32_t frel = (int32_t)threadIdx.x * LT_EPT;           // tile-relative first event
-    const int nv = (!staged || frel >= ne) ? 0 : (ne - frel < LT_EPT ? ne - frel : LT_EPT);
-    int32_t own[LT_EPT];
-    {
-        int32_t run = -1;
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) {
-            const int32_t v = frel + j < LT_TILE ? sm.own[frel + j] : -1;
-            run = v > run ? v : run;
-            own[j] = run;
-        }
-        const int32_t ex = block_exclusive_max(run, sm.scan32);
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) {
-            own[j] = own[j] > ex ? own[j] : ex;
-            if (frel + j < LT_TILE) sm.own[frel + j] = (int16_t)own[j];   // resolved, for the record pass
-        }
-    }
-    int32_t k[LT_EPT + 1];
-#pragma unroll
-    for (int j = 0; j <= LT_EPT; ++j) k[j] = frel + j <= ne ? sm.acc[frel + j] : 0;
-
-    // ---- walk 1: validation, period count, masks
-    int64_t cnt = 0;
-    uint32_t pmask = 0;                      // bit j: event j opens a period
-    uint32_t fmask = 0;                      // bit j: event j is its tensor's first access
-#pragma unroll
-    for (int j = 0; j < LT_EPT; ++j) {
-        if (j >= nv) break;
-        const int32_t e = frel + j, o = own[j];
-        const int32_t beg = sm.ptr[o], nxt = sm.ptr[o + 1];
-        const int32_t kk = k[j];
-        if (e == beg) fmask |= 1u << j;
-        if (e < beg || e >= nxt) { flags |= LF_BAD_PTR; continue; }
-        if ((uint32_t)kk >= (uint32_t)N) { flags |= LF_ACCESS_RANGE; continue; }
-        if (e != nxt - 1) {
-            const int32_t k2 = k[j + 1];
-            if (k2 <= kk) flags |= LF_NOT_INCREASING;
-            else if (k2 - kk > 1) { pmask |= 1u << j; ++cnt; }
-        } else if (sm.sk[o] >> 63) {
-            const int32_t fk = beg >= 0 ? sm.acc[beg] : __ldg(a.acc + e0 + beg);
-            if ((N - 1 - kk) + fk > 0) { pmask |= 1u << j; ++cnt; }
-        }
-    }
-    // tile-local offsets; the aggregate goes out before the atomics so the
-    // successors' look-backs only wait for this counting walk
-    int64_t tot;
-    const int64_t loc = block_exclusive_sum<int64_t>(cnt, sm.scan, &tot);
-    if (threadIdx.x < 32) agg_publish(est, egrp, tile, tot);
-
-    // ---- walk 2: per-kernel active bytes and the timeline difference array
-#ifndef LT_NO_REDS          // (timing experiments only: tools/build_variant.sh -DLT_NO_REDS)
-    if (!(flags & (LF_ACCESS_RANGE | LF_BAD_PTR))) {
-#else
-    if (false) {
-#endif
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) {
-            if (j >= nv) break;
-            const int32_t e = frel + j, o = own[j];
-            const int32_t kk = k[j];
-            const int64_t sz = (int64_t)(sm.sk[o] & ~(1ull << 63));
-            atomic_add_i64(&a.active[kk], sz);                     // per_kernel_active_bytes (:111-117)
-            if (!(sm.sk[o] >> 63)) {                               // compute_memory_timeline (:97-108)
-                if (e == sm.ptr[o]) atomic_add_i64(&a.diff[kk], sz);
-                if (e == sm.ptr[o + 1] - 1) atomic_add_i64(&a.diff[kk + 1], -sz);
+    if (staged) {
+        for (int32_t i = threadIdx.x; i <= no; i += LIFETIME_THREADS) {
+            const int64_t p = (o0 + i <= T) ? __ldg(a.ptr + o0 + i) : E;
+            const int64_t r = p - e0;
+            sm.ptr[i] = (int32_t)(r < INT32_MIN ? INT32_MIN : (r > INT32_MAX ? INT32_MAX : r));
+            if (i < no) {
+                sm.sk[i] = (uint64_t)__ldg(a.size + o0 + i) | ((uint64_t)(__ldg(a.kind + o0 + i) == 1) << 63);
+                if (i > 0 && r >= 0 && r < LT_TILE) atomicOr(&sm.head[r >> 5], 1u << (r & 31));
             }
         }
     }
-    __syncthreads();                         // sizes / kinds no longer needed: records reuse them
-
-    // ---- walk 3: period records in reference order (analysis.py:68-82:
-    // tensor order, gaps ascending, wrap last) at tile-local offsets
-    if (pmask && flags == 0) {
-        int32_t q = (int32_t)loc;
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j)
-            if (pmask & (1u << j)) sm.rec[q++] = (int16_t)(frel + j);
-    }
-
-    // ---- tile prefix
-    if (threadIdx.x < 32) {
-        int64_t pre;
-        agg_prefix<1>(est, 0, egrp, 0, tile, &pre);
-        if (threadIdx.x == 0) sm.prefix = pre;
-    }
-    __syncthreads();
-    const int64_t prefix = sm.prefix;
-    if (tile == NTe - 1 && threadIdx.x == 0) {
-        a.tensor_pptr[T] = prefix + tot;
-        a.scalars[SC_NUM_PERIODS] = prefix + tot;
-    }
-    const bool ok = __syncthreads_or(flags != 0) == 0;
-    if (!ok) return flags;
-    // per-tensor period offsets
-    if (fmask) {
-        int64_t q = prefix + loc;
-#pragma unroll
-        for (int j = 0; j < LT_EPT; ++j) {
-            if (fmask & (1u << j)) a.tensor_pptr[o0 + own[j]] = q;
-            if (pmask & (1u << j)) ++q;
-        }
-    }
-    // period records, stored coalesced: the staged event and the staged
-    // accesses / owner map give the record back
-#ifdef LT_NO_RECORDS
-    return flags;
-#endif
-    for (int64_t i = threadIdx.x; i < tot; i += blockDim.x) {
-        const int32_t e = sm.rec[i], o = sm.own[e], kk = sm.acc[e];
-        const int64_t g = prefix + i;
-        a.p_tensor[g] = o0 + o;
-        if (e != sm.ptr[o + 1] - 1) {
-            a.p_start[g] = kk + 1; a.p_end[g] = sm.acc[e + 1] - 1; a.p_wraps[g] = 0;
-        } else {
-            const int32_t beg = sm.ptr[o];
-            const int32_t fk = beg >= 0 ? sm.acc[beg] : __ldg(a.acc + e0 + beg);
-            a.p_start[g] = (kk + 1) % N; a.p_end[g] = ((fk - 1) % N + N) % N; a.p_wraps[g] = 1;
-        }
-    }
-    return flags;
-}
-
-#ifndef LT_MINB
-#define LT_MINB 6            // 40 registers: 5 blocks (shared memory bound) per SM; measured 211 vs 226 us at C3
-#endif
-__global__ void __launch_bounds__(LIFETIME_THREADS, LT_MINB)
-k_events(LifetimeArgs a) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");      // owners + zeroed status (programmatic launch)
-    extern __shared__ __align__(16) unsigned char smraw[];
-    EvSmem &sm = *reinterpret_cast<EvSmem *>(smraw);
-    const int64_t T = a.T, E = a.E;
-    const int64_t NTe = lifetime_event_tiles(E);
-    if (threadIdx.x == 0) sm.tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(a.work), 1ull);
-    __syncthreads();
-    const int64_t tile = sm.tile;
-    unsigned long long flags = 0;
-    const LtWork w = lt_work(a.work, a.N, E);
-    if (tile < NTe) flags = event_tile(a, sm, tile, NTe, w.est, w.egrp, w.owner);
-
-    // ---- a slice of the tensor table: CSR / size / kind / id order, global bytes
+    // tensor-table slice (validation, globals' bytes)
+    int64_t glob = 0;
     {
-        const int64_t per = (T + gridDim.x - 1) / gridDim.x;
+        const int64_t per = (T + NTe - 1) / NTe;
         const int64_t i0 = tile * per, i1 = i0 + per < T ? i0 + per : T;
-        int64_t glob = 0;
-        for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        for (int64_t i = i0 + threadIdx.x; i < i1; i += LIFETIME_THREADS) {
             if (__ldg(a.ptr + i + 1) <= __ldg(a.ptr + i)) flags |= LF_BAD_PTR;
             const int64_t sz = __ldg(a.size + i);
             if (sz <= 0) flags |= LF_BAD_SIZE;
@@ -425,8 +249,148 @@ k_events(LifetimeArgs a) {
             if (i + 1 < T && !(__ldg(a.tid + i) < __ldg(a.tid + i + 1))) a.scalars[SC_IDS_UNSORTED] = 1;
         }
         if (tile == 0 && threadIdx.x == 0 && (__ldg(a.ptr) != 0 || __ldg(a.ptr + T) != E)) flags |= LF_BAD_PTR;
-        const int64_t g = block_sum<int64_t>(glob, sm.scan);
-        if (threadIdx.x == 0 && g) atomic_add_i64(&a.scalars[SC_GLOBAL_BYTES], g);
+    }
+    if (!staged) flags |= LF_BAD_PTR;
+    __syncthreads();
+
+    // ---- walk: this warp's events, one per lane per step
+    const int32_t wbase = warp * (STEPS * 32);
+    // heads before this warp's first word (each lane sums its share, then the warp)
+    int32_t hb = 0;
+    for (int j = lane; j < (wbase >> 5); j += 32) hb += __popc(sm.head[j]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) hb += __shfl_xor_sync(0xffffffffu, hb, d);
+    const uint32_t le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);   // lanes <= this one
+    const uint32_t lt = (1u << lane) - 1u;                                  // lanes < this one
+    uint32_t pb[STEPS];                       // period ballot per step
+    int32_t wcnt = 0;
+    const bool live = staged && flags == 0;
+#pragma unroll
+    for (int st = 0; st < STEPS; ++st) {
+        const int32_t e = wbase + st * 32 + lane;
+        const uint32_t hw = sm.head[(wbase >> 5) + st];
+        const int32_t o = hb + __popc(hw & le);
+        hb += __popc(hw);
+        const bool in = live && e < ne && o < no;
+        bool per = false;
+        if (in) {
+            const int32_t beg = sm.ptr[o], nxt = sm.ptr[o + 1];
+            const int32_t kk = sm.acc[e];
+            const uint64_t sk = sm.sk[o];
+            const bool glob_t = sk >> 63;
+            const int64_t sz = (int64_t)(sk & ~(1ull << 63));
+            if (e < beg || e >= nxt) {
+                flags |= LF_BAD_PTR;
+            } else if ((uint32_t)kk >= (uint32_t)N) {
+                flags |= LF_ACCESS_RANGE;
+            } else {
+#ifndef LT_NO_REDS
+                atomic_add_i64(&a.active[kk], sz);                   // per_kernel_active_bytes (:111-117)
+                if (!glob_t) {                                       // compute_memory_timeline (:97-108)
+                    if (e == beg) atomic_add_i64(&a.diff[kk], sz);
+                    if (e == nxt - 1) atomic_add_i64(&a.diff[kk + 1], -sz);
+                }
+#endif
+                if (e != nxt - 1) {
+                    const int32_t k2 = sm.acc[e + 1];
+                    if (k2 <= kk) flags |= LF_NOT_INCREASING;
+                    else per = k2 - kk > 1;
+                } else if (glob_t) {
+                    const int32_t fk = beg >= 0 ? sm.acc[beg] : __ldg(a.acc + e0 + beg);
+                    per = (N - 1 - kk) + fk > 0;
+                }
+            }
+        }
+        pb[st] = __ballot_sync(0xffffffffu, per);
+        wcnt += __popc(pb[st]);
+    }
+
+    // ---- one block exchange: warp totals, globals' bytes, flags
+    const int64_t wg = warp_sum<int64_t>(glob);
+    unsigned long long wf = flags;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) wf |= __shfl_xor_sync(0xffffffffu, wf, d);
+    if (lane == 0) { sm.wcnt[warp] = wcnt; sm.wglob[warp] = wg; sm.wflags[warp] = wf; }
+    __syncthreads();
+    int32_t woff = 0, tot = 0;
+    int64_t gsum = 0;
+    unsigned long long fall = 0;
+#pragma unroll
+    for (int w = 0; w < LIFETIME_THREADS / 32; ++w) {
+        const int32_t c = sm.wcnt[w];
+        if (w < warp) woff += c;
+        tot += c;
+        gsum += sm.wglob[w];
+        fall |= sm.wflags[w];
+    }
+    if (warp == 0) {
+        agg_publish(est, egrp, tile, tot);
+        int64_t pre;
+        agg_prefix<1>(est, 0, egrp, 0, tile, &pre);
+        if (lane == 0) {
+            sm.prefix = pre;
+            if (gsum) atomic_add_i64(&a.scalars[SC_GLOBAL_BYTES], gsum);
+            if (tile == NTe - 1) {
+                a.tensor_pptr[T] = pre + tot;
+                a.scalars[SC_NUM_PERIODS] = pre + tot;
+            }
+        }
+    }
+    __syncthreads();
+    if (fall) return flags;
+#ifdef LT_NO_RECORDS
+    return flags;
+#endif
+    // ---- records and per-tensor period offsets, at their final positions
+    int64_t q = sm.prefix + woff;             // periods before this warp's current step
+    hb = 0;
+    for (int j = lane; j < (wbase >> 5); j += 32) hb += __popc(sm.head[j]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) hb += __shfl_xor_sync(0xffffffffu, hb, d);
+#pragma unroll
+    for (int st = 0; st < STEPS; ++st) {
+        const int32_t e = wbase + st * 32 + lane;
+        const uint32_t hw = sm.head[(wbase >> 5) + st];
+        const int32_t o = hb + __popc(hw & le);
+        hb += __popc(hw);
+        if (e < ne && o < no) {
+            const int32_t beg = sm.ptr[o];
+            const int64_t my = q + __popc(pb[st] & lt);
+            if (e == beg) a.tensor_pptr[o0 + o] = my;
+            if (pb[st] & (1u << lane)) {
+                const int32_t nxt = sm.ptr[o + 1], kk = sm.acc[e];
+                a.p_tensor[my] = o0 + o;
+                if (e != nxt - 1) {
+                    a.p_start[my] = kk + 1; a.p_end[my] = sm.acc[e + 1] - 1; a.p_wraps[my] = 0;
+                } else {
+                    const int32_t fk = beg >= 0 ? sm.acc[beg] : __ldg(a.acc + e0 + beg);
+                    a.p_start[my] = (kk + 1) % N; a.p_end[my] = ((fk - 1) % N + N) % N; a.p_wraps[my] = 1;
+                }
+            }
+        }
+        q += __popc(pb[st]);
+    }
+    return flags;
+}
+
+#ifndef LT_MINB
+#define LT_MINB 6            // 40 registers; 5 blocks per SM by shared memory
+#endif
+__global__ void __launch_bounds__(LIFETIME_THREADS, LT_MINB)
+k_events(LifetimeArgs a) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");      // owners + zeroed status (programmatic launch)
+    extern __shared__ __align__(16) unsigned char smraw[];
+    EvSmem &sm = *reinterpret_cast<EvSmem *>(smraw);
+    const int64_t NTe = lifetime_event_tiles(a.E);
+    for (int i = threadIdx.x; i < LT_TILE / 32; i += blockDim.x) sm.head[i] = 0;
+    if (threadIdx.x == 0) sm.tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(a.work), 1ull);
+    __syncthreads();
+    const int64_t tile = sm.tile;
+    const LtWork w = lt_work(a.work, a.N, a.E);
+    unsigned long long flags = 0;
+    if (tile < NTe) flags = event_tile(a, sm, tile, NTe, w.est, w.egrp, w.owner);
+    else if (a.T > 0) {
+        flags = LF_BAD_PTR;                  // tensors but no events: every tensor is empty
     }
     if (flags) atomicOr(reinterpret_cast<unsigned long long *>(&a.scalars[SC_FLAGS]), flags);
 }

@@ -28,6 +28,12 @@
 #include "common.cuh"
 #include "block_scan.cuh"
 #include "planner.cuh"
+#ifdef TIO_PLAN_PROFILE
+// warp fit-walk iterations (32 bookings each) of the refits: total and max
+__device__ unsigned long long g_wwalk_total, g_wwalk_max, g_wwalk_n;
+#define WWALK_COUNT(n) do { if ((threadIdx.x & 31) == 0) { atomicAdd(&g_wwalk_total, (unsigned long long)(n)); \
+    atomicAdd(&g_wwalk_n, 1ull); atomicMax(&g_wwalk_max, (unsigned long long)(n)); } } while (0)
+#endif
 #include "warp_search.cuh"
 
 namespace cg = cooperative_groups;
@@ -551,6 +557,7 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
     __shared__ bool s_prev_refit;          // refits ran here last round (their keys are in blk_best)
     __shared__ Key s_tmax;                 // best key over the own tiles (as of their last change)
     __shared__ int32_t s_ndirty;
+    __shared__ int64_t s_fmin, s_fmax;     // this round's flipped kernels in the block's chunk
 
     const int64_t N = a.N, I = a.iteration, cap = a.capacity;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -574,14 +581,32 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
     // ---- setup: chunk prefix of critical durations
     // prefix of duration x [residual > capacity] over this block's chunk,
     // four kernels per thread per block scan
-    auto rebuild_chunk = [&]() {
-        int64_t run = 0;
-        for (int64_t base = x0; base < x1; base += 4 * (int64_t)blockDim.x) {
+    // from: the first position whose prefix can have changed (the prefix up
+    // to it, local_cp[from], is unchanged and seeds the running sum)
+    // software-pipelined: the next step's residual / duration loads are in
+    // flight across this step's block scan
+    auto rebuild_chunk = [&](int64_t from) {
+        int64_t run = from > x0 ? ld_cg(&a.local_cp[from]) : 0;
+        const int64_t step = 4 * (int64_t)blockDim.x;
+        int64_t rc[4], dc[4];
+        auto load4 = [&](int64_t x, int64_t *r, int64_t *d) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool ok = x + u < x1 && x + u < N;
+                r[u] = ok ? ld_cg(&a.resid[x + u]) : 0;
+                d[u] = ok ? __ldg(&a.dur[x + u]) : 0;
+            }
+        };
+        load4(from + 4 * (int64_t)threadIdx.x, rc, dc);
+        for (int64_t base = from; base < x1; base += step) {
             const int64_t x = base + 4 * (int64_t)threadIdx.x;
+            int64_t rn[4], dn[4];
+            if (base + step < x1) load4(x + step, rn, dn);
             int64_t wv[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                wv[u] = (x + u < x1 && x + u < N && ld_cg(&a.resid[x + u]) > cap) ? __ldg(&a.dur[x + u]) : 0;
+            for (int u = 0; u < 4; ++u) wv[u] = rc[u] > cap ? dc[u] : 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { rc[u] = rn[u]; dc[u] = dn[u]; }
             int64_t tot;
             int64_t ex = run + block_exclusive_sum<int64_t>(wv[0] + wv[1] + wv[2] + wv[3], sm_scan, &tot);
 #pragma unroll
@@ -598,7 +623,7 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
         for (int64_t x = x0 + threadIdx.x; x < x1 && x < N; x += blockDim.x)
             crit += ld_cg(&a.resid[x]) > cap;
         __syncthreads();
-        rebuild_chunk();
+        rebuild_chunk(x0);
         int64_t tot = block_sum<int64_t>(crit, sm_scan);
         if (threadIdx.x == 0 && tot) atomic_add_i64(&a.scalars[PS_CRIT], tot);
         if (threadIdx.x == 0) {
@@ -612,7 +637,7 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
             if (b == 0)
                 for (int q = 0; q < 3; ++q) { flip[3 * q] = 0; flip[3 * q + 1] = INT64_MAX; flip[3 * q + 2] = -1; }
 #ifdef TIO_PLAN_PROFILE
-            if (b == 0) { g_walk_total = 0; g_walk_max = 0; }
+            if (b == 0) { g_walk_total = 0; g_walk_max = 0; g_wwalk_total = 0; g_wwalk_max = 0; g_wwalk_n = 0; }
 #endif
         }
     }
@@ -640,6 +665,8 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
     for (int64_t round = 0;; ++round) {
         // ---- round prologue: crit count, last round's flips, chunk prefix
         if (threadIdx.x == 0) {
+            s_fmin = INT64_MAX;            // this round's flips in the chunk (phase C)
+            s_fmax = -1;
             s_crit = ld_cg(&a.scalars[PS_CRIT]);
             if (round > 0) {
                 const int64_t *f = flip + 3 * ((round - 1) % 3);
@@ -1097,6 +1124,7 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
         // residual update on this block's kernel chunk (planner.py:322-324)
         {
             int32_t flips = 0;
+            int64_t kmin = INT64_MAX, kmax = -1;     // this thread's flipped kernels
             int64_t *fs = flip + 3 * (round % 3);
             for (int rq = 0; rq < 4; rq += 2) {
                 int64_t lo = w.r[rq], hi = w.r[rq + 1];
@@ -1104,13 +1132,23 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
                 if (lo < x0) lo = x0;
                 if (hi > x1 - 1) hi = x1 - 1;
                 if (hi > N - 1) hi = N - 1;
-                // 4 kernels per thread per step, loads issued together
-                for (int64_t k0 = lo + threadIdx.x; k0 <= hi; k0 += 4 * (int64_t)blockDim.x) {
+                // 4 kernels per thread per step, loads issued together, the
+                // next step's loads in flight before this step's stores
+                const int64_t stp = 4 * (int64_t)blockDim.x;
+                int64_t ovn[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t k = lo + threadIdx.x + (int64_t)u * blockDim.x;
+                    ovn[u] = k <= hi ? ld_cg(&a.resid[k]) : 0;
+                }
+                for (int64_t k0 = lo + threadIdx.x; k0 <= hi; k0 += stp) {
                     int64_t ov[4];
 #pragma unroll
+                    for (int u = 0; u < 4; ++u) ov[u] = ovn[u];
+#pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const int64_t k = k0 + (int64_t)u * blockDim.x;
-                        ov[u] = k <= hi ? ld_cg(&a.resid[k]) : 0;
+                        const int64_t k = k0 + stp + (int64_t)u * blockDim.x;
+                        ovn[u] = k <= hi ? ld_cg(&a.resid[k]) : 0;
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -1120,19 +1158,26 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
                         a.resid[k] = nw;
                         if (ov[u] > cap && nw <= cap) {
                             ++flips;
-                            atomicMin(reinterpret_cast<unsigned long long *>(fs + 1), (unsigned long long)k);
-                            atomicMax(reinterpret_cast<long long *>(fs + 2), (long long)k);
+                            kmin = k < kmin ? k : kmin;
+                            kmax = k > kmax ? k : kmax;
                         }
                     }
                 }
             }
+            if (flips) {
+                atomicMin(reinterpret_cast<unsigned long long *>(&s_fmin), (unsigned long long)kmin);
+                atomicMax(reinterpret_cast<long long *>(&s_fmax), (long long)kmax);
+            }
             int32_t tf = block_sum<int32_t>(flips, reinterpret_cast<int32_t *>(sm_scan));
             __syncthreads();
             if (tf) {
-                rebuild_chunk();
+                const int64_t fmin = s_fmin;
+                rebuild_chunk(fmin);             // only the prefix from the first flip changes
                 if (threadIdx.x == 0) {
                     atomic_add_i64(&a.scalars[PS_CRIT], -(int64_t)tf);
                     atomic_add_i64(fs, (int64_t)tf);
+                    atomicMin(reinterpret_cast<unsigned long long *>(fs + 1), (unsigned long long)fmin);
+                    atomicMax(reinterpret_cast<long long *>(fs + 2), (long long)s_fmax);
                 }
             }
         }
@@ -1180,6 +1225,8 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
     }
     PROF(if (tb) for (int q = 0; q < 8; ++q) a.scalars[PS_DBG + q] = dbg[q]);
     PROF(if (tb) { a.scalars[PS_DBG + 11] = (int64_t)g_walk_total; a.scalars[PS_DBG + 12] = (int64_t)g_walk_max; });
+    PROF(if (tb) printf("[plan-profile] warp fit walks: %llu walks, %llu iterations (32 bookings each), longest %llu\n",
+                        g_wwalk_n, g_wwalk_total, g_wwalk_max));
     PROF(if (threadIdx.x == 0 && a.prof) for (int q = 0; q < 7; ++q) a.prof[8 * b + q] = slow[q]);
 #undef TICK
 #undef PROF

@@ -225,7 +225,13 @@ class PlanGroup:
         return all(torch.equal(x.cpu(), allh[0].cpu()) for x in allh)
 
     def close(self) -> None:
+        """Unmap the peers' mailboxes and free this rank's.  Collective: every
+        rank calls it (a barrier first, so no rank frees a mailbox a peer is
+        still writing into)."""
+        import torch.distributed as dist
         from . import _native
+        if dist.is_initialized():
+            dist.barrier(group=self.group)
         for ptr in self._mapped:
             try:
                 _native.mailbox_close(ptr)

@@ -209,8 +209,12 @@ class Step:
     """Model + optimizer + batch; `__call__()` runs one training step on the
     current stream and returns the loss tensor (on the device)."""
 
-    def __init__(self, c: LlamaConfig = LLAMA3_8B_MODEL, seed: int = 0, device="cuda"):
+    def __init__(self, c: LlamaConfig = LLAMA3_8B_MODEL, seed: int = 0, device="cuda", dp_group=None):
         self.c = c
+        # data parallel (configs C5): the gradients are all-reduced (mean) over
+        # the group between backward and the optimizer step; every rank runs
+        # the same seed, hence the same model, batch, trace and plan
+        self.dp_group = dp_group
         torch.manual_seed(seed)
         old = torch.get_default_dtype()
         torch.set_default_dtype(torch.bfloat16)
@@ -241,6 +245,12 @@ class Step:
         b = self.batch if batch is None else batch
         loss = self.model(b[:, :-1], b[:, 1:])
         loss.backward()
+        if self.dp_group is not None:
+            import torch.distributed as dist
+            world = dist.get_world_size(self.dp_group)
+            for p in self.model.parameters():
+                dist.all_reduce(p.grad, group=self.dp_group)
+                p.grad.div_(world)
         self.opt.step()
         return loss.detach()
 

@@ -82,3 +82,28 @@ def test_two_rank_line_on_one_gpu():
     assert d["config"]["plan_sha256"] == rec["plan_sha256"]
     assert d["config"]["plan_sha256_equal_on_all_ranks"] is True
     assert d["sharded_lifetime"]["bit_exact_vs_unsharded"] is True
+
+
+@pytest.mark.gpu
+def test_two_rank_data_parallel_offload_leg_on_one_gpu():
+    """Configs C5 path (bench.py --c5): two data-parallel ranks (gradient
+    all-reduce inside the step), each profiling, planning and running its own
+    online engine; here both ranks share cuda:0 (TIO_BENCH_ONE_GPU, gloo) on
+    the small model: identical plans, zero byte mismatches, a step-time ratio."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ, TIO_BENCH_ONE_GPU="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "c1", "--secondary", "",
+                          "--no-migration", "--c5", "--c5-fracs", "0.8", "--offload-model", "tiny"],
+                         capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    c5 = d["migration_dp"]
+    assert c5["ranks"] == 2 and c5["plans_identical"]
+    r = c5["runs"][0]
+    assert r["verify_mismatches"] == 0 and r["step_vs_ideal"] > 0
