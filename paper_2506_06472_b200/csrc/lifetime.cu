@@ -273,6 +273,8 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
         hb += __popc(hw);
         const bool in = live && e < ne && o < no;
         bool per = false;
+        int32_t akey = -1 - lane;                 // this lane's active-bytes RED: kernel (or a unique no-op key)
+        uint64_t asz = 0;
         if (in) {
             const int32_t beg = sm.ptr[o], nxt = sm.ptr[o + 1];
             const int32_t kk = sm.acc[e];
@@ -284,8 +286,9 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
             } else if ((uint32_t)kk >= (uint32_t)N) {
                 flags |= LF_ACCESS_RANGE;
             } else {
+                akey = kk;                                           // per_kernel_active_bytes (:111-117)
+                asz = (uint64_t)sz;
 #ifndef LT_NO_REDS
-                atomic_add_i64(&a.active[kk], sz);                   // per_kernel_active_bytes (:111-117)
                 if (!glob_t) {                                       // compute_memory_timeline (:97-108)
                     if (e == beg) atomic_add_i64(&a.diff[kk], sz);
                     if (e == nxt - 1) atomic_add_i64(&a.diff[kk + 1], -sz);
@@ -301,6 +304,9 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
                 }
             }
         }
+#ifndef LT_NO_REDS
+        if (akey >= 0) atomicAdd(reinterpret_cast<unsigned long long *>(&a.active[akey]), (unsigned long long)asz);
+#endif
         pb[st] = __ballot_sync(0xffffffffu, per);
         wcnt += __popc(pb[st]);
     }
