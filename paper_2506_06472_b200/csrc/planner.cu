@@ -309,6 +309,8 @@ __device__ __forceinline__ bool kbetter(const Key &a, const Key &b) {
     return (uint64_t)a.meta < (uint64_t)b.meta;   // tie: lowest candidate index = first in (tensor_id, start_kernel) order
 }
 
+__device__ __forceinline__ Key none_key() { return Key{0, 0, 1, 0}; }
+
 __device__ __forceinline__ Key kshfl(const Key &k, int src) {
     Key o;
     o.blo = __shfl_sync(0xffffffffu, k.blo, src);
@@ -457,6 +459,8 @@ __device__ __forceinline__ WinMsg msg_load(const WinMsg *src) {
 // win_gen; every block waits for win_gen and reads the winner.
 __device__ void round_winner(const PlanArgs &a, int64_t round, int G, Key *sm_key, WinMsg *out) {
     __shared__ int s_last;
+    __shared__ WinMsg s_msg;
+    __shared__ int s_pick, s_lost;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long *ctr = reinterpret_cast<unsigned long long *>(a.bar);
@@ -486,38 +490,64 @@ __device__ void round_winner(const PlanArgs &a, int64_t round, int G, Key *sm_ke
                 m.pre_e = m.pre_s + __ldg(&a.c_d[4 * c + q0 + 1]);
                 for (int q = 0; q < 4; ++q) m.r[q] = ld_cg(&a.rng[4 * c + q]);
             }
-            if (a.nranks > 1) {
-                // slot parity follows the tag, so it keeps alternating across
-                // consecutive planning calls (epoch += rounds + 2 between calls)
-                const unsigned long long tag = a.epoch + (unsigned long long)round + 1;
-                const int slot = (int)(tag & 1);
-                for (int p = 0; p < a.nranks; ++p) {
-                    Mailbox *mb = a.mb_peer[p];
-                    msg_store(&mb->msg[slot][a.rank], m);
-                    st_release_sys(&mb->flag[a.rank], tag);
-                }
-                Mailbox *me = a.mb_self;
-                // bounded wait: a rank that never arrives (died, or was never
-                // launched) ends this planning call with status 3 instead of
-                // hanging the GPU; the round then has no winner on this rank
-                const int64_t t0 = gtime();
-                bool lost = false;
-                unsigned spins = 0;
-                for (int p = 0; p < a.nranks && !lost; ++p)
-                    while (ld_acquire_sys(&me->flag[p]) < tag)
-                        if ((++spins & 1023u) == 0 && gtime() - t0 > EXCHANGE_TIMEOUT_NS) { lost = true; break; }
-                if (lost) {
-                    a.scalars[PS_STATUS] = 3;
-                    memset(&m, 0, sizeof(m));
-                } else {
-                    WinMsg best = msg_load(&me->msg[slot][0]);
-                    for (int p = 1; p < a.nranks; ++p) {
-                        const WinMsg o = msg_load(&me->msg[slot][p]);
-                        if (kbetter(o.k, best.k)) best = o;
-                    }
-                    m = best;
-                }
+            s_msg = m;
+            s_pick = 0;
+            s_lost = 0;
+        }
+        __syncthreads();
+        if (a.nranks > 1 && threadIdx.x < 32) {
+            // the exchange, one lane per rank p (in parallel): lane p puts
+            // this rank's message into rank p's mailbox and raises its flag
+            // there (release, system scope), then waits for rank p's flag in
+            // this rank's mailbox (acquire).  The slot parity follows the tag,
+            // so it keeps alternating across consecutive planning calls
+            // (epoch += rounds + 2 between calls).
+            const int lane = threadIdx.x;
+            const unsigned long long tag = a.epoch + (unsigned long long)round + 1;
+            const int slot = (int)(tag & 1);
+            const int R = a.nranks;
+            if (lane < R) {
+                Mailbox *mb = a.mb_peer[lane];
+                msg_store(&mb->msg[slot][a.rank], s_msg);
+                st_release_sys(&mb->flag[a.rank], tag);
             }
+            // bounded wait: a rank that never arrives (died, or was never
+            // launched) ends this planning call with status 3 instead of
+            // hanging the GPU; the round then has no winner on this rank
+            bool lost = false;
+            if (lane < R) {
+                const int64_t t0 = gtime();
+                unsigned spins = 0;
+                while (ld_acquire_sys(&a.mb_self->flag[lane]) < tag)
+                    if ((++spins & 1023u) == 0 && gtime() - t0 > EXCHANGE_TIMEOUT_NS) { lost = true; break; }
+            }
+            lost = __any_sync(0xffffffffu, lost);
+            // best of the R messages: ratio, then lowest candidate index
+            // (the same winner on every rank)
+            Key k = none_key();
+            if (!lost && lane < R) k = msg_load(&a.mb_self->msg[slot][lane]).k;
+            int who = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const Key ok = kshfl(k, (lane + o) & 31);
+                const int ow = __shfl_sync(0xffffffffu, who, (lane + o) & 31);
+                if (lane + o < 32 && kbetter(ok, k)) { k = ok; who = ow; }
+            }
+            if (lane == 0) {
+                if (lost) { s_lost = 1; a.scalars[PS_STATUS] = 3; }
+                s_pick = who;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                WinMsg m;
+                if (s_lost) memset(&m, 0, sizeof(m));
+                else m = msg_load(&a.mb_self->msg[slot][s_pick]);
+                s_msg = m;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const WinMsg m = s_msg;
 #ifdef TIO_VDEBUG
             printf("[vdbg] rank %d/%d round %lld blk %d: winner meta %llx blo %llx\n", a.rank, a.nranks,
                    (long long)round, (int)blockIdx.x, (unsigned long long)m.k.meta, (unsigned long long)m.k.blo);
