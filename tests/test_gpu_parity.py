@@ -422,38 +422,12 @@ def test_c2_host_tier_plan_prefix_vs_oracle():
     assert np.array_equal(g["residual"], o["residual"])
 
 
-def test_c2_host_tier_long_prefix_vs_oracle_fingerprint():
-    """Config C2 with the host tier (host 50,000 B/us, host_cap 256e9): the
-    first 14,000 commits of the device plan against the oracle's fingerprint
-    of the same prefix (tests/golden/c2host_prefix14000.json.gz, `make_c2.py
-    c2host 14000`: ~3 h of oracle time on 8 cores; the full ~33k-round
-    host-tier plan needs ~7 h)."""
-    import gzip
-    import json
-    import os
-    from conftest import ROOT
-    from paper_2506_06472_b200 import LLAMA3_8B, gen_llama_trace
-    from paper_2506_06472_b200.tracegen import llama_peak_bytes
-    path = os.path.join(ROOT, "tests", "golden", "c2host_prefix14000.json.gz")
-    if not os.path.exists(path):
-        pytest.skip("c2host prefix fingerprint not generated")
-    with gzip.open(path, "rt") as f:
-        rec = json.load(f)
-    tr = gen_llama_trace(LLAMA3_8B)
-    cap = llama_peak_bytes(tr) // 2
-    g = plan_device(tr, cap, ChannelRates.symmetric(16_000, host=50_000), rec["host_cap"],
-                    max_rounds=rec["max_rounds"])
-    assert int(g["info"].num_commits) == rec["num_commits"]
-    assert rec["host_commits"] > 1000
-    assert hashlib.sha256(g["plan_bytes"]).hexdigest() == rec["plan_sha256"]
-    assert hashlib.sha256(g["residual"].astype("<i8").tobytes()).hexdigest() == rec["residual_sha256"]
-
-
 def test_c2_host_tier_full_plan_vs_oracle_fingerprint():
     """Config C2 with the host tier of SURVEY §8(d) (host 50,000 B/us both
-    ways, host_cap 256e9), the WHOLE plan: plan bytes and residual timeline
-    against the oracle's fingerprint (tests/golden/c2host.json.gz, made by
-    tests/golden/make_c2.py c2host — hours of oracle time on the host's
+    ways, host_cap 256e9), the WHOLE plan (18,756 commits, 11,843 of them to
+    the host under the live host-cap test): plan bytes, residual timeline and
+    planned host bytes against the oracle's fingerprint
+    (tests/golden/c2host.json.gz, tests/golden/make_c2.py c2host: 374 s on 8
     cores)."""
     import gzip
     import json
