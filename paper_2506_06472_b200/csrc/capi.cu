@@ -655,6 +655,17 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
     a.st = st; a.place = place; a.rng = rng; a.hidx = hidx; a.hver = hver;
     a.ch_cap = ch_cap;
     a.occ_s = occ_s; a.occ_e = occ_e; a.occ_size = occ_z;
+    if (has_host) {                    // host-occupancy index (planner.cuh PlanArgs)
+        const int64_t nx = P + 1;
+        for (int bb = 0; bb < 2; ++bb) {
+            PTRY(A.alloc(&a.hx_s[bb], nx)); PTRY(A.alloc(&a.hx_sz[bb], nx));
+            PTRY(A.alloc(&a.hx_e[bb], nx)); PTRY(A.alloc(&a.hx_ez[bb], nx));
+            PTRY(A.alloc(&a.hx_ps[bb], nx)); PTRY(A.alloc(&a.hx_pe[bb], nx));
+            PTRY(A.alloc(&a.hx_a[bb], nx));
+        }
+        a.hx_nbmax = (P + 31) / 32 + 1;
+        PTRY(A.alloc(&a.hx_tab, HX_LEVELS * a.hx_nbmax));
+    }
     a.blk_best = blk_best; a.commits = p->commits; a.scalars = ps; a.c_tid = c_tid; a.c_tpos = c_tpos;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     PCUDA(cudaEventCreate(&ev0));
@@ -723,7 +734,9 @@ int tio_plan_create2(tio_trace *t, int64_t capacity, const tio_rates *rates, int
         PTRY(exclusive_scan(flag, pos, N, ovt, pos + N, s));
         k_over_write<<<grid_for(N), 256, 0, s>>>(flag, pos, N, p->over); ::tio::count_launch();
     }
-    k_planned_host<<<1, 256, 0, s>>>(occ_s, occ_e, occ_z, hs[PS_OCC], hostp); ::tio::count_launch();
+    PCUDA(cudaMemsetAsync(hostp, 0, 8, s));
+    k_planned_host<<<grid_for(hs[PS_OCC] > 0 ? hs[PS_OCC] : 1), 256, 0, s>>>(occ_s, occ_e, occ_z, hs[PS_OCC], hostp);
+    ::tio::count_launch();
     PTRY(A.alloc(&p->entries, 2 * nc));
     if (nc > 0) {
         const int64_t ne = 2 * nc;

@@ -176,18 +176,20 @@ __global__ void k_over_write(const int64_t *flag, const int64_t *pos, int64_t N,
 }
 
 __global__ void k_planned_host(const int64_t *os, const int64_t *oe, const int64_t *oz, int64_t h, int64_t *out) {
-    // _host_peak_occupancy over [min start, max end] (planner.py:354-358); all starts qualify
+    // _host_peak_occupancy over [min start, max end] (planner.py:354-358); all
+    // starts qualify, so it is the largest occupancy at any start: one start
+    // per thread over the grid, block maxima, atomicMax into *out (zeroed)
     __shared__ int64_t sm[40];
     int64_t best = 0;
-    for (int64_t p = threadIdx.x; p < h; p += blockDim.x) {
-        int64_t t = os[p], sum = 0;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < h; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = os[p];
+        int64_t sum = 0;
         for (int64_t j = 0; j < h; ++j)
             if (os[j] <= t && t < oe[j]) sum += oz[j];
         if (sum > best) best = sum;
     }
-    // block max via shuffles
     for (int o = 16; o > 0; o >>= 1) {
-        int64_t x = __shfl_xor_sync(0xffffffffu, best, o);
+        const int64_t x = __shfl_xor_sync(0xffffffffu, best, o);
         if (x > best) best = x;
     }
     if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = best;
@@ -195,7 +197,7 @@ __global__ void k_planned_host(const int64_t *os, const int64_t *oe, const int64
     if (threadIdx.x == 0) {
         int64_t m = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) if (sm[w] > m) m = sm[w];
-        *out = h > 0 ? m : 0;
+        if (m > 0) atomicMax(reinterpret_cast<long long *>(out), (long long)m);
     }
 }
 

@@ -240,6 +240,111 @@ __device__ int64_t host_peak(const int64_t *os, const int64_t *oe, const int64_t
     return peak;
 }
 
+// ---- host-occupancy index (see PlanArgs): the same maximum as host_peak in
+// O(log h): occ(p) = (sizes of starts <= p) - (sizes of ends <= p); the points
+// are lo and the starts in [lo, hi].
+__device__ __forceinline__ int64_t hx_ub(const int64_t *v, int64_t n, int64_t x) {   // first i: v[i] > x
+    int64_t lo = 0, hi = n;
+    while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (ld_cg(v + m) <= x) lo = m + 1; else hi = m; }
+    return lo;
+}
+__device__ __forceinline__ int64_t hx_lb(const int64_t *v, int64_t n, int64_t x) {   // first i: v[i] >= x
+    int64_t lo = 0, hi = n;
+    while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (ld_cg(v + m) < x) lo = m + 1; else hi = m; }
+    return lo;
+}
+__device__ int64_t host_peak_ix(const PlanArgs &a, int64_t h, int64_t lo, int64_t hi) {
+    if (h <= 0) return 0;
+    const int buf = (int)(h & 1);
+    const int64_t *S = a.hx_s[buf], *E = a.hx_e[buf], *A = a.hx_a[buf];
+    const int64_t us = hx_ub(S, h, lo), ue = hx_ub(E, h, lo);
+    int64_t peak = (us ? ld_cg(a.hx_ps[buf] + us) : 0) - (ue ? ld_cg(a.hx_pe[buf] + ue) : 0);
+    if (peak < 0) peak = 0;
+    const int64_t i0 = hx_lb(S, us, lo), i1 = hx_ub(S, h, hi);      // starts in [lo, hi]: [i0, i1)
+    if (i0 >= i1) return peak;
+    const int64_t b0 = i0 >> 5, b1 = (i1 - 1) >> 5;
+    int64_t m = INT64_MIN;
+    const int64_t e0 = b0 == b1 ? i1 : (b0 + 1) << 5;
+    for (int64_t i = i0; i < e0; ++i) { const int64_t v = ld_cg(A + i); m = v > m ? v : m; }
+    if (b1 > b0) {
+        for (int64_t i = b1 << 5; i < i1; ++i) { const int64_t v = ld_cg(A + i); m = v > m ? v : m; }
+        if (b1 - b0 >= 2) {                       // whole blocks b0+1 .. b1-1 from the table
+            const int64_t L = b0 + 1, R = b1;     // [L, R)
+            int l = 0;
+            while (((int64_t)2 << l) <= R - L) ++l;
+            const int64_t x = ld_cg(a.hx_tab + (int64_t)l * a.hx_nbmax + L);
+            const int64_t y = ld_cg(a.hx_tab + (int64_t)l * a.hx_nbmax + R - ((int64_t)1 << l));
+            m = x > m ? x : m;
+            m = y > m ? y : m;
+        }
+    }
+    return m > peak ? m : peak;
+}
+
+// Block 0, after a CPU commit of [s_new, e_new) x z: the index of h + 1
+// intervals into buffer (h + 1) & 1 from buffer h & 1 (one sorted insertion
+// per array; prefix sums and occupancies shift and add, no scan), then the
+// 32-start block maxima and the range-max table.
+__device__ void hx_insert(const PlanArgs &a, int64_t h, int64_t s_new, int64_t e_new, int64_t z,
+                          int64_t *sm_i) {
+    const int ob = (int)(h & 1), nbuf = (int)((h + 1) & 1);
+    const int64_t *S0 = a.hx_s[ob], *Z0 = a.hx_sz[ob], *E0 = a.hx_e[ob], *EZ0 = a.hx_ez[ob];
+    const int64_t *PS0 = a.hx_ps[ob], *PE0 = a.hx_pe[ob], *A0 = a.hx_a[ob];
+    int64_t *S1 = a.hx_s[nbuf], *Z1 = a.hx_sz[nbuf], *E1 = a.hx_e[nbuf], *EZ1 = a.hx_ez[nbuf];
+    int64_t *PS1 = a.hx_ps[nbuf], *PE1 = a.hx_pe[nbuf], *A1 = a.hx_a[nbuf];
+    if (threadIdx.x == 0) {
+        const int64_t ks = hx_ub(S0, h, s_new), ke = hx_ub(E0, h, e_new);
+        // occupancy at the new start: the old intervals over s_new, plus itself
+        const int64_t us = ks, ue = hx_ub(E0, h, s_new);
+        sm_i[0] = ks;
+        sm_i[1] = ke;
+        sm_i[2] = (us ? ld_cg(PS0 + us) : 0) - (ue ? ld_cg(PE0 + ue) : 0) + z;
+    }
+    __syncthreads();
+    const int64_t ks = sm_i[0], ke = sm_i[1], a_new = sm_i[2], n = h + 1;
+    for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) {
+        if (i < n) {
+            int64_t sv, zv, av;
+            if (i < ks) { sv = ld_cg(S0 + i); zv = ld_cg(Z0 + i); av = ld_cg(A0 + i); }
+            else if (i == ks) { sv = s_new; zv = z; av = a_new; }
+            else { sv = ld_cg(S0 + i - 1); zv = ld_cg(Z0 + i - 1); av = ld_cg(A0 + i - 1); }
+            if (i != ks && sv >= s_new && sv < e_new) av += z;     // the new interval holds this start
+            S1[i] = sv; Z1[i] = zv; A1[i] = av;
+            int64_t ev, ezv;
+            if (i < ke) { ev = ld_cg(E0 + i); ezv = ld_cg(EZ0 + i); }
+            else if (i == ke) { ev = e_new; ezv = z; }
+            else { ev = ld_cg(E0 + i - 1); ezv = ld_cg(EZ0 + i - 1); }
+            E1[i] = ev; EZ1[i] = ezv;
+        }
+        // prefix sums (n + 1 entries): shifted by the insertion, plus z after it
+        // (entry 0 of every prefix array is 0: never read from memory)
+        PS1[i] = i <= ks ? (i ? ld_cg(PS0 + i) : 0) : (i > 1 ? ld_cg(PS0 + i - 1) : 0) + z;
+        PE1[i] = i <= ke ? (i ? ld_cg(PE0 + i) : 0) : (i > 1 ? ld_cg(PE0 + i - 1) : 0) + z;
+    }
+    __syncthreads();
+    // 32-start block maxima = table level 0 (one warp per block of starts)
+    const int64_t nb = (n + 31) >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int64_t j = warp; j < nb; j += nw) {
+        const int64_t i = (j << 5) + lane;
+        int64_t v = i < n ? ld_cg(A1 + i) : INT64_MIN;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) { const int64_t w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
+        if (lane == 0) a.hx_tab[j] = v;
+    }
+    __syncthreads();
+    for (int l = 1; l < HX_LEVELS && ((int64_t)1 << l) <= nb; ++l) {
+        const int64_t half = (int64_t)1 << (l - 1);
+        const int64_t *src = a.hx_tab + (int64_t)(l - 1) * a.hx_nbmax;
+        int64_t *dst = a.hx_tab + (int64_t)l * a.hx_nbmax;
+        for (int64_t j = threadIdx.x; j + 2 * half <= nb; j += blockDim.x) {
+            const int64_t x = ld_cg(src + j), y = ld_cg(src + j + half);
+            dst[j] = x > y ? x : y;
+        }
+        __syncthreads();
+    }
+}
+
 // _covered_kernels (planner.py:232-250) as <= 2 kernel ranges
 __device__ void covered_ranges(const StartsView &starts, int64_t N, int64_t iteration,
                                int wraps, int32_t sk, int32_t ek, int32_t first, int32_t last,
@@ -804,7 +909,7 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
                     }
                     if (recap) {
                         int64_t lo = ld_cg(&a.place[4 * c + 2]) + d2, hi = ld_cg(&a.place[4 * c + 3]);
-                        int64_t occ = host_peak(a.occ_s, a.occ_e, a.occ_size, s_nocc, lo, hi);
+                        int64_t occ = host_peak_ix(a, s_nocc, lo, hi);
                         host = (occ + __ldg(&a.c_size[c]) > a.host_cap) ? H_CAPFAIL : H_OK;
                     }
                 }
@@ -1238,6 +1343,10 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
             }
         }
         __syncthreads();
+        if (b == 0 && w.dest == TIO_DEST_CPU) {
+            hx_insert(a, s_nocc, w.off_e, w.pre_s, w.size, reinterpret_cast<int64_t *>(sm_scan));
+            __syncthreads();
+        }
         if (threadIdx.x == 0) {
             last.dest = w.dest;
             for (int j = 0; j < nb; ++j) {

@@ -54,6 +54,8 @@ struct Mailbox {
     WinMsg msg[2][MAX_RANKS];
 };
 
+constexpr int HX_LEVELS = 26;      // range-max table levels (2^26 blocks of 32 starts)
+
 struct PlanArgs {
     int64_t N, P, iteration, capacity, host_cap;
     int32_t has_host;
@@ -96,6 +98,14 @@ struct PlanArgs {
     int64_t ch_cap;
     // host occupancy intervals (CPU commits)
     int64_t *occ_s, *occ_e, *occ_size;
+    // host-occupancy index (planner.py:179-186 as O(log h) queries), rebuilt
+    // by block 0 after every CPU commit; buffer (h & 1) holds the index of h
+    // intervals: starts / ends sorted with their sizes, prefix sums of the
+    // sizes (h + 1), occupancy at every sorted start, and a range-max table
+    // over 32-start blocks (single buffer: read only in phase E)
+    int64_t *hx_s[2], *hx_sz[2], *hx_e[2], *hx_ez[2], *hx_ps[2], *hx_pe[2], *hx_a[2];
+    int64_t *hx_tab;               // [HX_LEVELS x hx_nbmax]
+    int64_t hx_nbmax;
     // reduction + outputs
     Key *blk_best;                 // [grid]
     int64_t *prof;                 // [grid * 8] phase-E split per block (debug build)

@@ -448,3 +448,28 @@ def test_c2_host_tier_full_plan_vs_oracle_fingerprint():
     assert hashlib.sha256(g["plan_bytes"]).hexdigest() == rec["plan_sha256"]
     assert hashlib.sha256(g["residual"].astype("<i8").tobytes()).hexdigest() == rec["residual_sha256"]
     assert int(g["info"].planned_host_bytes) == rec["planned_host_bytes"]
+
+
+def test_c3_host_tier_full_plan_vs_oracle_fingerprint():
+    """Config C3 (9.9M events) with the host tier of SURVEY §8(d): the whole
+    plan against the oracle's fingerprint (tests/golden/c3host.json.gz,
+    tests/golden/make_c2.py c3host)."""
+    import gzip
+    import json
+    import os
+    from conftest import ROOT
+    from paper_2506_06472_b200 import LLAMA3_70B, gen_llama_trace
+    from paper_2506_06472_b200.tracegen import llama_peak_bytes
+    path = os.path.join(ROOT, "tests", "golden", "c3host.json.gz")
+    if not os.path.exists(path):
+        pytest.skip("c3host fingerprint not generated")
+    with gzip.open(path, "rt") as f:
+        rec = json.load(f)
+    tr = gen_llama_trace(LLAMA3_70B)
+    cap = llama_peak_bytes(tr) // 2
+    assert cap == rec["capacity"]
+    g = plan_device(tr, cap, ChannelRates.symmetric(16_000, host=50_000), rec["host_cap"])
+    assert int(g["info"].num_commits) == rec["num_commits"]
+    assert hashlib.sha256(g["plan_bytes"]).hexdigest() == rec["plan_sha256"]
+    assert hashlib.sha256(g["residual"].astype("<i8").tobytes()).hexdigest() == rec["residual_sha256"]
+    assert int(g["info"].planned_host_bytes) == rec["planned_host_bytes"]
