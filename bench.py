@@ -74,6 +74,11 @@ def _trace(config: str):
         tr = G.gen_llama_trace(G.LLAMA3_8B)
         cap = G.llama_peak_bytes(tr) // 2
         return tr, cap, ChannelRates.symmetric(16_000), 0, "C2 Llama-3-8B-shaped trace (Appendix C, 292 microbatches)"
+    if config in ("c2host", "c3host"):
+        tr = G.gen_llama_trace(G.LLAMA3_8B if config == "c2host" else G.LLAMA3_70B)
+        cap = G.llama_peak_bytes(tr) // 2
+        return tr, cap, ChannelRates.symmetric(16_000, host=50_000), 256 * 10**9, \
+            f"{config[:2].upper()} trace with the host tier (SURVEY 8d: host 50,000 B/us, host_cap 256e9)"
     if config == "c3":
         tr = G.gen_llama_trace(G.LLAMA3_70B)
         cap = G.llama_peak_bytes(tr) // 2
@@ -393,7 +398,8 @@ def measure(config: str, steps: int, warmup: int, dev, rank: int, world: int) ->
     return {
         "value": E * K / (tot_ms_max / 1e3), "ms_per_step": tot_ms_max / K,
         "config": {"workload": desc, "events": E, "kernels": N, "tensors": T, "periods": P,
-                   "capacity": cap, "rates": "ssd 16000 B/us symmetric", "host_cap": hc,
+                   "capacity": cap, "rates": ("ssd 16000 B/us symmetric" + (", host 50000 B/us" if hc else "")),
+                   "host_cap": hc,
                    "parallelism": (f"sharded{world}: one trace, candidate tiles split over ranks, per-round "
                                    f"winner exchange through CUDA-IPC mailboxes over NVLink") if world > 1
                    else "single",
@@ -490,6 +496,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     extra = None
     if args.secondary and args.secondary != args.config:
         extra = measure(args.secondary, args.steps, warm, dev, rank, world)
+    host_m = measure(args.host_leg, args.steps, warm, dev, rank, world) if args.host_leg else None
     c5 = c5_leg(args, rank, world) if args.c5 and world > 1 else None
     if rank != 0:
         return
@@ -513,6 +520,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         line["sharded_lifetime"] = m_sh
     if c5 is not None:
         line["migration_dp"] = c5
+    if host_m is not None:
+        host_m.pop("clocks", None)
+        host_m.pop("rounds", None)
+        line[args.host_leg] = host_m
     if not args.no_migration and world == 1:
         # C4 on one GPU; at N > 1 the per-rank pinned host extents (24-78 GB
         # each) would exceed the box's host memory, so the leg runs at N = 1 only
@@ -845,6 +856,8 @@ def main(argv=None):
                     help="headline workload (default C3: the north star's 10M-event trace)")
     ap.add_argument("--secondary", default="c2", choices=["", "c1", "c2", "c3", "llama1"],
                     help="second workload reported under its own key (default C2, BASELINE configs[1])")
+    ap.add_argument("--host-leg", default="c2host", choices=["", "c2host", "c3host"],
+                    help="also plan a trace with the host tier (reported under its own key)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-migration", action="store_true", help="skip the C4 offloaded-step leg")
     ap.add_argument("--offload-model", default="8b", choices=["8b", "tiny"],
