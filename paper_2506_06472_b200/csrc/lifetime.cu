@@ -37,7 +37,10 @@ enum : unsigned long long {
     LF_NOT_INCREASING = 16, LF_BAD_KIND = 32
 };
 
-constexpr int LT_EPT = 8;                           // events per thread
+#ifndef TIO_LT_EPT
+#define TIO_LT_EPT 8
+#endif
+constexpr int LT_EPT = TIO_LT_EPT;                         // events per thread
 constexpr int LT_TILE = LIFETIME_THREADS * LT_EPT;  // events per tile
 constexpr int LT_MAXO = LT_TILE + 2;                // staged tensors per tile
 #ifndef KT_THREADS

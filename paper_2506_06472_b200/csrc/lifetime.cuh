@@ -5,7 +5,10 @@
 
 namespace tio {
 
-constexpr int LIFETIME_THREADS = 256;
+#ifndef TIO_LT_THREADS
+#define TIO_LT_THREADS 256
+#endif
+constexpr int LIFETIME_THREADS = TIO_LT_THREADS;   // event-tile block size (build knob)
 
 // scalars[] slots shared by the lifetime and planner kernels
 enum { SC_GLOBAL_BYTES = 0, SC_NUM_PERIODS = 1, SC_FLAGS = 2, SC_IDS_UNSORTED = 3, SC_COUNT = 8 };
