@@ -284,47 +284,80 @@ __device__ int64_t host_peak_ix(const PlanArgs &a, int64_t h, int64_t lo, int64_
 // Block 0, after a CPU commit of [s_new, e_new) x z: the index of h + 1
 // intervals into buffer (h + 1) & 1 from buffer h & 1 (one sorted insertion
 // per array; prefix sums and occupancies shift and add, no scan), then the
-// 32-start block maxima and the range-max table.
+// 32-start block maxima and the range-max table.  The three insertion
+// searches run as 32-ary warp searches on warps 0-2; the shift loop keeps
+// four elements' loads in flight per thread.
 __device__ void hx_insert(const PlanArgs &a, int64_t h, int64_t s_new, int64_t e_new, int64_t z,
                           int64_t *sm_i) {
     const int ob = (int)(h & 1), nbuf = (int)((h + 1) & 1);
-    const int64_t *S0 = a.hx_s[ob], *Z0 = a.hx_sz[ob], *E0 = a.hx_e[ob], *EZ0 = a.hx_ez[ob];
-    const int64_t *PS0 = a.hx_ps[ob], *PE0 = a.hx_pe[ob], *A0 = a.hx_a[ob];
-    int64_t *S1 = a.hx_s[nbuf], *Z1 = a.hx_sz[nbuf], *E1 = a.hx_e[nbuf], *EZ1 = a.hx_ez[nbuf];
-    int64_t *PS1 = a.hx_ps[nbuf], *PE1 = a.hx_pe[nbuf], *A1 = a.hx_a[nbuf];
-    if (threadIdx.x == 0) {
-        const int64_t ks = hx_ub(S0, h, s_new), ke = hx_ub(E0, h, e_new);
-        // occupancy at the new start: the old intervals over s_new, plus itself
-        const int64_t us = ks, ue = hx_ub(E0, h, s_new);
-        sm_i[0] = ks;
-        sm_i[1] = ke;
-        sm_i[2] = (us ? ld_cg(PS0 + us) : 0) - (ue ? ld_cg(PE0 + ue) : 0) + z;
+    const int64_t *__restrict__ S0 = a.hx_s[ob];
+    const int64_t *__restrict__ Z0 = a.hx_sz[ob];
+    const int64_t *__restrict__ E0 = a.hx_e[ob];
+    const int64_t *__restrict__ EZ0 = a.hx_ez[ob];
+    const int64_t *__restrict__ PS0 = a.hx_ps[ob];
+    const int64_t *__restrict__ PE0 = a.hx_pe[ob];
+    const int64_t *__restrict__ A0 = a.hx_a[ob];
+    int64_t *__restrict__ S1 = a.hx_s[nbuf];
+    int64_t *__restrict__ Z1 = a.hx_sz[nbuf];
+    int64_t *__restrict__ E1 = a.hx_e[nbuf];
+    int64_t *__restrict__ EZ1 = a.hx_ez[nbuf];
+    int64_t *__restrict__ PS1 = a.hx_ps[nbuf];
+    int64_t *__restrict__ PE1 = a.hx_pe[nbuf];
+    int64_t *__restrict__ A1 = a.hx_a[nbuf];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (warp < 3) {
+        // ks = first start > s_new, ke = first end > e_new, ue = first end > s_new
+        const int64_t *v = warp == 0 ? S0 : E0;
+        const int64_t x = warp == 1 ? e_new : s_new;
+        const int64_t r = warp_lower_bound(0, h, [&](int64_t j) { return ld_cg(v + j) > x; });
+        if (lane == 0) sm_i[warp] = r;
     }
     __syncthreads();
-    const int64_t ks = sm_i[0], ke = sm_i[1], a_new = sm_i[2], n = h + 1;
-    for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) {
-        if (i < n) {
-            int64_t sv, zv, av;
-            if (i < ks) { sv = ld_cg(S0 + i); zv = ld_cg(Z0 + i); av = ld_cg(A0 + i); }
-            else if (i == ks) { sv = s_new; zv = z; av = a_new; }
-            else { sv = ld_cg(S0 + i - 1); zv = ld_cg(Z0 + i - 1); av = ld_cg(A0 + i - 1); }
-            if (i != ks && sv >= s_new && sv < e_new) av += z;     // the new interval holds this start
-            S1[i] = sv; Z1[i] = zv; A1[i] = av;
-            int64_t ev, ezv;
-            if (i < ke) { ev = ld_cg(E0 + i); ezv = ld_cg(EZ0 + i); }
-            else if (i == ke) { ev = e_new; ezv = z; }
-            else { ev = ld_cg(E0 + i - 1); ezv = ld_cg(EZ0 + i - 1); }
-            E1[i] = ev; EZ1[i] = ezv;
+    const int64_t ks = sm_i[0], ke = sm_i[1], ue = sm_i[2], n = h + 1;
+    const int64_t bd = blockDim.x;
+    for (int64_t i0 = threadIdx.x; i0 <= n; i0 += 4 * bd) {
+        int64_t sv[4], zv[4], av[4], ev[4], ezv[4], ps[4], pe[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * bd;
+            sv[u] = zv[u] = av[u] = ev[u] = ezv[u] = ps[u] = pe[u] = 0;
+            if (i > n) continue;
+            if (i < n) {
+                if (i != ks) {
+                    const int64_t si = i < ks ? i : i - 1;
+                    sv[u] = ld_cg(S0 + si); zv[u] = ld_cg(Z0 + si); av[u] = ld_cg(A0 + si);
+                } else {
+                    // occupancy at the new start: the old intervals over s_new, plus itself
+                    av[u] = (ks ? ld_cg(PS0 + ks) : 0) - (ue ? ld_cg(PE0 + ue) : 0);
+                }
+                if (i != ke) {
+                    const int64_t ei = i < ke ? i : i - 1;
+                    ev[u] = ld_cg(E0 + ei); ezv[u] = ld_cg(EZ0 + ei);
+                }
+            }
+            // prefix sums (n + 1 entries; entry 0 is 0 and never read)
+            const int64_t pi = i <= ks ? i : i - 1, qi = i <= ke ? i : i - 1;
+            ps[u] = pi ? ld_cg(PS0 + pi) : 0;
+            pe[u] = qi ? ld_cg(PE0 + qi) : 0;
         }
-        // prefix sums (n + 1 entries): shifted by the insertion, plus z after it
-        // (entry 0 of every prefix array is 0: never read from memory)
-        PS1[i] = i <= ks ? (i ? ld_cg(PS0 + i) : 0) : (i > 1 ? ld_cg(PS0 + i - 1) : 0) + z;
-        PE1[i] = i <= ke ? (i ? ld_cg(PE0 + i) : 0) : (i > 1 ? ld_cg(PE0 + i - 1) : 0) + z;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * bd;
+            if (i > n) continue;
+            if (i < n) {
+                if (i == ks) { sv[u] = s_new; zv[u] = z; av[u] += z; }
+                else if (sv[u] >= s_new && sv[u] < e_new) av[u] += z;      // the new interval holds this start
+                if (i == ke) { ev[u] = e_new; ezv[u] = z; }
+                S1[i] = sv[u]; Z1[i] = zv[u]; A1[i] = av[u];
+                E1[i] = ev[u]; EZ1[i] = ezv[u];
+            }
+            PS1[i] = ps[u] + (i > ks ? z : 0);
+            PE1[i] = pe[u] + (i > ke ? z : 0);
+        }
     }
     __syncthreads();
     // 32-start block maxima = table level 0 (one warp per block of starts)
     const int64_t nb = (n + 31) >> 5;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int64_t j = warp; j < nb; j += nw) {
         const int64_t i = (j << 5) + lane;
         int64_t v = i < n ? ld_cg(A1 + i) : INT64_MIN;
