@@ -325,8 +325,12 @@ int tio_lifetime(tio_trace *t, void *stream) {
         TIO_CUDA(cudaMemsetAsync(t->diff, 0, 8 * (t->N + 1), s));   // the kernel re-zeroes it behind its scan
         TIO_TRY(t->arena.alloc(&t->scalars, SC_COUNT));
     }
-    TIO_CUDA(cudaMemsetAsync(t->active, 0, 8 * (t->N > 0 ? t->N : 1), s));
-    TIO_CUDA(cudaMemsetAsync(t->scalars, 0, 8 * SC_COUNT, s));
+    // active bytes and the scalars are zeroed by the stage's first kernel
+    // (k_tile_owners) — or here when it has no kernels
+    if (t->N == 0) {
+        TIO_CUDA(cudaMemsetAsync(t->active, 0, 8, s));
+        TIO_CUDA(cudaMemsetAsync(t->scalars, 0, 8 * SC_COUNT, s));
+    }
     if (t->T == 0) TIO_CUDA(cudaMemsetAsync(t->tpp, 0, 8, s));
     LifetimeArgs a;
     a.N = t->N; a.T = t->T; a.E = t->E;

@@ -168,11 +168,23 @@ __device__ void agg_prefix(const int64_t *st, int64_t sst, const int64_t *grp, i
 // owner[t] = largest i in [0, T) with ptr[i] <= e_t, e_t = min(t * LT_TILE, E - 1)
 // Also zeroes the tile counters and the look-back status words for the two
 // kernels that follow (work[0, 2) and zero[0, nzero)).
+// It also zeroes the stage's accumulators (active bytes, scalars): one
+// launch instead of three memsets ahead of the stage.
 __global__ void k_tile_owners(const int64_t *ptr, int64_t T, int64_t E, int64_t ntiles, int64_t *owner,
-                              int64_t *work, int64_t *zero, int64_t nzero) {
+                              int64_t *work, int64_t *zero, int64_t nzero, int64_t *active, int64_t N,
+                              int64_t *scalars) {
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     if (gtid < 2) work[gtid] = 0;
-    for (int64_t i = gtid; i < nzero; i += (int64_t)gridDim.x * blockDim.x) zero[i] = 0;
+    if (gtid < SC_COUNT) scalars[gtid] = 0;
+    for (int64_t i = gtid; i < nzero; i += nthr) zero[i] = 0;
+    if (((uintptr_t)active & 15) == 0) {
+        longlong2 *a2 = reinterpret_cast<longlong2 *>(active);
+        for (int64_t i = gtid; i < (N >> 1); i += nthr) a2[i] = make_longlong2(0, 0);
+        if ((N & 1) && gtid == 0) active[N - 1] = 0;
+    } else {
+        for (int64_t i = gtid; i < N; i += nthr) active[i] = 0;
+    }
     const int64_t warp = gtid >> 5;
     if (warp > ntiles) return;
     int64_t e = warp * LT_TILE;
@@ -503,11 +515,14 @@ int launch_lifetime(const LifetimeArgs &args, cudaStream_t stream) {
     if (NTe > 0) {
         const int64_t thr = 32 * (NTe + 1);
         k_tile_owners<<<(unsigned)((thr + 255) / 256), 256, 0, stream>>>(args.ptr, args.T, args.E, NTe, args.work + 2,
-                                                                          args.work, status, nstatus);
+                                                                          args.work, status, nstatus, args.active,
+                                                                          args.N, args.scalars);
         count_launch();
     } else {
         TIO_CUDA(cudaMemsetAsync(args.work, 0, sizeof(int64_t) * 2, stream));
         TIO_CUDA(cudaMemsetAsync(status, 0, sizeof(int64_t) * nstatus, stream));
+        TIO_CUDA(cudaMemsetAsync(args.active, 0, sizeof(int64_t) * (args.N > 0 ? args.N : 1), stream));
+        TIO_CUDA(cudaMemsetAsync(args.scalars, 0, sizeof(int64_t) * SC_COUNT, stream));
     }
     // the next two kernels launch programmatically (PDL): their blocks become
     // resident while the previous grid drains and wait in griddepcontrol.wait
