@@ -35,7 +35,8 @@ def test_reference_arm_line_on_cpu():
 
 @pytest.mark.gpu
 def test_our_arm_line_on_gpu():
-    d = _run(["--config", "llama1", "--secondary", "c1", "--steps", "3", "--warmup", "3", "--no-migration"])
+    d = _run(["--config", "llama1", "--secondary", "c1", "--host-leg", "", "--steps", "3", "--warmup", "3",
+              "--no-migration"])
     assert BASE_KEYS <= set(d)
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["dtype"] == "int64"
     r = d["roofline"]
@@ -70,7 +71,8 @@ def test_two_rank_line_on_one_gpu():
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
                           "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "llama1", "--secondary", "c1",
-                          "--no-migration"], capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+                          "--host-leg", "", "--no-migration"], capture_output=True, text=True, timeout=900, cwd=ROOT,
+                         env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout
@@ -99,7 +101,7 @@ def test_two_rank_data_parallel_offload_leg_on_one_gpu():
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
                           "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "c1", "--secondary", "",
-                          "--no-migration", "--c5", "--c5-fracs", "0.8", "--offload-model", "tiny"],
+                          "--host-leg", "", "--no-migration", "--c5", "--c5-fracs", "0.8", "--offload-model", "tiny"],
                          capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
