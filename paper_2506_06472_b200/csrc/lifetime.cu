@@ -164,6 +164,48 @@ __device__ void agg_prefix(const int64_t *st, int64_t sst, const int64_t *grp, i
     for (int c = 0; c < NCH; ++c) prefix[c] = warp_sum<int64_t>(acc[c]);
 }
 
+// The event chain's group words pack {count, sum} into one 64-bit word
+// (count << 40 | sum: a tile has at most LT_TILE periods, so a group's sum
+// stays below 2^17): a relaxed RED publishes both, a relaxed load reads both —
+// no release on the publishing side, no fence and no second load on the
+// reading side.
+constexpr int GP_SHIFT = 40;
+__device__ __forceinline__ void agg_publish_packed(int64_t *st, int64_t *grp, int64_t tile, int64_t agg) {
+    if ((threadIdx.x & 31) == 0) {
+        status_store(st, tile, agg, 1);
+        const unsigned long long w = (1ull << GP_SHIFT) + (unsigned long long)agg;
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(grp + 2 * (tile / LB_GROUP)), "l"(w) : "memory");
+    }
+}
+__device__ int64_t agg_prefix_packed(const int64_t *st, const int64_t *grp, int64_t tile) {
+    constexpr int U = 4;
+    const int lane = threadIdx.x & 31;
+    const int64_t g = tile / LB_GROUP;
+    const int64_t j = g * LB_GROUP + lane;
+    int64_t tv = 0, tf = 1, acc = 0;
+    if (j < tile) status_load(st, j, &tv, &tf);
+    for (int64_t q0 = lane; q0 < g; q0 += 32 * U) {
+        long long n[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            n[u] = (long long)LB_GROUP << GP_SHIFT;
+            if (q0 + 32 * u < g)
+                asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(n[u]) : "l"(grp + 2 * (q0 + 32 * u)) : "memory");
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            while ((n[u] >> GP_SHIFT) < LB_GROUP)
+                asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(n[u]) : "l"(grp + 2 * (q0 + 32 * u)) : "memory");
+            if (q0 + 32 * u < g) acc += n[u] & ((1ll << GP_SHIFT) - 1);
+        }
+    }
+    if (j < tile) {
+        while (tf == 0) status_load(st, j, &tv, &tf);
+        acc += tv;
+    }
+    return warp_sum<int64_t>(acc);
+}
+
 // ---------------------------------------------------------------- owners
 // owner[t] = largest i in [0, T) with ptr[i] <= e_t, e_t = min(t * LT_TILE, E - 1)
 // Also zeroes the tile counters and the look-back status words for the two
@@ -345,9 +387,8 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
         fall |= sm.wflags[w];
     }
     if (warp == 0) {
-        agg_publish(est, egrp, tile, tot);
-        int64_t pre;
-        agg_prefix<1>(est, 0, egrp, 0, tile, &pre);
+        agg_publish_packed(est, egrp, tile, tot);
+        const int64_t pre = agg_prefix_packed(est, egrp, tile);
         if (lane == 0) {
             sm.prefix = pre;
             if (gsum) atomic_add_i64(&a.scalars[SC_GLOBAL_BYTES], gsum);
