@@ -5,8 +5,8 @@
 //
 //   k_tile_owners  owner tensor of every event-tile boundary (32-ary warp
 //                  searches over the CSR offsets).
-//   k_events       one tile of LT_TILE events per block (tiles claimed in
-//                  order from an atomic counter), walked warp-contiguously
+//   k_events       one tile of LT_TILE events per block (tile = blockIdx),
+//                  walked warp-contiguously
 //                  (lane = event) with owners from a tensor-head bitmask:
 //                    active[k] += size                (per_kernel_active_bytes, :111-117)
 //                    diff[first] += size, diff[last+1] -= size for intermediates
@@ -62,9 +62,12 @@ __host__ __device__ int64_t lifetime_kernel_tiles(int64_t N) { return (N + KT_TI
 // aggregate {value, flag} and adds it into its group of LB_GROUP tiles
 // ({sum, count}); a tile's exclusive prefix is the sum of the complete groups
 // before its own plus the aggregates of the earlier tiles of its group, all
-// loaded in parallel by one warp.  Tiles are claimed in order from an atomic
-// ticket, so every earlier tile is resident or finished and publishes without
-// waiting on anything: the wait is for the slowest predecessor's publish, not
+// loaded in parallel by one warp.  A block's tile is its blockIdx: blocks of
+// a 1-D grid are dispatched in index order (the premise of CUB's single-pass
+// scan, which also takes its tile from blockIdx), so every earlier tile is
+// resident or finished and publishes without waiting on anything (an atomic
+// ticket per block measured 4% slower at C3: one more L2 round trip ahead of
+// every tile's loads): the wait is for the slowest predecessor's publish, not
 // for a chain of inclusive prefixes (a decoupled look-back's inclusive
 // frontier advances ~64 tiles per L2 round trip — at C3's 4,851 event tiles
 // that chain was the k_events time).
@@ -208,8 +211,8 @@ __device__ int64_t agg_prefix_packed(const int64_t *st, const int64_t *grp, int6
 
 // ---------------------------------------------------------------- owners
 // owner[t] = largest i in [0, T) with ptr[i] <= e_t, e_t = min(t * LT_TILE, E - 1)
-// Also zeroes the tile counters and the look-back status words for the two
-// kernels that follow (work[0, 2) and zero[0, nzero)).
+// Also zeroes the look-back status words for the two kernels that follow
+// (zero[0, nzero); work[0, 2) are spare counters).
 // It also zeroes the stage's accumulators (active bytes, scalars): one
 // launch instead of three memsets ahead of the stage.
 __global__ void k_tile_owners(const int64_t *ptr, int64_t T, int64_t E, int64_t ntiles, int64_t *owner,
@@ -271,7 +274,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     const int32_t no = (int32_t)(o1 - o0 + 1);
     const bool staged = no <= LT_MAXO;
 
-    // ---- staging; the head mask (zeroed before the ticket barrier)
+    // ---- staging; the head mask (zeroed before the first barrier)
     if (((uintptr_t)a.acc & 15) == 0 && ne == LT_TILE) {
         const int4 *q = reinterpret_cast<const int4 *>(a.acc + e0);
         for (int i = threadIdx.x; i < LT_TILE / 4; i += LIFETIME_THREADS)
@@ -294,7 +297,11 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     // tensor-table slice (validation, globals' bytes)
     int64_t glob = 0;
     {
+#ifdef LT_NO_TABLE
+        const int64_t per = 0;
+#else
         const int64_t per = (T + NTe - 1) / NTe;
+#endif
         const int64_t i0 = tile * per, i1 = i0 + per < T ? i0 + per : T;
         for (int64_t i = i0 + threadIdx.x; i < i1; i += LIFETIME_THREADS) {
             if (__ldg(a.ptr + i + 1) <= __ldg(a.ptr + i)) flags |= LF_BAD_PTR;
@@ -445,7 +452,7 @@ k_events(LifetimeArgs a) {
     EvSmem &sm = *reinterpret_cast<EvSmem *>(smraw);
     const int64_t NTe = lifetime_event_tiles(a.E);
     for (int i = threadIdx.x; i < LT_TILE / 32; i += blockDim.x) sm.head[i] = 0;
-    if (threadIdx.x == 0) sm.tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(a.work), 1ull);
+    if (threadIdx.x == 0) sm.tile = blockIdx.x;
     __syncthreads();
     const int64_t tile = sm.tile;
     const LtWork w = lt_work(a.work, a.N, a.E);
@@ -467,7 +474,7 @@ k_kernels(LifetimeArgs a) {
     const int64_t N = a.N, E = a.E;
     const int64_t NTe = lifetime_event_tiles(E), NTk = lifetime_kernel_tiles(N);
     const LtWork w = lt_work(a.work, N, E);                     // dur chain, then diff chain
-    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(a.work + 1), 1ull);
+    if (threadIdx.x == 0) s_tile = blockIdx.x;
     // the globals' bytes (k_events' sum) load early, beside the tile's loads
     const int64_t gbytes = __ldcg(reinterpret_cast<const long long *>(&a.scalars[SC_GLOBAL_BYTES]));
     __syncthreads();

@@ -450,6 +450,34 @@ def test_c2_host_tier_full_plan_vs_oracle_fingerprint():
     assert int(g["info"].planned_host_bytes) == rec["planned_host_bytes"]
 
 
+def test_c3_host_tier_plan_prefix_vs_oracle_fingerprint():
+    """Config C3 (9.9M events) with the host tier of SURVEY §8(d) (host 50,000
+    B/us both ways, host_cap 256e9): the first 1,700 commits of the device plan
+    against the oracle's (tests/golden/c3host_prefix1700.json.gz,
+    tests/golden/make_c2.py c3host 1700: 718 s on 8 cores) — plan bytes,
+    residual timeline and planned host bytes.  669 of the 1,700 commits go to
+    the host under the live host-cap test, at the 10M-event scale (the whole
+    C3 host-tier plan, ~52k rounds, is out of the oracle's reach)."""
+    import gzip
+    import json
+    import os
+    from conftest import ROOT
+    from paper_2506_06472_b200 import LLAMA3_70B, gen_llama_trace
+    from paper_2506_06472_b200.tracegen import llama_peak_bytes
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "c3host_prefix1700.json.gz"), "rt") as f:
+        rec = json.load(f)
+    tr = gen_llama_trace(LLAMA3_70B)
+    cap = llama_peak_bytes(tr) // 2
+    assert cap == rec["capacity"]
+    R = rec["max_rounds"]
+    g = plan_device(tr, cap, ChannelRates.symmetric(16_000, host=50_000), rec["host_cap"], max_rounds=R)
+    assert int(g["info"].num_commits) == rec["num_commits"] == R
+    assert rec["host_commits"] >= 600                                   # the host tier is exercised
+    assert hashlib.sha256(g["plan_bytes"]).hexdigest() == rec["plan_sha256"]
+    assert hashlib.sha256(g["residual"].astype("<i8").tobytes()).hexdigest() == rec["residual_sha256"]
+    assert int(g["info"].planned_host_bytes) == rec["planned_host_bytes"]
+
+
 def test_c3_host_tier_full_plan_vs_oracle_fingerprint():
     """Config C3 (9.9M events) with the host tier of SURVEY §8(d): the whole
     plan against the oracle's fingerprint (tests/golden/c3host.json.gz,
