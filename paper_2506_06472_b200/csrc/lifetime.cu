@@ -6,7 +6,8 @@
 //   k_tile_owners  owner tensor of every event-tile boundary (32-ary warp
 //                  searches over the CSR offsets).
 //   k_events       one tile of LT_TILE events per block (tile = blockIdx),
-//                  walked warp-contiguously
+//                  walked warp-contiguously (periods and checks; the atomics
+//                  go out after the tile's period count is published)
 //                  (lane = event) with owners from a tensor-head bitmask:
 //                    active[k] += size                (per_kernel_active_bytes, :111-117)
 //                    diff[first] += size, diff[last+1] -= size for intermediates
@@ -337,27 +338,16 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
         hb += __popc(hw);
         const bool in = live && e < ne && o < no;
         bool per = false;
-        int32_t akey = -1 - lane;                 // this lane's active-bytes RED: kernel (or a unique no-op key)
-        uint64_t asz = 0;
         if (in) {
             const int32_t beg = sm.ptr[o], nxt = sm.ptr[o + 1];
             const int32_t kk = sm.acc[e];
             const uint64_t sk = sm.sk[o];
             const bool glob_t = sk >> 63;
-            const int64_t sz = (int64_t)(sk & ~(1ull << 63));
             if (e < beg || e >= nxt) {
                 flags |= LF_BAD_PTR;
             } else if ((uint32_t)kk >= (uint32_t)N) {
                 flags |= LF_ACCESS_RANGE;
             } else {
-                akey = kk;                                           // per_kernel_active_bytes (:111-117)
-                asz = (uint64_t)sz;
-#ifndef LT_NO_REDS
-                if (!glob_t) {                                       // compute_memory_timeline (:97-108)
-                    if (e == beg) atomic_add_i64(&a.diff[kk], sz);
-                    if (e == nxt - 1) atomic_add_i64(&a.diff[kk + 1], -sz);
-                }
-#endif
                 if (e != nxt - 1) {
                     const int32_t k2 = sm.acc[e + 1];
                     if (k2 <= kk) flags |= LF_NOT_INCREASING;
@@ -368,9 +358,6 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
                 }
             }
         }
-#ifndef LT_NO_REDS
-        if (akey >= 0) atomicAdd(reinterpret_cast<unsigned long long *>(&a.active[akey]), (unsigned long long)asz);
-#endif
         pb[st] = __ballot_sync(0xffffffffu, per);
         wcnt += __popc(pb[st]);
     }
@@ -393,8 +380,46 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
         gsum += sm.wglob[w];
         fall |= sm.wflags[w];
     }
+    // ---- the tile's atomics: per_kernel_active_bytes (:111-117) and the
+    // timeline difference array of the intermediates (compute_memory_timeline,
+    // :97-108).  They go out after the tile's period count is published
+    // (warp 0: publish, atomics, then its predecessors' counts; warps 1-7
+    // straight away), overlapping the wait for the predecessors instead of
+    // delaying this tile's publish, which its successors wait on (issued
+    // inside the walk they cost C3 182 -> 164 us).  Only for a tile whose
+    // events all passed the walk's checks (indices in range).
+    auto tile_reds = [&]() {
+#ifndef LT_NO_REDS
+        if (fall) return;
+        int32_t h2 = 0;
+        for (int j = lane; j < (wbase >> 5); j += 32) h2 += __popc(sm.head[j]);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) h2 += __shfl_xor_sync(0xffffffffu, h2, d);
+#pragma unroll
+        for (int st = 0; st < STEPS; ++st) {
+            const int32_t e = wbase + st * 32 + lane;
+            const uint32_t hw = sm.head[(wbase >> 5) + st];
+            const int32_t o = h2 + __popc(hw & le);
+            h2 += __popc(hw);
+            if (e < ne && o < no) {
+                const int32_t beg = sm.ptr[o], nxt = sm.ptr[o + 1];
+                const int32_t kk = sm.acc[e];
+                const uint64_t sk = sm.sk[o];
+                const int64_t sz = (int64_t)(sk & ~(1ull << 63));
+                atomicAdd(reinterpret_cast<unsigned long long *>(&a.active[kk]), (unsigned long long)sz);
+                if (!(sk >> 63)) {
+                    if (e == beg) atomic_add_i64(&a.diff[kk], sz);
+                    if (e == nxt - 1) atomic_add_i64(&a.diff[kk + 1], -sz);
+                }
+            }
+        }
+#endif
+    };
+    if (warp != 0) tile_reds();
+
     if (warp == 0) {
         agg_publish_packed(est, egrp, tile, tot);
+        tile_reds();
         const int64_t pre = agg_prefix_packed(est, egrp, tile);
         if (lane == 0) {
             sm.prefix = pre;
