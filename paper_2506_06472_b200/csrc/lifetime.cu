@@ -493,6 +493,7 @@ k_events(LifetimeArgs a) {
 __global__ void __launch_bounds__(KT_THREADS, KT_MINB)
 k_kernels(LifetimeArgs a) {
     asm volatile("griddepcontrol.wait;" ::: "memory");      // k_events complete (programmatic launch)
+    static_assert(KT_THREADS <= 512, "scan[] holds 16 warp totals per chain");
     __shared__ int64_t scan[40];
     __shared__ int64_t s_pre[2];
     __shared__ int64_t s_tile;
@@ -532,9 +533,20 @@ k_kernels(LifetimeArgs a) {
         sf += df[j];
     }
     if (flags) atomicOr(reinterpret_cast<unsigned long long *>(&a.scalars[SC_FLAGS]), flags);
-    int64_t agg[2];
-    int64_t xd = block_exclusive_sum<int64_t>(sd, scan, &agg[0]);
-    int64_t xf = block_exclusive_sum<int64_t>(sf, scan, &agg[1]);
+    // both chains in one exchange: warp-level inclusive scans, the warp totals
+    // through shared memory, one barrier; warp 0 then publishes the tile's
+    // aggregates and resolves its prefix (one more barrier)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t id = warp_inclusive_sum<int64_t>(sd), iff = warp_inclusive_sum<int64_t>(sf);
+    if (lane == 31) { scan[warp] = id; scan[16 + warp] = iff; }
+    __syncthreads();
+    int64_t xd = id - sd, xf = iff - sf, agg[2] = {0, 0};
+#pragma unroll
+    for (int q = 0; q < KT_THREADS / 32; ++q) {
+        const int64_t vd = scan[q], vf = scan[16 + q];
+        if (q < warp) { xd += vd; xf += vf; }
+        agg[0] += vd; agg[1] += vf;
+    }
     if (threadIdx.x < 32) {
         agg_publish(w.kst, w.kgrp, tile, agg[0]);
         agg_publish(w.kst + 2 * NTk, w.kgrp + 2 * lb_groups(NTk), tile, agg[1]);
