@@ -278,13 +278,19 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     // ---- staging; the head mask (zeroed before the first barrier)
     if (((uintptr_t)a.acc & 15) == 0 && ne == LT_TILE) {
         const int4 *q = reinterpret_cast<const int4 *>(a.acc + e0);
-        for (int i = threadIdx.x; i < LT_TILE / 4; i += LIFETIME_THREADS)
-            reinterpret_cast<int4 *>(sm.acc)[i] = __ldg(q + i);
+        // asynchronous copies: the thread goes on to issue the CSR-slice and
+        // tensor-table loads while the access column lands in shared memory
+        for (int i = threadIdx.x; i < LT_TILE / 4; i += LIFETIME_THREADS) {
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(reinterpret_cast<int4 *>(sm.acc) + i);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(q + i) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     } else {
         for (int i = threadIdx.x; i < ne; i += LIFETIME_THREADS) sm.acc[i] = __ldg(a.acc + e0 + i);
     }
     if (threadIdx.x == 0) sm.acc[ne] = e1 < E ? __ldg(a.acc + e1) : 0;
     if (staged) {
+#pragma unroll 2                       // two tensors' loads in flight per thread
         for (int32_t i = threadIdx.x; i <= no; i += LIFETIME_THREADS) {
             const int64_t p = (o0 + i <= T) ? __ldg(a.ptr + o0 + i) : E;
             const int64_t r = p - e0;
@@ -304,6 +310,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
         const int64_t per = (T + NTe - 1) / NTe;
 #endif
         const int64_t i0 = tile * per, i1 = i0 + per < T ? i0 + per : T;
+#pragma unroll 2                       // two tensors' loads in flight per thread
         for (int64_t i = i0 + threadIdx.x; i < i1; i += LIFETIME_THREADS) {
             if (__ldg(a.ptr + i + 1) <= __ldg(a.ptr + i)) flags |= LF_BAD_PTR;
             const int64_t sz = __ldg(a.size + i);
@@ -316,6 +323,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
         if (tile == 0 && threadIdx.x == 0 && (__ldg(a.ptr) != 0 || __ldg(a.ptr + T) != E)) flags |= LF_BAD_PTR;
     }
     if (!staged) flags |= LF_BAD_PTR;
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
     // ---- walk: this warp's events, one per lane per step
