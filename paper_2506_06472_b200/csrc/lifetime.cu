@@ -256,7 +256,6 @@ struct EvSmem {
     int64_t wglob[LIFETIME_THREADS / 32];
     unsigned long long wflags[LIFETIME_THREADS / 32];
     int64_t prefix;
-    int64_t tile;
 };
 
 __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, EvSmem &sm, int64_t tile,
@@ -275,7 +274,7 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     const int32_t no = (int32_t)(o1 - o0 + 1);
     const bool staged = no <= LT_MAXO;
 
-    // ---- staging; the head mask (zeroed before the first barrier)
+    // ---- staging
     if (((uintptr_t)a.acc & 15) == 0 && ne == LT_TILE) {
         const int4 *q = reinterpret_cast<const int4 *>(a.acc + e0);
         // asynchronous copies: the thread goes on to issue the CSR-slice and
@@ -288,6 +287,10 @@ __device__ __forceinline__ unsigned long long event_tile(const LifetimeArgs &a, 
     } else {
         for (int i = threadIdx.x; i < ne; i += LIFETIME_THREADS) sm.acc[i] = __ldg(a.acc + e0 + i);
     }
+    // the head mask is zeroed here, with the owner loads and the access-column
+    // copies already in flight (the barrier orders it before the atomicOr below)
+    for (int i = threadIdx.x; i < LT_TILE / 32; i += LIFETIME_THREADS) sm.head[i] = 0;
+    __syncthreads();
     if (threadIdx.x == 0) sm.acc[ne] = e1 < E ? __ldg(a.acc + e1) : 0;
     if (staged) {
 #pragma unroll 2                       // two tensors' loads in flight per thread
@@ -484,10 +487,7 @@ k_events(LifetimeArgs a) {
     extern __shared__ __align__(16) unsigned char smraw[];
     EvSmem &sm = *reinterpret_cast<EvSmem *>(smraw);
     const int64_t NTe = lifetime_event_tiles(a.E);
-    for (int i = threadIdx.x; i < LT_TILE / 32; i += blockDim.x) sm.head[i] = 0;
-    if (threadIdx.x == 0) sm.tile = blockIdx.x;
-    __syncthreads();
-    const int64_t tile = sm.tile;
+    const int64_t tile = blockIdx.x;
     const LtWork w = lt_work(a.work, a.N, a.E);
     unsigned long long flags = 0;
     if (tile < NTe) flags = event_tile(a, sm, tile, NTe, w.est, w.egrp, w.owner);
