@@ -174,6 +174,8 @@ __device__ void agg_prefix(const int64_t *st, int64_t sst, const int64_t *grp, i
 // no release on the publishing side, no fence and no second load on the
 // reading side.
 constexpr int GP_SHIFT = 40;
+static_assert((int64_t)LB_GROUP * LT_TILE < (1ll << GP_SHIFT) && LB_GROUP < (1 << (63 - GP_SHIFT)),
+              "a group's period count and tile count fit the packed word");
 __device__ __forceinline__ void agg_publish_packed(int64_t *st, int64_t *grp, int64_t tile, int64_t agg) {
     if ((threadIdx.x & 31) == 0) {
         status_store(st, tile, agg, 1);
