@@ -882,7 +882,7 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
         // Re-derive candidate c's key against the current state (planner.py:147-262):
         // first fit (round 0), refit flags from phase R, host path, benefit
         // from the critical prefix or the cached key; writes st / vkey.
-        auto eval_lane = [&](int64_t c, int32_t cid, int8_t st, const Key &ck, const int4 &rr) -> Key {
+        auto eval_lane = [&](int64_t c, int32_t cid, int8_t st, const Key &ck, const int4 &rr, bool rr_fresh) -> Key {
             Key mine = none;
             if (!(st & ST_GONE)) {
                 int ssd = st & 3, host = (st >> 2) & 3;
@@ -977,11 +977,13 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
                                            __ldg(&a.c_ek[c]), __ldg(&a.c_first[c]), __ldg(&a.c_last[c]),
                                            os + doff, ps, r);
                             *reinterpret_cast<int4 *>(&a.rng[4 * c]) = make_int4(r[0], r[1], r[2], r[3]);
-                        } else if (need) {
-                            // first fit above or phase R: the ranges were just written
+                        } else if (need && !rr_fresh) {
+                            // first fit above: the ranges were just written
                             const int4 r2 = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * c]));
                             r[0] = r2.x; r[1] = r2.y; r[2] = r2.z; r[3] = r2.w;
                         } else {
+                            // cached ranges, or phase R's refit passing the ranges it
+                            // just derived (no reload of what this thread stored)
                             r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
                         }
                         // sum of critical durations over the <= 2 covered ranges: the
@@ -1034,6 +1036,7 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
                 const int2 hx = __ldcg(reinterpret_cast<const int2 *>(&a.hidx[2 * cc]));
                 const int32_t hv = ld_cg(&a.hver[cc]);
                 const int4 rr = __ldcg(reinterpret_cast<const int4 *>(&a.rng[4 * cc]));
+                const int32_t ccid = (int32_t)__ldg(&a.tcand[cc]);     // loaded with the rest, used after the fit
                 const int64_t d0 = dd.x, d1 = dd.y;
                 const int64_t h_off = pl.x, h_pre = pl.y + d1;
                 const int64_t delta = cv[0].n - hv;
@@ -1061,7 +1064,7 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
                         a.hver[cc] = (int32_t)cv[0].n;
                     }
                     const int8_t st2 = (int8_t)((sc & ~3) | (ok ? S_OK : S_DEAD) | ST_REFIT);
-                    const Key kk = eval_lane(cc, (int32_t)__ldg(&a.tcand[cc]), st2, none, make_int4(1, 0, 1, 0));
+                    const Key kk = eval_lane(cc, ccid, st2, none, make_int4(r[0], r[1], r[2], r[3]), ok);
                     if (kbetter(kk, s_rbest[warp])) s_rbest[warp] = kk;
                 }
                 __syncwarp();
@@ -1122,7 +1125,7 @@ __device__ __forceinline__ void plan_loop_body(const PlanArgs &a, const int G, c
                 // queued for a refit by the last commit: phase R owns it this round
                 const bool tile_queued = round > 0 && ld_cg(&a.t_refit[t]) == (int32_t)(round - 1);
                 const bool qround_skip = tile_queued && c >= 0 && ld_cg(&a.qround[c]) == (int32_t)(round - 1);
-                const Key mine = qround_skip ? none : eval_lane(c, cid, st, ck, rr);
+                const Key mine = qround_skip ? none : eval_lane(c, cid, st, ck, rr, false);
                 if (round == 0) {
                     // hulls of the tile's SSD placements (offload, prefetch); the
                     // refit queueing tests a commit's bookings against them
